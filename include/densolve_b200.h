@@ -1,0 +1,197 @@
+/*
+ * densolve_b200.h — C ABI of the B200 (sm_100a) dense linear-solver hot path.
+ *
+ * This is the drop-in boundary for the reference package `densolve`
+ * (/root/reference/pkg/src/densolve).  The reference is pure Python/NumPy; the
+ * seam it designed for an accelerator is the `Backend` op contract
+ * (backends.py:76-200) plus the three solver entry points it drives
+ * (krylov.py:36 cg_solve, krylov.py:75 gmres_solve, direct.py:50
+ * lu_factor_blocked / direct.py:25 lu_factor_unblocked / direct.py:155 lu_solve).
+ * Each entry point below names the reference interface it replaces.  The Python
+ * host layer (paper_1511_07207_b200/) binds these with ctypes, exactly as
+ * INTEGRATION.md shows for the reference side.
+ *
+ * Conventions (all entry points):
+ *  - return an int status (DS_OK == 0); on failure ds_last_error() returns a
+ *    thread-local message.  No C++ exception crosses the ABI.
+ *  - matrices are column-major ("F-order", core.py:1-6) with a leading
+ *    dimension; vectors are contiguous.  dtype is DS_F32 or DS_F64 and every
+ *    operand of one call shares it (core.py:50-58).
+ *  - pointers named d_* are DEVICE pointers (cudaMalloc'd by ds_malloc, or any
+ *    device allocation in the same CUDA context); h_* are HOST pointers.
+ *  - every call is ordered on the context's stream; calls that return host
+ *    scalars or host arrays synchronise that stream before returning.
+ *  - status codes map 1:1 onto the reference exceptions (core.py:17-42).
+ */
+#ifndef DENSOLVE_B200_H
+#define DENSOLVE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+/* ---- status codes (core.py:17-42) ------------------------------------- */
+#define DS_OK 0
+#define DS_EDIM 1       /* DimensionError       core.py:21  */
+#define DS_EPREC 2      /* PrecisionError       core.py:25  */
+#define DS_EDEGRHS 3    /* DegenerateRhsError   core.py:29  */
+#define DS_ESINGULAR 4  /* SingularMatrixError  core.py:33  */
+#define DS_ENOTSPD 5    /* NotSpdError          core.py:37  */
+#define DS_EINVAL 6     /* ValueError (bad config / argument) */
+#define DS_ECUDA 7      /* RuntimeError: CUDA failure */
+#define DS_ENOMEM 8     /* MemoryError: device allocation failed */
+
+/* ---- dtypes (core.py:14 SUPPORTED_DTYPES) ------------------------------ */
+#define DS_F32 0
+#define DS_F64 1
+
+/* ---- orthogonalisation (core.py:175 SolverConfig.orthogonalization) ---- */
+#define DS_ORTH_MODIFIED 0  /* "modified": fused CGS2 (CGS + one reorthogonalisation) */
+#define DS_ORTH_CLASSICAL 1 /* "classical": single-pass CGS, krylov.py:134-138 */
+
+/* ---- GMRES breakdown tags (krylov.py:175) ------------------------------ */
+#define DS_BREAKDOWN_NONE 0
+#define DS_BREAKDOWN_HAPPY 1 /* "happy-breakdown" */
+
+typedef struct ds_ctx ds_ctx;
+
+/* Result of an iterative solve; mirrors SolveReport (core.py:193-201).  The
+ * residual history and restart cycle list are written to caller arrays. */
+typedef struct ds_solve_info {
+  int32_t converged;                /* SolveReport.converged */
+  int32_t breakdown;                /* DS_BREAKDOWN_*        */
+  int64_t iterations;               /* SolveReport.iterations */
+  double final_relative_residual;   /* SolveReport.final_relative_residual */
+  int64_t history_len;              /* entries written to h_hist */
+  int64_t cycles_len;               /* entries written to h_cycles (GMRES) */
+  int64_t error_index;              /* NotSpdError / SingularMatrixError detail, else -1 */
+  double error_value;               /* e.g. the offending p'Ap (krylov.py:57-58) */
+  int64_t kernel_launches;          /* device kernels launched by this call */
+  int64_t residual_evals;           /* GMRES: evaluations of r = b - A x (krylov.py:104) */
+} ds_solve_info;
+
+/* GMRES workspace sink (krylov.py:80-81,168-169): called once per restart
+ * cycle with HOST copies of V (n x (m+1), F-order) and the pre-rotation
+ * Hessenberg Hraw ((m+1) x m, F-order), the inner-step count and beta. */
+typedef void (*ds_sink_fn)(void* user, const void* h_V, const void* h_Hraw, int64_t inner,
+                           double beta);
+
+/* ---- context, memory, staging (the Backend.stage_in/stage_out seam,
+ *      backends.py:94-100) ---------------------------------- */
+const char* ds_last_error(void);
+const char* ds_version(void);
+int ds_device_count(int* out);
+int ds_ctx_create(int device, ds_ctx** out);
+int ds_ctx_destroy(ds_ctx* ctx);
+int ds_ctx_set_stream(ds_ctx* ctx, void* cuda_stream); /* NULL -> library-owned stream */
+int ds_ctx_synchronize(ds_ctx* ctx);
+int ds_ctx_kernel_launches(ds_ctx* ctx, int64_t* out); /* running launch counter */
+int ds_malloc(ds_ctx* ctx, size_t bytes, void** d_out);
+int ds_free(ds_ctx* ctx, void* d_ptr);
+int ds_host_alloc(size_t bytes, void** h_out); /* page-locked host memory */
+int ds_host_free(void* h_ptr);
+int ds_host_register(void* h_ptr, size_t bytes); /* pin an existing host buffer */
+int ds_host_unregister(void* h_ptr);
+int ds_memcpy_h2d(ds_ctx* ctx, void* d_dst, const void* h_src, size_t bytes);
+int ds_memcpy_d2h(ds_ctx* ctx, void* h_dst, const void* d_src, size_t bytes);
+int ds_memcpy_d2d(ds_ctx* ctx, void* d_dst, const void* d_src, size_t bytes);
+int ds_memset(ds_ctx* ctx, void* d_dst, int value, size_t bytes);
+/* Copy a host matrix into a column-major device matrix with leading dimension
+ * ld_dev.  order 0 = host is F-order with leading dimension ld_host, 1 = host
+ * is C-order with row stride ld_host (transposed on device).  Replaces the
+ * implicit np.asfortranarray of core.py:82-87 / direct.py:61. */
+int ds_upload_matrix(ds_ctx* ctx, int dtype, const void* h_src, int64_t rows, int64_t cols,
+                     int64_t ld_host, int order, void* d_dst, int64_t ld_dev);
+int ds_download_matrix(ds_ctx* ctx, int dtype, const void* d_src, int64_t rows, int64_t cols,
+                       int64_t ld_dev, void* h_dst, int64_t ld_host);
+
+/* ---- Backend op contract (backends.py:104-200); device operands -------- */
+/* axpy: d_out = d_y + alpha * d_x            (backends.py:104-107) */
+int ds_axpy(ds_ctx* ctx, int dtype, int64_t n, double alpha, const void* d_x, const void* d_y,
+            void* d_out);
+/* dot: *h_result = x . y                     (backends.py:109-112) */
+int ds_dot(ds_ctx* ctx, int dtype, int64_t n, const void* d_x, const void* d_y, double* h_result);
+/* nrm2: overflow-safe 2-norm                 (backends.py:114-122) */
+int ds_nrm2(ds_ctx* ctx, int dtype, int64_t n, const void* d_x, double* h_result);
+/* scal: d_out = alpha * d_x                  (backends.py:124-126) */
+int ds_scal(ds_ctx* ctx, int dtype, int64_t n, double alpha, const void* d_x, void* d_out);
+/* iamax: first index of max |x|              (backends.py:128-132) */
+int ds_iamax(ds_ctx* ctx, int dtype, int64_t n, const void* d_x, int64_t* h_result);
+/* gemv: d_y = A x, A m x n column-major     (backends.py:136-142) */
+int ds_gemv(ds_ctx* ctx, int dtype, int64_t m, int64_t n, const void* d_A, int64_t lda,
+            const void* d_x, void* d_y);
+/* ger: d_out = A + alpha x y^T               (backends.py:144-156); d_out may alias d_A */
+int ds_ger(ds_ctx* ctx, int dtype, int64_t m, int64_t n, const void* d_A, int64_t lda,
+           double alpha, const void* d_x, const void* d_y, void* d_out, int64_t ldo);
+/* gemm: d_out = beta C + alpha A B           (backends.py:160-174, 234-252); d_out may alias C */
+int ds_gemm(ds_ctx* ctx, int dtype, int64_t m, int64_t n, int64_t k, double alpha,
+            const void* d_A, int64_t lda, const void* d_B, int64_t ldb, double beta,
+            const void* d_C, int64_t ldc, void* d_out, int64_t ldo);
+/* trsm_lower_unit: Z = L^-1 B, L unit lower b x b (backends.py:176-186); Z may alias B */
+int ds_trsm_lower_unit(ds_ctx* ctx, int dtype, int64_t b, int64_t m, const void* d_L, int64_t ldl,
+                       const void* d_B, int64_t ldb, void* d_Z, int64_t ldz);
+/* trsm_upper: Z = U^-1 B, U upper non-unit  (backends.py:188-200); Z may alias B */
+int ds_trsm_upper(ds_ctx* ctx, int dtype, int64_t b, int64_t m, const void* d_U, int64_t ldu,
+                  const void* d_B, int64_t ldb, void* d_Z, int64_t ldz);
+
+/* ---- solvers ----------------------------------------------------------- */
+/* CG: replaces krylov.cg_solve (krylov.py:36-72).  d_x receives x.  h_hist has
+ * room for hist_cap entries (>= max_it + 1).  check_sym runs the symmetry gate
+ * of krylov.py:41-44 on the device. */
+int ds_cg(ds_ctx* ctx, int dtype, int64_t n, const void* d_A, int64_t lda, const void* d_b,
+          const void* d_x0, void* d_x, double tol, int64_t max_it, int check_sym,
+          double* h_hist, int64_t hist_cap, ds_solve_info* info);
+
+/* GMRES(m): replaces krylov.gmres_solve (krylov.py:75-182). */
+int ds_gmres(ds_ctx* ctx, int dtype, int64_t n, const void* d_A, int64_t lda, const void* d_b,
+             const void* d_x0, void* d_x, double tol, int64_t max_it, int64_t restart_m,
+             int orth, double* h_hist, int64_t hist_cap, int64_t* h_cycles, int64_t cycles_cap,
+             ds_sink_fn sink, void* sink_user, ds_solve_info* info);
+
+/* Blocked right-looking LU with partial pivoting, in place on d_A: replaces
+ * direct.lu_factor_blocked (direct.py:50-84); nb == n gives
+ * direct.lu_factor_unblocked (direct.py:25-47).  h_piv receives the pivot
+ * rows (LuFactors.pivots, int64); h_zero_cols (nullable) gets 1 for every
+ * column whose pivot was exactly zero (direct.py:72-74); *h_singular = any. */
+int ds_lu_factor(ds_ctx* ctx, int dtype, int64_t n, void* d_A, int64_t lda, int64_t nb,
+                 int64_t* h_piv, int8_t* h_zero_cols, int32_t* h_singular);
+
+/* Same as ds_lu_factor but with a device-side pivot array (int64) so the
+ * factor/solve pair stays on the device (used by the multi-GPU path). */
+int ds_lu_factor_dev(ds_ctx* ctx, int dtype, int64_t n, void* d_A, int64_t lda, int64_t nb,
+                     int64_t* d_piv, int32_t* h_singular);
+
+/* lu_solve: x = U^-1 L^-1 P b from packed factors (direct.py:155-163 with
+ * core.apply_pivots core.py:94-100).  h_piv is the host pivot array. */
+int ds_lu_solve(ds_ctx* ctx, int dtype, int64_t n, const void* d_LU, int64_t lda,
+                const int64_t* h_piv, const void* d_b, void* d_x);
+
+/* Triangular substitution (direct.py:123-152).  On a zero diagonal returns
+ * DS_ESINGULAR and ds_solve_info-free *h_bad_row = the row the reference
+ * would report. */
+int ds_forward_substitution(ds_ctx* ctx, int dtype, int64_t n, const void* d_L, int64_t ldl,
+                            const void* d_b, void* d_y, int unit_diagonal, int64_t* h_bad_row);
+int ds_backward_substitution(ds_ctx* ctx, int dtype, int64_t n, const void* d_U, int64_t ldu,
+                             const void* d_y, void* d_x, int64_t* h_bad_row);
+
+/* relative_residual ||b - A x|| / ||b|| (core.py:204-210). */
+int ds_relative_residual(ds_ctx* ctx, int dtype, int64_t n, const void* d_A, int64_t lda,
+                         const void* d_x, const void* d_b, double* h_result);
+
+/* max|A - A^T| and max|A| (the SPD gate of krylov.py:41-44). */
+int ds_symmetry_check(ds_ctx* ctx, int dtype, int64_t n, const void* d_A, int64_t lda,
+                      double* h_maxdiff, double* h_amax);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* DENSOLVE_B200_H */

@@ -1,0 +1,1138 @@
+// ds_blas.cu — the Backend op contract on sm_100a (backends.py:104-200).
+//
+// Level-1 ops are single-pass grid-stride kernels with deterministic
+// two-stage reductions; GEMV is the HBM-streaming kernel every Krylov
+// iteration is built on (K1 in SURVEY.md §2b); GEMM is the FP64 DMMA
+// (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4) trailing-update kernel of the
+// blocked LU (K13); TRSM/GER are the panel-side helpers (K12, K10).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "ds_common.cuh"
+#include "ds_kernels.cuh"
+
+namespace ds {
+
+// ============================================================================
+// vector load helpers
+// ============================================================================
+template <typename T, int VEC>
+struct VecT;
+template <>
+struct VecT<double, 2> {
+  using type = double2;
+};
+template <>
+struct VecT<float, 4> {
+  using type = float4;
+};
+template <>
+struct VecT<double, 1> {
+  using type = double;
+};
+template <>
+struct VecT<float, 1> {
+  using type = float;
+};
+
+template <typename V>
+__device__ __forceinline__ V ldg_stream(const V* p) {
+  return __ldg(p);
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ void vec_to_array(const typename VecT<T, VEC>::type& v, T* out);
+template <>
+__device__ __forceinline__ void vec_to_array<double, 2>(const double2& v, double* o) {
+  o[0] = v.x;
+  o[1] = v.y;
+}
+template <>
+__device__ __forceinline__ void vec_to_array<float, 4>(const float4& v, float* o) {
+  o[0] = v.x;
+  o[1] = v.y;
+  o[2] = v.z;
+  o[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void vec_to_array<double, 1>(const double& v, double* o) {
+  o[0] = v;
+}
+template <>
+__device__ __forceinline__ void vec_to_array<float, 1>(const float& v, float* o) {
+  o[0] = v;
+}
+
+// ============================================================================
+// GEMV  (Backend.gemv, backends.py:136-142; call sites krylov.py:47,55,104,128,167)
+// ============================================================================
+constexpr int kGemvThreads = 256;
+
+GemvPlan gemv_plan(ds_ctx* ctx, int64_t m, int64_t n, size_t elem) {
+  GemvPlan p;
+  p.m = m;
+  p.n = n;
+  const int vec = elem == 8 ? 2 : 4;
+  p.rows_per_cta = kGemvThreads * vec;
+  p.rowtiles = ceil_div(std::max<int64_t>(m, 1), p.rows_per_cta);
+  // aim for ~8 CTAs per SM in flight across several waves; chunk >= 64 columns
+  const int64_t target = (int64_t)ctx->num_sms * 16;
+  int64_t nch = std::max<int64_t>(1, target / p.rowtiles);
+  int64_t chunk = ceil_div(std::max<int64_t>(n, 1), nch);
+  chunk = std::max<int64_t>(chunk, 64);
+  chunk = std::min<int64_t>(chunk, 2048);
+  chunk = ceil_div(chunk, 8) * 8;
+  p.chunk = chunk;
+  p.nchunks = ceil_div(std::max<int64_t>(n, 1), chunk);
+  p.part_bytes = (size_t)p.nchunks * (size_t)std::max<int64_t>(m, 1) * sizeof(double);
+  return p;
+}
+
+template <typename T, int VEC, int UNR>
+__global__ void __launch_bounds__(kGemvThreads)
+    gemv_partial_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+                        const T* __restrict__ x, int64_t chunk, double* __restrict__ part,
+                        Gate gate) {
+  if (gated(gate)) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* xs = reinterpret_cast<T*>(smem_raw);
+  const int64_t c0 = (int64_t)blockIdx.y * chunk;
+  const int64_t cn = min(chunk, n - c0);
+  for (int64_t j = threadIdx.x; j < cn; j += blockDim.x) xs[j] = x[c0 + j];
+  __syncthreads();
+  using V = typename VecT<T, VEC>::type;
+  const int64_t r0 = (int64_t)blockIdx.x * (kGemvThreads * VEC) + (int64_t)threadIdx.x * VEC;
+  if (r0 >= m) return;
+  double acc[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) acc[e] = 0.0;
+  const T* a = A + c0 * lda + r0;
+  if (r0 + VEC <= m) {
+    int64_t j = 0;
+    for (; j + UNR <= cn; j += UNR) {
+      V v[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) v[u] = ldg_stream(reinterpret_cast<const V*>(a + (j + u) * lda));
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        T t[VEC];
+        vec_to_array<T, VEC>(v[u], t);
+        const double xv = (double)xs[j + u];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[e] = fma((double)t[e], xv, acc[e]);
+      }
+    }
+    for (; j < cn; ++j) {
+      V v = ldg_stream(reinterpret_cast<const V*>(a + j * lda));
+      T t[VEC];
+      vec_to_array<T, VEC>(v, t);
+      const double xv = (double)xs[j];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[e] = fma((double)t[e], xv, acc[e]);
+    }
+  } else {
+    // ragged row tail (m not a multiple of VEC)
+    for (int64_t j = 0; j < cn; ++j) {
+      const double xv = (double)xs[j];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        if (r0 + e < m) acc[e] = fma((double)__ldg(a + j * lda + e), xv, acc[e]);
+    }
+  }
+  double* out = part + (int64_t)blockIdx.y * m + r0;
+#pragma unroll
+  for (int e = 0; e < VEC; ++e)
+    if (r0 + e < m) out[e] = acc[e];
+}
+
+constexpr int kRedThreads = 256;
+
+template <typename T, int EPI>
+__global__ void __launch_bounds__(kRedThreads)
+    gemv_reduce_kernel(const double* __restrict__ part, int64_t m, int64_t nchunks, T* y,
+                       const T* __restrict__ v, double* __restrict__ red, Gate gate) {
+  if (gated(gate)) return;
+  __shared__ double sm[64];
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double s = 0.0;
+  if (i < m) {
+    for (int64_t c = 0; c < nchunks; ++c) s += part[c * m + i];
+  }
+  const T yi = (T)s;
+  if (EPI == EPI_STORE) {
+    if (i < m) y[i] = yi;
+  } else if (EPI == EPI_DOT) {
+    double d = 0.0;
+    if (i < m) {
+      y[i] = yi;
+      d = (double)v[i] * (double)yi;
+    }
+    d = block_sum(d, sm);
+    if (threadIdx.x == 0) red[blockIdx.x] = d;
+  } else if (EPI == EPI_RESID) {
+    // r = axpy(-1, A x, b) = b - A x  (krylov.py:47,104: one rounding, the -1 is exact)
+    Ssq q{0.0, 0.0};
+    double p2 = 0.0;
+    if (i < m) {
+      const T r = sub_rn(v[i], yi);
+      y[i] = r;
+      q = ssq_add(q, (double)r);
+      p2 = (double)r * (double)r;
+    }
+    Ssq b = block_ssq(q, sm);
+    p2 = block_sum(p2, sm);
+    if (threadIdx.x == 0) {
+      red[2 * blockIdx.x] = b.scale;
+      red[2 * blockIdx.x + 1] = b.ssq;
+      red[2 * gridDim.x + blockIdx.x] = p2;
+    }
+  } else if (EPI == EPI_AXPY_INTO) {
+    // x = axpy(1.0, V y, x) = x + 1.0*(V y)   (krylov.py:167)
+    if (i < m) y[i] = add_rn(y[i], yi);
+  }
+}
+
+template <typename T>
+int gemv_launch(ds_ctx* ctx, const GemvPlan& p, const T* A, int64_t lda, const T* x, T* y,
+                double* part, GemvEpi epi, const T* v, double* red, int* red_blocks,
+                Gate stop) {
+  const int64_t m = p.m, n = p.n;
+  const int rblocks = (int)ceil_div(std::max<int64_t>(m, 1), kRedThreads);
+  if (red_blocks) *red_blocks = rblocks;
+  if (m == 0) return DS_OK;
+  if (n == 0) {
+    // A x = 0: run the reduce kernel over a zeroed partial row
+    DS_CUDA(cudaMemsetAsync(part, 0, (size_t)m * sizeof(double), ctx->stream));
+  } else {
+    dim3 grid((unsigned)p.rowtiles, (unsigned)p.nchunks);
+    const size_t smem = (size_t)p.chunk * sizeof(T);
+    constexpr int VEC = sizeof(T) == 8 ? 2 : 4;
+    const bool aligned = (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (lda % VEC == 0);
+    if (aligned) {
+      gemv_partial_kernel<T, VEC, 8>
+          <<<grid, kGemvThreads, smem, ctx->stream>>>(A, lda, m, n, x, p.chunk, part, stop);
+    } else {
+      dim3 g1((unsigned)ceil_div(m, kGemvThreads), (unsigned)p.nchunks);
+      gemv_partial_kernel<T, 1, 8>
+          <<<g1, kGemvThreads, smem, ctx->stream>>>(A, lda, m, n, x, p.chunk, part, stop);
+    }
+    count_launch(ctx);
+    DS_CHECK_LAUNCH();
+  }
+  const int64_t nch = n == 0 ? 1 : p.nchunks;
+  switch (epi) {
+    case EPI_STORE:
+      gemv_reduce_kernel<T, EPI_STORE>
+          <<<rblocks, kRedThreads, 0, ctx->stream>>>(part, m, nch, y, v, red, stop);
+      break;
+    case EPI_DOT:
+      gemv_reduce_kernel<T, EPI_DOT>
+          <<<rblocks, kRedThreads, 0, ctx->stream>>>(part, m, nch, y, v, red, stop);
+      break;
+    case EPI_RESID:
+      gemv_reduce_kernel<T, EPI_RESID>
+          <<<rblocks, kRedThreads, 0, ctx->stream>>>(part, m, nch, y, v, red, stop);
+      break;
+    case EPI_AXPY_INTO:
+      gemv_reduce_kernel<T, EPI_AXPY_INTO>
+          <<<rblocks, kRedThreads, 0, ctx->stream>>>(part, m, nch, y, v, red, stop);
+      break;
+  }
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+
+template int gemv_launch<double>(ds_ctx*, const GemvPlan&, const double*, int64_t, const double*,
+                                 double*, double*, GemvEpi, const double*, double*, int*,
+                                 Gate);
+template int gemv_launch<float>(ds_ctx*, const GemvPlan&, const float*, int64_t, const float*,
+                                float*, double*, GemvEpi, const float*, double*, int*, Gate);
+
+// ============================================================================
+// level-1 reductions
+// ============================================================================
+int reduce_grid(ds_ctx* ctx, int64_t n) {
+  int64_t want = ceil_div(std::max<int64_t>(n, 1), (int64_t)kRedThreads * 4);
+  return (int)std::min<int64_t>(want, (int64_t)ctx->num_sms * 4);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+    dot_kernel(int64_t n, const T* __restrict__ x, const T* __restrict__ y, double* red) {
+  __shared__ double sm[32];
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    s = fma((double)x[i], (double)y[i], s);
+  s = block_sum(s, sm);
+  if (threadIdx.x == 0) red[blockIdx.x] = s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+    ssq_kernel(int64_t n, const T* __restrict__ x, double* red) {
+  __shared__ double sm[64];
+  Ssq q{0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    q = ssq_add(q, (double)x[i]);
+  q = block_ssq(q, sm);
+  if (threadIdx.x == 0) {
+    red[2 * blockIdx.x] = q.scale;
+    red[2 * blockIdx.x + 1] = q.ssq;
+  }
+}
+
+__global__ void finish_sum_kernel(const double* red, int nblk, double* out) {
+  __shared__ double sm[32];
+  double s = reduce_sum_partials(red, nblk, sm);
+  if (threadIdx.x == 0) out[0] = s;
+}
+
+__global__ void finish_ssq_kernel(const double* red, int nblk, double* out) {
+  __shared__ double sm[64];
+  Ssq q{0.0, 0.0};
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) q = ssq_merge(q, Ssq{red[2 * i], red[2 * i + 1]});
+  q = block_ssq(q, sm);
+  if (threadIdx.x == 0) out[0] = ssq_norm(q.scale, q.ssq);
+}
+
+template <typename T>
+int dot_launch(ds_ctx* ctx, int64_t n, const T* x, const T* y, double* red, int* nblk) {
+  int g = reduce_grid(ctx, n);
+  *nblk = g;
+  dot_kernel<T><<<g, kRedThreads, 0, ctx->stream>>>(n, x, y, red);
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+template <typename T>
+int ssq_launch(ds_ctx* ctx, int64_t n, const T* x, double* red, int* nblk) {
+  int g = reduce_grid(ctx, n);
+  *nblk = g;
+  ssq_kernel<T><<<g, kRedThreads, 0, ctx->stream>>>(n, x, red);
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+int finish_sum(ds_ctx* ctx, const double* red, int nblk, double* out) {
+  finish_sum_kernel<<<1, kRedThreads, 0, ctx->stream>>>(red, nblk, out);
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+int finish_ssq(ds_ctx* ctx, const double* red, int nblk, double* out) {
+  finish_ssq_kernel<<<1, kRedThreads, 0, ctx->stream>>>(red, nblk, out);
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+template int dot_launch<double>(ds_ctx*, int64_t, const double*, const double*, double*, int*);
+template int dot_launch<float>(ds_ctx*, int64_t, const float*, const float*, double*, int*);
+template int ssq_launch<double>(ds_ctx*, int64_t, const double*, double*, int*);
+template int ssq_launch<float>(ds_ctx*, int64_t, const float*, double*, int*);
+
+// iamax: first index of the maximum |x|; NaN wins (first NaN), ties -> lowest
+// index (np.argmax(np.abs(x)), backends.py:128-132).
+__device__ __forceinline__ bool iamax_better(double av, int64_t ai, double bv, int64_t bi) {
+  const bool an = av != av, bn = bv != bv;
+  if (an || bn) {
+    if (an && bn) return ai < bi;
+    return an;
+  }
+  if (av != bv) return av > bv;
+  return ai < bi;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads)
+    iamax_kernel(int64_t n, const T* __restrict__ x, double* red_v, int64_t* red_i) {
+  __shared__ double sv[32];
+  __shared__ int64_t si[32];
+  double bv = -1.0;
+  int64_t bi = INT64_MAX;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = fabs((double)x[i]);
+    if (iamax_better(v, i, bv, bi)) {
+      bv = v;
+      bi = i;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (iamax_better(ov, oi, bv, bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    sv[wid] = bv;
+    si[wid] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (iamax_better(sv[w], si[w], bv, bi)) {
+        bv = sv[w];
+        bi = si[w];
+      }
+    red_v[blockIdx.x] = bv;
+    red_i[blockIdx.x] = bi;
+  }
+}
+
+__global__ void iamax_finish_kernel(const double* red_v, const int64_t* red_i, int nblk,
+                                    int64_t* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double bv = -1.0;
+    int64_t bi = INT64_MAX;
+    for (int b = 0; b < nblk; ++b)
+      if (iamax_better(red_v[b], red_i[b], bv, bi)) {
+        bv = red_v[b];
+        bi = red_i[b];
+      }
+    out[0] = bi;
+  }
+}
+
+// ============================================================================
+// elementwise ops (NumPy rounding: alpha cast to the array dtype, NEP 50)
+// ============================================================================
+template <typename T>
+__global__ void axpy_kernel(int64_t n, T alpha, const T* __restrict__ x, const T* y, T* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = add_rn(y[i], mul_rn(alpha, x[i]));
+}
+template <typename T>
+__global__ void scal_kernel(int64_t n, T alpha, const T* x, T* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = mul_rn(alpha, x[i]);
+}
+
+static int ew_grid(ds_ctx* ctx, int64_t n) {
+  int64_t want = ceil_div(std::max<int64_t>(n, 1), 256);
+  return (int)std::min<int64_t>(want, (int64_t)ctx->num_sms * 8);
+}
+
+template <typename T>
+int axpy_launch(ds_ctx* ctx, int64_t n, double alpha, const T* x, const T* y, T* out) {
+  if (n == 0) return DS_OK;
+  axpy_kernel<T><<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, (T)alpha, x, y, out);
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+template <typename T>
+int scal_launch(ds_ctx* ctx, int64_t n, double alpha, const T* x, T* out) {
+  if (n == 0) return DS_OK;
+  scal_kernel<T><<<ew_grid(ctx, n), 256, 0, ctx->stream>>>(n, (T)alpha, x, out);
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+template int axpy_launch<double>(ds_ctx*, int64_t, double, const double*, const double*, double*);
+template int axpy_launch<float>(ds_ctx*, int64_t, double, const float*, const float*, float*);
+template int scal_launch<double>(ds_ctx*, int64_t, double, const double*, double*);
+template int scal_launch<float>(ds_ctx*, int64_t, double, const float*, float*);
+
+// ============================================================================
+// GER: out = A + alpha * outer(x, y)   (backends.py:144-156)
+//   outer element rounded, times alpha rounded, then added: three roundings,
+//   exactly NumPy's `A + alpha * np.outer(x, y)`.
+// ============================================================================
+template <typename T>
+__global__ void ger_kernel(int64_t m, int64_t n, const T* A, int64_t lda, T alpha,
+                           const T* __restrict__ x, const T* __restrict__ y, T* out, int64_t ldo) {
+  const int64_t total = m * n;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % m, j = t / m;
+    out[i + j * ldo] = add_rn(A[i + j * lda], mul_rn(alpha, mul_rn(x[i], y[j])));
+  }
+}
+template <typename T>
+int ger_launch(ds_ctx* ctx, int64_t m, int64_t n, const T* A, int64_t lda, double alpha,
+               const T* x, const T* y, T* out, int64_t ldo) {
+  if (m == 0 || n == 0) return DS_OK;
+  ger_kernel<T><<<ew_grid(ctx, m * n), 256, 0, ctx->stream>>>(m, n, A, lda, (T)alpha, x, y, out,
+                                                              ldo);
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+template int ger_launch<double>(ds_ctx*, int64_t, int64_t, const double*, int64_t, double,
+                                const double*, const double*, double*, int64_t);
+template int ger_launch<float>(ds_ctx*, int64_t, int64_t, const float*, int64_t, double,
+                               const float*, const float*, float*, int64_t);
+
+// ============================================================================
+// symmetry gate (krylov.py:41-44): max|A - A^T| (difference rounded in T, as
+// NumPy's A - A.T) and max|A|, over upper-triangular 32x32 tile pairs.
+// ============================================================================
+template <typename T>
+__global__ void __launch_bounds__(256)
+    symcheck_kernel(int64_t n, const T* __restrict__ A, int64_t lda, double* red) {
+  __shared__ T tl[32][33];
+  __shared__ T tu[32][33];
+  __shared__ double sm[32];
+  const int64_t nt = ceil_div(n, 32);
+  const int64_t npairs = nt * (nt + 1) / 2;
+  double dmax = 0.0, amax = 0.0;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int64_t p = blockIdx.x; p < npairs; p += gridDim.x) {
+    // p -> (bi, bj) with bi <= bj, row-major over the upper triangle
+    int64_t bi = (int64_t)((2.0 * nt + 1.0 - sqrt((2.0 * nt + 1.0) * (2.0 * nt + 1.0) - 8.0 * p)) / 2.0);
+    if (bi < 0) bi = 0;
+    while (bi > 0 && bi * nt - bi * (bi - 1) / 2 > p) --bi;
+    while ((bi + 1) * nt - (bi + 1) * bi / 2 <= p) ++bi;
+    const int64_t bj = bi + (p - (bi * nt - bi * (bi - 1) / 2));
+    const int64_t r0 = bi * 32, c0 = bj * 32;
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+      const int64_t r = r0 + tx, c = c0 + k;  // tile (bi,bj): element (r, c)
+      tl[k][tx] = (r < n && c < n) ? A[r + c * lda] : T(0);
+      const int64_t r2 = c0 + tx, c2 = r0 + k;  // tile (bj,bi): element (r2, c2)
+      tu[k][tx] = (r2 < n && c2 < n) ? A[r2 + c2 * lda] : T(0);
+    }
+    __syncthreads();
+    for (int k = ty; k < 32; k += 8) {
+      // element (r0+tx, c0+k) vs its transpose (c0+k, r0+tx) = tu[tx][k]
+      const T a = tl[k][tx], b = tu[tx][k];
+      dmax = nanmax(dmax, fabs((double)sub_rn(a, b)));
+      amax = nanmax(amax, fabs((double)a));
+      amax = nanmax(amax, fabs((double)tu[k][tx]));
+    }
+  }
+  dmax = block_nanmax(dmax, sm);
+  amax = block_nanmax(amax, sm);
+  if (threadIdx.x == 0) {
+    red[2 * blockIdx.x] = dmax;
+    red[2 * blockIdx.x + 1] = amax;
+  }
+}
+
+template <typename T>
+int symcheck_launch(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, double* red, int* nblk) {
+  const int64_t nt = ceil_div(n, 32);
+  const int64_t npairs = nt * (nt + 1) / 2;
+  int g = (int)std::min<int64_t>(npairs, (int64_t)ctx->num_sms * 8);
+  *nblk = g;
+  symcheck_kernel<T><<<g, 256, 0, ctx->stream>>>(n, A, lda, red);
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+template int symcheck_launch<double>(ds_ctx*, int64_t, const double*, int64_t, double*, int*);
+template int symcheck_launch<float>(ds_ctx*, int64_t, const float*, int64_t, double*, int*);
+
+__global__ void finish_max2_kernel(const double* red, int nblk, double* out) {
+  __shared__ double sm[32];
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    a = nanmax(a, red[2 * i]);
+    b = nanmax(b, red[2 * i + 1]);
+  }
+  a = block_nanmax(a, sm);
+  b = block_nanmax(b, sm);
+  if (threadIdx.x == 0) {
+    out[0] = a;
+    out[1] = b;
+  }
+}
+
+// ============================================================================
+// GEMM — FP64 on the DMMA tensor pipe.  out = beta*C + alpha*(A B).
+//   CTA tile 128x64, 4 warps (2x2) of 64x32, BK=16 k-slab, 3-stage cp.async
+//   pipeline, mma.sync.m8n8k4.row.col.f64 (native DMMA.8x8x4; the only FP64
+//   tensor-core instruction on sm_100a — tcgen05 has no kind::f64).
+// ============================================================================
+namespace gemm64 {
+constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3, THREADS = 128;
+constexpr int LDA_S = BM + 4;  // smem row (one k) of the A slab, +4 doubles: conflict-free frags
+constexpr int LDB_S = BK + 4;  // smem row (one n) of the B slab
+constexpr int A_STAGE = BK * LDA_S;
+constexpr int B_STAGE = BN * LDB_S;
+constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
+}  // namespace gemm64
+
+__device__ __forceinline__ void cp_async_16(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_8(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <bool VEC16>
+__device__ __forceinline__ void gemm64_load_stage(double* As, double* Bs, const double* A,
+                                                  int64_t lda, const double* B, int64_t ldb,
+                                                  int64_t m, int64_t n, int64_t k, int64_t m0,
+                                                  int64_t n0, int64_t k0) {
+  using namespace gemm64;
+  const int tid = threadIdx.x;
+  if (VEC16) {
+    // A slab: BK columns x BM rows, 2 doubles per 16 B chunk -> BK*BM/2 chunks
+#pragma unroll
+    for (int it = 0; it < (BK * BM / 2) / THREADS; ++it) {
+      const int c = tid + it * THREADS;
+      const int kk = c / (BM / 2), mm = (c % (BM / 2)) * 2;
+      const int64_t gr = m0 + mm, gk = k0 + kk;
+      int bytes = 0;
+      if (gk < k) bytes = gr + 1 < m ? 16 : (gr < m ? 8 : 0);
+      const double* src = bytes ? A + gk * lda + gr : A;
+      cp_async_16(As + kk * LDA_S + mm, src, bytes);
+    }
+    // B slab: BN columns x BK rows
+#pragma unroll
+    for (int it = 0; it < (BK * BN / 2) / THREADS; ++it) {
+      const int c = tid + it * THREADS;
+      const int nn = c / (BK / 2), kk = (c % (BK / 2)) * 2;
+      const int64_t gk = k0 + kk, gc = n0 + nn;
+      int bytes = 0;
+      if (gc < n) bytes = gk + 1 < k ? 16 : (gk < k ? 8 : 0);
+      const double* src = bytes ? B + gc * ldb + gk : B;
+      cp_async_16(Bs + nn * LDB_S + kk, src, bytes);
+    }
+  } else {
+#pragma unroll 4
+    for (int it = 0; it < (BK * BM) / THREADS; ++it) {
+      const int c = tid + it * THREADS;
+      const int kk = c / BM, mm = c % BM;
+      const int64_t gr = m0 + mm, gk = k0 + kk;
+      const bool ok = gk < k && gr < m;
+      cp_async_8(As + kk * LDA_S + mm, ok ? A + gk * lda + gr : A, ok ? 8 : 0);
+    }
+#pragma unroll 4
+    for (int it = 0; it < (BK * BN) / THREADS; ++it) {
+      const int c = tid + it * THREADS;
+      const int nn = c / BK, kk = c % BK;
+      const int64_t gk = k0 + kk, gc = n0 + nn;
+      const bool ok = gc < n && gk < k;
+      cp_async_8(Bs + nn * LDB_S + kk, ok ? B + gc * ldb + gk : B, ok ? 8 : 0);
+    }
+  }
+}
+
+template <bool VEC16, int MODE /*0: general, 1: out = C - AB*/>
+__global__ void __launch_bounds__(gemm64::THREADS, 2)
+    gemm64_kernel(int64_t m, int64_t n, int64_t k, double alpha, const double* __restrict__ A,
+                  int64_t lda, const double* __restrict__ B, int64_t ldb, double beta,
+                  const double* C, int64_t ldc, double* out, int64_t ldo) {
+  using namespace gemm64;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* As = reinterpret_cast<double*>(smem_raw);
+  double* Bs = As + STAGES * A_STAGE;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+  const int g = lane >> 2, t = lane & 3;
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int64_t ktiles = ceil_div(k, BK);
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ktiles)
+      gemm64_load_stage<VEC16>(As + s * A_STAGE, Bs + s * B_STAGE, A, lda, B, ldb, m, n, k, m0, n0,
+                               (int64_t)s * BK);
+    cp_async_commit();
+  }
+  for (int64_t kt = 0; kt < ktiles; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    // prefetch slab kt + STAGES - 1 into the stage freed at iteration kt - 1
+    const int64_t pf = kt + STAGES - 1;
+    if (pf < ktiles) {
+      const int s = (int)(pf % STAGES);
+      gemm64_load_stage<VEC16>(As + s * A_STAGE, Bs + s * B_STAGE, A, lda, B, ldb, m, n, k, m0, n0,
+                               pf * BK);
+    }
+    cp_async_commit();
+    const int s = (int)(kt % STAGES);
+    const double* as = As + s * A_STAGE + wm * 64 + g;
+    const double* bs = Bs + s * B_STAGE + (wn * 32 + g) * LDB_S + t;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double a[8], b[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = as[(kk + t) * LDA_S + i * 8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = bs[j * 8 * LDB_S + kk];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  cp_async_wait<0>();
+  // epilogue: out = beta*C + alpha*acc (NumPy rounding, backends.py:244); MODE 1 = C - acc
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t r = m0 + wm * 64 + i * 8 + g;
+    if (r >= m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t c = n0 + wn * 32 + j * 8 + 2 * t + e;
+        if (c >= n) continue;
+        const double v = acc[i][j][e];
+        double o;
+        if (MODE == 1) {
+          o = __dsub_rn(C[r + c * ldc], v);
+        } else {
+          const double cb = beta == 0.0 ? 0.0 : __dmul_rn(beta, C[r + c * ldc]);
+          o = __dadd_rn(cb, __dmul_rn(alpha, v));
+        }
+        out[r + c * ldo] = o;
+      }
+    }
+  }
+}
+
+// FP32 GEMM (FFMA, fp32 accumulation like sgemm): 64x64 tile, 256 threads, 4x4 per thread.
+template <int MODE>
+__global__ void __launch_bounds__(256)
+    gemm32_kernel(int64_t m, int64_t n, int64_t k, float alpha, const float* __restrict__ A,
+                  int64_t lda, const float* __restrict__ B, int64_t ldb, float beta, const float* C,
+                  int64_t ldc, float* out, int64_t ldo) {
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t m0 = (int64_t)blockIdx.x * 64, n0 = (int64_t)blockIdx.y * 64;
+  float acc[4][4] = {};
+  for (int64_t k0 = 0; k0 < k; k0 += 16) {
+    for (int c = threadIdx.x; c < 16 * 64; c += 256) {
+      const int kk = c / 64, mm = c % 64;
+      const int64_t gr = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gr < m && gk < k) ? A[gr + gk * lda] : 0.f;
+      const int nn = c / 16, kb = c % 16;
+      const int64_t gc = n0 + nn, gk2 = k0 + kb;
+      Bs[kb][nn] = (gc < n && gk2 < k) ? B[gk2 + gc * ldb] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][tx + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][ty + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t r = m0 + tx + 16 * i, c = n0 + ty + 16 * j;
+      if (r < m && c < n) {
+        float o;
+        if (MODE == 1)
+          o = __fsub_rn(C[r + c * ldc], acc[i][j]);
+        else {
+          const float cb = beta == 0.f ? 0.f : __fmul_rn(beta, C[r + c * ldc]);
+          o = __fadd_rn(cb, __fmul_rn(alpha, acc[i][j]));
+        }
+        out[r + c * ldo] = o;
+      }
+    }
+}
+
+template <>
+int gemm_launch<double>(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha,
+                        const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                        const double* C, int64_t ldc, double* out, int64_t ldo) {
+  using namespace gemm64;
+  if (m == 0 || n == 0) return DS_OK;
+  static bool attr_done = false;
+  if (!attr_done) {
+    DS_CUDA(cudaFuncSetAttribute(gemm64_kernel<true, 0>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    DS_CUDA(cudaFuncSetAttribute(gemm64_kernel<true, 1>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    DS_CUDA(cudaFuncSetAttribute(gemm64_kernel<false, 0>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    DS_CUDA(cudaFuncSetAttribute(gemm64_kernel<false, 1>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    attr_done = true;
+  }
+  dim3 grid((unsigned)ceil_div(m, BM), (unsigned)ceil_div(n, BN));
+  const bool vec = (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(B) % 16 == 0) && (lda % 2 == 0) && (ldb % 2 == 0);
+  const bool sub = (alpha == -1.0 && beta == 1.0);
+  if (k == 0) {
+    // out = beta*C (alpha*0 added)
+    if (vec && sub)
+      gemm64_kernel<true, 1><<<grid, THREADS, SMEM, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb,
+                                                                    beta, C, ldc, out, ldo);
+    else
+      gemm64_kernel<false, 0><<<grid, THREADS, SMEM, ctx->stream>>>(m, n, k, alpha, A, lda, B,
+                                                                     ldb, beta, C, ldc, out, ldo);
+  } else if (vec) {
+    if (sub)
+      gemm64_kernel<true, 1><<<grid, THREADS, SMEM, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb,
+                                                                    beta, C, ldc, out, ldo);
+    else
+      gemm64_kernel<true, 0><<<grid, THREADS, SMEM, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb,
+                                                                    beta, C, ldc, out, ldo);
+  } else {
+    if (sub)
+      gemm64_kernel<false, 1><<<grid, THREADS, SMEM, ctx->stream>>>(m, n, k, alpha, A, lda, B,
+                                                                     ldb, beta, C, ldc, out, ldo);
+    else
+      gemm64_kernel<false, 0><<<grid, THREADS, SMEM, ctx->stream>>>(m, n, k, alpha, A, lda, B,
+                                                                     ldb, beta, C, ldc, out, ldo);
+  }
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+
+template <>
+int gemm_launch<float>(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A,
+                       int64_t lda, const float* B, int64_t ldb, double beta, const float* C,
+                       int64_t ldc, float* out, int64_t ldo) {
+  if (m == 0 || n == 0) return DS_OK;
+  dim3 grid((unsigned)ceil_div(m, 64), (unsigned)ceil_div(n, 64));
+  if (alpha == -1.0 && beta == 1.0)
+    gemm32_kernel<1><<<grid, 256, 0, ctx->stream>>>(m, n, k, (float)alpha, A, lda, B, ldb,
+                                                    (float)beta, C, ldc, out, ldo);
+  else
+    gemm32_kernel<0><<<grid, 256, 0, ctx->stream>>>(m, n, k, (float)alpha, A, lda, B, ldb,
+                                                    (float)beta, C, ldc, out, ldo);
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+
+// ============================================================================
+// TRSM (backends.py:176-200): one thread per right-hand-side column.
+//   lower-unit: z_i = b_i - (L[i,:i] . z[:i])           (stored diagonal ignored)
+//   upper:      z_i = (b_i - U[i,i+1:] . z[i+1:]) / U_ii
+// b <= 64: L staged in shared memory, z in registers (fully unrolled);
+// b > 64: generic path working in place on Z.
+// ============================================================================
+template <typename T>
+__global__ void __launch_bounds__(128)
+    trsm_lower_unit_small(int b, int64_t m, const T* __restrict__ L, int64_t ldl,
+                          const T* __restrict__ B, int64_t ldb, T* Z, int64_t ldz) {
+  __shared__ T Ls[64][65];
+  for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
+    const int i = idx % b, j = idx / b;
+    Ls[i][j] = L[i + (int64_t)j * ldl];
+  }
+  __syncthreads();
+  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= m) return;
+  T z[64];
+#pragma unroll
+  for (int i = 0; i < 64; ++i)
+    if (i < b) z[i] = B[i + col * ldb];
+#pragma unroll
+  for (int i = 1; i < 64; ++i) {
+    if (i < b) {
+      T acc = T(0);
+#pragma unroll
+      for (int j = 0; j < 64; ++j)
+        if (j < i) acc = fma(Ls[i][j], z[j], acc);
+      z[i] = sub_rn(z[i], acc);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 64; ++i)
+    if (i < b) Z[i + col * ldz] = z[i];
+}
+
+template <typename T>
+__global__ void trsm_lower_unit_big(int64_t b, int64_t m, const T* __restrict__ L, int64_t ldl,
+                                    const T* B, int64_t ldb, T* Z, int64_t ldz) {
+  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= m) return;
+  T* z = Z + col * ldz;
+  const T* bb = B + col * ldb;
+  if (z != bb)
+    for (int64_t i = 0; i < b; ++i) z[i] = bb[i];
+  for (int64_t i = 1; i < b; ++i) {
+    T acc = T(0);
+    for (int64_t j = 0; j < i; ++j) acc = fma(L[i + j * ldl], z[j], acc);
+    z[i] = sub_rn(z[i], acc);
+  }
+}
+
+template <typename T>
+__global__ void trsm_upper_kernel(int64_t b, int64_t m, const T* __restrict__ U, int64_t ldu,
+                                  const T* B, int64_t ldb, T* Z, int64_t ldz) {
+  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= m) return;
+  T* z = Z + col * ldz;
+  const T* bb = B + col * ldb;
+  if (z != bb)
+    for (int64_t i = 0; i < b; ++i) z[i] = bb[i];
+  for (int64_t i = b - 1; i >= 0; --i) {
+    T acc = T(0);
+    for (int64_t j = i + 1; j < b; ++j) acc = fma(U[i + j * ldu], z[j], acc);
+    T v = i + 1 < b ? sub_rn(z[i], acc) : z[i];
+    z[i] = div_rn(v, U[i + i * ldu]);
+  }
+}
+
+template <typename T>
+int trsm_lower_unit_launch(ds_ctx* ctx, int64_t b, int64_t m, const T* L, int64_t ldl, const T* B,
+                           int64_t ldb, T* Z, int64_t ldz) {
+  if (b == 0 || m == 0) return DS_OK;
+  if (b <= 64) {
+    trsm_lower_unit_small<T><<<(unsigned)ceil_div(m, 128), 128, 0, ctx->stream>>>(
+        (int)b, m, L, ldl, B, ldb, Z, ldz);
+  } else {
+    trsm_lower_unit_big<T><<<(unsigned)ceil_div(m, 128), 128, 0, ctx->stream>>>(b, m, L, ldl, B,
+                                                                               ldb, Z, ldz);
+  }
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+template <typename T>
+int trsm_upper_launch(ds_ctx* ctx, int64_t b, int64_t m, const T* U, int64_t ldu, const T* B,
+                      int64_t ldb, T* Z, int64_t ldz) {
+  if (b == 0 || m == 0) return DS_OK;
+  trsm_upper_kernel<T><<<(unsigned)ceil_div(m, 128), 128, 0, ctx->stream>>>(b, m, U, ldu, B, ldb,
+                                                                           Z, ldz);
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+template int trsm_lower_unit_launch<double>(ds_ctx*, int64_t, int64_t, const double*, int64_t,
+                                            const double*, int64_t, double*, int64_t);
+template int trsm_lower_unit_launch<float>(ds_ctx*, int64_t, int64_t, const float*, int64_t,
+                                           const float*, int64_t, float*, int64_t);
+template int trsm_upper_launch<double>(ds_ctx*, int64_t, int64_t, const double*, int64_t,
+                                       const double*, int64_t, double*, int64_t);
+template int trsm_upper_launch<float>(ds_ctx*, int64_t, int64_t, const float*, int64_t,
+                                      const float*, int64_t, float*, int64_t);
+
+}  // namespace ds
+
+// ============================================================================
+// extern "C" op contract
+// ============================================================================
+using namespace ds;
+
+namespace {
+struct Scratch {
+  double* red = nullptr;  // reduction partials
+  double* out = nullptr;  // 8 doubles of results
+  int64_t* iout = nullptr;
+};
+int get_scratch(ds_ctx* ctx, size_t red_doubles, Scratch* s) {
+  void* ws = nullptr;
+  DS_TRY(ctx_workspace(ctx, (red_doubles + 16) * sizeof(double) * 2, &ws));
+  s->out = reinterpret_cast<double*>(ws);
+  s->iout = reinterpret_cast<int64_t*>(s->out + 8);
+  s->red = s->out + 16;
+  return DS_OK;
+}
+int fetch(ds_ctx* ctx, void* host, const void* dev, size_t bytes) {
+  DS_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return DS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int ds_axpy(ds_ctx* ctx, int dtype, int64_t n, double alpha, const void* x, const void* y,
+            void* out) {
+  DS_TRY(ctx_begin(ctx));
+  DS_DISPATCH(dtype, T, DS_TRY(axpy_launch<T>(ctx, n, alpha, (const T*)x, (const T*)y, (T*)out)));
+  return DS_OK;
+}
+
+int ds_scal(ds_ctx* ctx, int dtype, int64_t n, double alpha, const void* x, void* out) {
+  DS_TRY(ctx_begin(ctx));
+  DS_DISPATCH(dtype, T, DS_TRY(scal_launch<T>(ctx, n, alpha, (const T*)x, (T*)out)));
+  return DS_OK;
+}
+
+int ds_dot(ds_ctx* ctx, int dtype, int64_t n, const void* x, const void* y, double* result) {
+  DS_TRY(ctx_begin(ctx));
+  Scratch s;
+  DS_TRY(get_scratch(ctx, (size_t)ctx->num_sms * 4, &s));
+  int nblk = 0;
+  DS_DISPATCH(dtype, T, DS_TRY(dot_launch<T>(ctx, n, (const T*)x, (const T*)y, s.red, &nblk)));
+  DS_TRY(finish_sum(ctx, s.red, nblk, s.out));
+  return fetch(ctx, result, s.out, sizeof(double));
+}
+
+int ds_nrm2(ds_ctx* ctx, int dtype, int64_t n, const void* x, double* result) {
+  DS_TRY(ctx_begin(ctx));
+  if (n == 0) {
+    *result = 0.0;
+    return DS_OK;
+  }
+  Scratch s;
+  DS_TRY(get_scratch(ctx, (size_t)ctx->num_sms * 8, &s));
+  int nblk = 0;
+  DS_DISPATCH(dtype, T, DS_TRY(ssq_launch<T>(ctx, n, (const T*)x, s.red, &nblk)));
+  DS_TRY(finish_ssq(ctx, s.red, nblk, s.out));
+  return fetch(ctx, result, s.out, sizeof(double));
+}
+
+int ds_iamax(ds_ctx* ctx, int dtype, int64_t n, const void* x, int64_t* result) {
+  DS_TRY(ctx_begin(ctx));
+  if (n <= 0) {
+    set_error("iamax of empty vector");
+    return DS_EDIM;
+  }
+  Scratch s;
+  DS_TRY(get_scratch(ctx, (size_t)ctx->num_sms * 8, &s));
+  const int g = reduce_grid(ctx, n);
+  int64_t* ri = reinterpret_cast<int64_t*>(s.red + g);
+  DS_DISPATCH(dtype, T,
+              iamax_kernel<T><<<g, kRedThreads, 0, ctx->stream>>>(n, (const T*)x, s.red, ri));
+  iamax_finish_kernel<<<1, 32, 0, ctx->stream>>>(s.red, ri, g, s.iout);
+  count_launch(ctx, 2);
+  DS_CHECK_LAUNCH();
+  return fetch(ctx, result, s.iout, sizeof(int64_t));
+}
+
+int ds_gemv(ds_ctx* ctx, int dtype, int64_t m, int64_t n, const void* A, int64_t lda,
+            const void* x, void* y) {
+  DS_TRY(ctx_begin(ctx));
+  if (m == 0) return DS_OK;
+  const GemvPlan p = gemv_plan(ctx, m, n, dtype_size(dtype));
+  void* ws = nullptr;
+  DS_TRY(ctx_workspace(ctx, p.part_bytes + 4096, &ws));
+  DS_DISPATCH(dtype, T,
+              DS_TRY(gemv_launch<T>(ctx, p, (const T*)A, lda, (const T*)x, (T*)y, (double*)ws,
+                                    EPI_STORE, nullptr, nullptr, nullptr)));
+  return DS_OK;
+}
+
+int ds_ger(ds_ctx* ctx, int dtype, int64_t m, int64_t n, const void* A, int64_t lda, double alpha,
+           const void* x, const void* y, void* out, int64_t ldo) {
+  DS_TRY(ctx_begin(ctx));
+  DS_DISPATCH(dtype, T,
+              DS_TRY(ger_launch<T>(ctx, m, n, (const T*)A, lda, alpha, (const T*)x, (const T*)y,
+                                   (T*)out, ldo)));
+  return DS_OK;
+}
+
+int ds_gemm(ds_ctx* ctx, int dtype, int64_t m, int64_t n, int64_t k, double alpha, const void* A,
+            int64_t lda, const void* B, int64_t ldb, double beta, const void* C, int64_t ldc,
+            void* out, int64_t ldo) {
+  DS_TRY(ctx_begin(ctx));
+  DS_DISPATCH(dtype, T,
+              DS_TRY(gemm_launch<T>(ctx, m, n, k, alpha, (const T*)A, lda, (const T*)B, ldb, beta,
+                                    (const T*)C, ldc, (T*)out, ldo)));
+  return DS_OK;
+}
+
+int ds_trsm_lower_unit(ds_ctx* ctx, int dtype, int64_t b, int64_t m, const void* L, int64_t ldl,
+                       const void* B, int64_t ldb, void* Z, int64_t ldz) {
+  DS_TRY(ctx_begin(ctx));
+  DS_DISPATCH(dtype, T,
+              DS_TRY(trsm_lower_unit_launch<T>(ctx, b, m, (const T*)L, ldl, (const T*)B, ldb,
+                                               (T*)Z, ldz)));
+  return DS_OK;
+}
+
+int ds_trsm_upper(ds_ctx* ctx, int dtype, int64_t b, int64_t m, const void* U, int64_t ldu,
+                  const void* B, int64_t ldb, void* Z, int64_t ldz) {
+  DS_TRY(ctx_begin(ctx));
+  DS_DISPATCH(dtype, T,
+              DS_TRY(trsm_upper_launch<T>(ctx, b, m, (const T*)U, ldu, (const T*)B, ldb, (T*)Z,
+                                          ldz)));
+  return DS_OK;
+}
+
+int ds_symmetry_check(ds_ctx* ctx, int dtype, int64_t n, const void* A, int64_t lda,
+                      double* maxdiff, double* amax) {
+  DS_TRY(ctx_begin(ctx));
+  if (n == 0) {
+    *maxdiff = 0.0;
+    *amax = 0.0;
+    return DS_OK;
+  }
+  Scratch s;
+  DS_TRY(get_scratch(ctx, (size_t)ctx->num_sms * 16 + 64, &s));
+  int nblk = 0;
+  DS_DISPATCH(dtype, T, DS_TRY(symcheck_launch<T>(ctx, n, (const T*)A, lda, s.red, &nblk)));
+  finish_max2_kernel<<<1, 256, 0, ctx->stream>>>(s.red, nblk, s.out);
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  double h[2];
+  DS_TRY(fetch(ctx, h, s.out, 2 * sizeof(double)));
+  *maxdiff = h[0];
+  *amax = h[1];
+  return DS_OK;
+}
+
+int ds_relative_residual(ds_ctx* ctx, int dtype, int64_t n, const void* A, int64_t lda,
+                         const void* x, const void* b, double* result) {
+  DS_TRY(ctx_begin(ctx));
+  const GemvPlan p = gemv_plan(ctx, n, n, dtype_size(dtype));
+  const int rblocks = (int)ceil_div(std::max<int64_t>(n, 1), 256);
+  const size_t es = dtype_size(dtype);
+  void* ws = nullptr;
+  const size_t red_off = (p.part_bytes + 255) / 256 * 256;
+  const size_t r_off = red_off + ((size_t)rblocks * 3 + 64) * sizeof(double);
+  const size_t o_off = (r_off + (size_t)n * es + 255) / 256 * 256;
+  DS_TRY(ctx_workspace(ctx, o_off + 256 + 4 * sizeof(double) * rblocks, &ws));
+  char* base = (char*)ws;
+  double* part = (double*)base;
+  double* red = (double*)(base + red_off);
+  void* r = base + r_off;
+  double* out = (double*)(base + o_off);
+  int nb = 0;
+  DS_DISPATCH(dtype, T,
+              DS_TRY(gemv_launch<T>(ctx, p, (const T*)A, lda, (const T*)x, (T*)r, part, EPI_RESID,
+                                    (const T*)b, red, &nb)));
+  // ||b - Ax|| with the plain 2-norm (np.linalg.norm, core.py:207-210): sum red[2nb..3nb)
+  DS_TRY(finish_sum(ctx, red + 2 * nb, nb, out));
+  int nb2 = 0;
+  double* red2 = red + 3 * nb + 8;
+  DS_DISPATCH(dtype, T, DS_TRY(dot_launch<T>(ctx, n, (const T*)b, (const T*)b, red2, &nb2)));
+  DS_TRY(finish_sum(ctx, red2, nb2, out + 1));
+  double h[2];
+  DS_TRY(fetch(ctx, h, out, 2 * sizeof(double)));
+  const double bnorm = sqrt(h[1]);
+  if (bnorm == 0.0) {
+    set_error("||b|| = 0: relative residual undefined (x = 0 is exact)");
+    return DS_EDEGRHS;
+  }
+  *result = sqrt(h[0]) / bnorm;
+  return DS_OK;
+}
+
+}  // extern "C"

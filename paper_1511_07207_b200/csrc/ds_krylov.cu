@@ -1,0 +1,719 @@
+// ds_krylov.cu — CG and restarted GMRES(m) with device-side convergence control.
+//
+// CG  restates krylov.cg_solve    (/root/reference/pkg/src/densolve/krylov.py:36-72)
+// GMRES restates krylov.gmres_solve (krylov.py:75-182)
+//
+// Every iteration is a short fixed sequence of kernels; all scalars (alpha,
+// beta, rho, Givens rotations, residual estimates, stop decisions) live on the
+// device.  Kernels of iteration k are gated on a device word `stop_it`
+// (Gate{stop_it, k}) so the host enqueues iterations speculatively in growing
+// chunks and synchronises only once per chunk — never once per dot product as
+// the reference's Python loop does.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "ds_common.cuh"
+#include "ds_kernels.cuh"
+
+namespace ds {
+
+constexpr int kT = 256;  // threads per block of the vector kernels
+
+// ============================================================================
+// CG
+// ============================================================================
+struct CgDev {
+  int64_t stop_it;  // number of completed iterations at which the loop stops
+  int32_t status;   // DS_OK or DS_ENOTSPD
+  int32_t pad;
+  double bad_val;   // offending p'Ap
+  double bnorm;
+};
+
+// r0 = b - A x0 was produced by gemv EPI_RESID; finish the setup of krylov.py:47-52
+__global__ void cg_init_kernel(const double* red, int nblk, CgDev* st, double* rs_hist,
+                               double* hist, double tol, int64_t cap) {
+  __shared__ double sm[64];
+  Ssq q{0.0, 0.0};
+  double s2 = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    q = ssq_merge(q, Ssq{red[2 * i], red[2 * i + 1]});
+    s2 += red[2 * nblk + i];
+  }
+  q = block_ssq(q, sm);
+  s2 = block_sum(s2, sm);
+  if (threadIdx.x == 0) {
+    const double res = ssq_norm(q.scale, q.ssq) / st->bnorm;  // nrm2(r)/bnorm (krylov.py:48)
+    hist[0] = res;
+    rs_hist[0] = s2;  // rs = dot(r, r) (krylov.py:52)
+    st->stop_it = (res > tol && 0 < cap) ? cap : 0;
+    st->status = DS_OK;
+  }
+}
+
+// alpha = rs/pAp ; x += alpha p ; r -= alpha Ap ; partials of r.r and ssq(r)
+template <typename T>
+__global__ void __launch_bounds__(kT)
+    cg_update_kernel(int64_t n, T* __restrict__ x, T* __restrict__ r, const T* __restrict__ p,
+                     const T* __restrict__ Ap, const double* __restrict__ red_pap, int nblk_pap,
+                     const double* __restrict__ rs_hist, CgDev* st, double* __restrict__ red_out,
+                     Gate gate) {
+  if (gated(gate)) return;
+  __shared__ double sm[64];
+  const double pAp = reduce_sum_partials(red_pap, nblk_pap, sm);  // same order in every block
+  if (pAp <= 0.0) {  // krylov.py:57-58
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->status = DS_ENOTSPD;
+      st->bad_val = pAp;
+      st->stop_it = gate.k;
+    }
+    return;
+  }
+  const double alpha = rs_hist[gate.k] / pAp;  // krylov.py:59
+  const T a = (T)alpha, na = (T)(-alpha);
+  Ssq q{0.0, 0.0};
+  double s2 = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = add_rn(x[i], mul_rn(a, p[i]));              // x = axpy(alpha, p, x)
+    const T ri = add_rn(r[i], mul_rn(na, Ap[i]));      // r = axpy(-alpha, Ap, r)
+    r[i] = ri;
+    const double rd = (double)ri;
+    s2 = fma(rd, rd, s2);
+    q = ssq_add(q, rd);
+  }
+  q = block_ssq(q, sm);
+  s2 = block_sum(s2, sm);
+  if (threadIdx.x == 0) {
+    red_out[blockIdx.x] = s2;
+    red_out[gridDim.x + 2 * blockIdx.x] = q.scale;
+    red_out[gridDim.x + 2 * blockIdx.x + 1] = q.ssq;
+  }
+}
+
+// beta = rs_new/rs ; p = r + beta p ; history, stop decision (krylov.py:62-67)
+template <typename T>
+__global__ void __launch_bounds__(kT)
+    cg_finish_kernel(int64_t n, const T* __restrict__ r, T* __restrict__ p,
+                     const double* __restrict__ red, int nblk, double* rs_hist, double* hist,
+                     CgDev* st, double tol, int64_t cap, Gate gate) {
+  if (gated(gate)) return;
+  __shared__ double sm[64];
+  double s2 = 0.0;
+  Ssq q{0.0, 0.0};
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    s2 += red[i];
+    q = ssq_merge(q, Ssq{red[nblk + 2 * i], red[nblk + 2 * i + 1]});
+  }
+  s2 = block_sum(s2, sm);
+  q = block_ssq(q, sm);
+  const int64_t k = gate.k;
+  const double beta = s2 / rs_hist[k];
+  const T bt = (T)beta;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = add_rn(r[i], mul_rn(bt, p[i]));  // p = axpy(rs_new/rs, p, r)
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const double res = ssq_norm(q.scale, q.ssq) / st->bnorm;
+    rs_hist[k + 1] = s2;
+    hist[k + 1] = res;
+    if (!(res > tol) || k + 1 >= cap) st->stop_it = k + 1;
+  }
+}
+
+__global__ void set_bnorm_kernel(const double* norm, CgDev* st) {
+  if (threadIdx.x == 0) st->bnorm = norm[0];
+}
+
+static int vec_grid(ds_ctx* ctx, int64_t n) {
+  int64_t want = ceil_div(std::max<int64_t>(n, 1), kT * 4);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->num_sms * 2));
+}
+
+
+template <typename T>
+int cg_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, const T* x0, T* x,
+            double tol, int64_t cap, int check_sym, double* h_hist, int64_t hist_cap,
+            ds_solve_info* info) {
+  const int64_t launches0 = ctx->launches;
+  const double u = (sizeof(T) == 8 ? 1.1102230246251565e-16 : 5.960464477539063e-08);
+  if (check_sym) {
+    double md = 0, am = 0;
+    DS_TRY(ds_symmetry_check(ctx, sizeof(T) == 8 ? DS_F64 : DS_F32, n, A, lda, &md, &am));
+    if (md > 10.0 * u * am) {  // krylov.py:42-44
+      set_error("matrix is not symmetric");
+      info->error_index = -1;
+      return DS_ENOTSPD;
+    }
+  }
+  const GemvPlan gp = gemv_plan(ctx, n, n, sizeof(T));
+  const int rblocks = (int)ceil_div(std::max<int64_t>(n, 1), 256);
+  const int vg = vec_grid(ctx, n);
+  // workspace
+  size_t need = 0;
+  {
+    need += gp.part_bytes + 256;
+    need += (size_t)n * sizeof(T) * 3 + 3 * 256;                    // r, p, Ap
+    need += ((size_t)rblocks * 3 + (size_t)vg * 3 + 64) * sizeof(double) * 2 + 4 * 256;
+    need += (size_t)(cap + 2) * sizeof(double) * 2 + 2 * 256;       // rs_hist, hist
+    need += sizeof(CgDev) + 256 + 64;
+  }
+  void* ws = nullptr;
+  DS_TRY(ctx_workspace(ctx, need, &ws));
+  Carver cv{(char*)ws};
+  double* part = cv.take<double>(gp.part_bytes);
+  T* r = cv.take<T>((size_t)n * sizeof(T));
+  T* p = cv.take<T>((size_t)n * sizeof(T));
+  T* Ap = cv.take<T>((size_t)n * sizeof(T));
+  double* red_a = cv.take<double>(((size_t)rblocks * 3 + 64) * sizeof(double));
+  double* red_b = cv.take<double>(((size_t)vg * 3 + 64) * sizeof(double));
+  double* rs_hist = cv.take<double>((size_t)(cap + 2) * sizeof(double));
+  double* hist = cv.take<double>((size_t)(cap + 2) * sizeof(double));
+  CgDev* st = cv.take<CgDev>(sizeof(CgDev));
+  double* scal = cv.take<double>(64);
+
+  // ||b|| = nrm2(b) (krylov.py:45 -> _rhs_norm :29-33)
+  int nb = 0;
+  DS_TRY(ssq_launch<T>(ctx, n, b, red_b, &nb));
+  DS_TRY(finish_ssq(ctx, red_b, nb, scal));
+  double bnorm = 0;
+  DS_CUDA(cudaMemcpyAsync(&bnorm, scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (bnorm == 0.0) {
+    set_error("||b|| = 0");
+    return DS_EDEGRHS;
+  }
+  set_bnorm_kernel<<<1, 32, 0, ctx->stream>>>(scal, st);
+  count_launch(ctx);
+  // x = x0.copy(); r = b - A x; res; p = r; rs = r.r   (krylov.py:46-52)
+  if (x != x0) DS_CUDA(cudaMemcpyAsync(x, x0, n * sizeof(T), cudaMemcpyDeviceToDevice, ctx->stream));
+  int rb = 0;
+  DS_TRY(gemv_launch<T>(ctx, gp, A, lda, x, r, part, EPI_RESID, b, red_a, &rb));
+  cg_init_kernel<<<1, 256, 0, ctx->stream>>>(red_a, rb, st, rs_hist, hist, tol, cap);
+  count_launch(ctx);
+  DS_CUDA(cudaMemcpyAsync(p, r, n * sizeof(T), cudaMemcpyDeviceToDevice, ctx->stream));
+  DS_CHECK_LAUNCH();
+
+  // hot loop (krylov.py:54-67), enqueued in growing chunks
+  int64_t* h_stop = nullptr;
+  DS_TRY(ctx_hostbuf(ctx, 64, (void**)&h_stop));
+  int64_t k = 0, chunk = 2;
+  int64_t stop_it = cap;
+  while (true) {
+    // read the stop word produced so far
+    DS_CUDA(cudaMemcpyAsync(h_stop, &st->stop_it, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    DS_CUDA(cudaStreamSynchronize(ctx->stream));
+    stop_it = *h_stop;
+    if (stop_it <= k || k >= cap) break;
+    const int64_t kend = std::min<int64_t>(cap, k + chunk);
+    for (; k < kend; ++k) {
+      const Gate g{&st->stop_it, k};
+      int rb2 = 0;
+      DS_TRY(gemv_launch<T>(ctx, gp, A, lda, p, Ap, part, EPI_DOT, p, red_a, &rb2, g));
+      cg_update_kernel<T><<<vg, kT, 0, ctx->stream>>>(n, x, r, p, Ap, red_a, rb2, rs_hist, st,
+                                                      red_b, g);
+      cg_finish_kernel<T><<<vg, kT, 0, ctx->stream>>>(n, r, p, red_b, vg, rs_hist, hist, st, tol,
+                                                      cap, g);
+      count_launch(ctx, 2);
+    }
+    DS_CHECK_LAUNCH();
+    chunk = std::min<int64_t>(chunk * 2, 64);
+  }
+  // results
+  CgDev hst;
+  DS_CUDA(cudaMemcpyAsync(&hst, st, sizeof(CgDev), cudaMemcpyDeviceToHost, ctx->stream));
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (hst.status == DS_ENOTSPD) {
+    set_error("p'Ap = %.17g <= 0: matrix is not positive definite", hst.bad_val);
+    info->error_value = hst.bad_val;
+    info->error_index = hst.stop_it;
+    return DS_ENOTSPD;
+  }
+  const int64_t iters = std::min<int64_t>(hst.stop_it, cap);
+  const int64_t hl = std::min<int64_t>(iters + 1, hist_cap);
+  if (h_hist && hl > 0)
+    DS_CUDA(cudaMemcpyAsync(h_hist, hist, hl * sizeof(double), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  double res = 0;
+  DS_CUDA(cudaMemcpyAsync(&res, hist + iters, sizeof(double), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  info->iterations = iters;
+  info->history_len = hl;
+  info->final_relative_residual = res;
+  info->converged = res <= tol;  // krylov.py:68
+  info->breakdown = DS_BREAKDOWN_NONE;
+  info->kernel_launches = ctx->launches - launches0;
+  return DS_OK;
+}
+
+// ============================================================================
+// GMRES(m)
+// ============================================================================
+struct GmDev {
+  int64_t stop_k;  // inner step at which the cycle stops (m if it runs full)
+  int32_t happy;
+  int32_t status;  // DS_OK / DS_ESINGULAR (LS solve)
+  int64_t bad_row;
+  double beta;     // ||r0|| of the cycle
+  double bnorm;    // nrm2(b)
+};
+
+// multi-dot  h_j = V[:,j] . w  for j < kc (one pass over V, w kept in registers)
+template <typename T>
+__global__ void __launch_bounds__(kT)
+    multidot_kernel(int64_t n, const T* __restrict__ V, int64_t ldv, int kc,
+                    const T* __restrict__ w, double* __restrict__ part, int ldp, Gate gate) {
+  if (gated(gate)) return;
+  __shared__ double sm[kT / 32][64];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const double wi = i < n ? (double)w[i] : 0.0;
+  for (int j = 0; j < kc; ++j) {
+    double s = i < n ? (double)V[i + (int64_t)j * ldv] * wi : 0.0;
+    s = warp_sum(s);
+    if (lane == 0) sm[wid][j] = s;
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < kc; j += blockDim.x) {
+    double s = 0.0;
+    for (int q = 0; q < kT / 32; ++q) s += sm[q][j];
+    part[(int64_t)blockIdx.x * ldp + j] = s;
+  }
+}
+
+// w -= sum_j h_j V[:,j] (sequential axpys, krylov.py:136-138); optionally emits
+// ssq partials of the updated w; block 0 records the coefficients.
+//   pass 0: H[j,k] = h_j, hsave = h      pass 1 (reorth): H[j,k] = hsave + h
+template <typename T>
+__global__ void __launch_bounds__(kT)
+    cgs_update_kernel(int64_t n, const T* __restrict__ V, int64_t ldv, int kc, T* __restrict__ w,
+                      const double* __restrict__ part, int ldp, int nparts, T* Hcol,
+                      double* hsave, int pass, double* red_ssq, Gate gate) {
+  if (gated(gate)) return;
+  __shared__ double hs[64];
+  __shared__ double sm[64];
+  for (int j = threadIdx.x; j < kc; j += blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nparts; ++b) s += part[(int64_t)b * ldp + j];
+    hs[j] = s;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    for (int j = threadIdx.x; j < kc; j += blockDim.x) {
+      if (pass == 0) {
+        hsave[j] = hs[j];
+        Hcol[j] = (T)hs[j];
+      } else {
+        Hcol[j] = (T)(hsave[j] + hs[j]);
+      }
+    }
+  }
+  Ssq q{0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    T wi = w[i];
+    for (int j = 0; j < kc; ++j) wi = add_rn(wi, mul_rn((T)(-hs[j]), V[i + (int64_t)j * ldv]));
+    w[i] = wi;
+    q = ssq_add(q, (double)wi);
+  }
+  if (red_ssq) {
+    q = block_ssq(q, sm);
+    if (threadIdx.x == 0) {
+      red_ssq[2 * blockIdx.x] = q.scale;
+      red_ssq[2 * blockIdx.x + 1] = q.ssq;
+    }
+  }
+}
+
+// h_{k+1,k} = ||w|| ; v_{k+1} = w / h ; Givens rotation ; LS estimate ; stop gate
+// (krylov.py:139-163)
+template <typename T>
+__global__ void __launch_bounds__(kT)
+    gm_step_finish_kernel(int64_t n, T* __restrict__ w /* = V[:,k+1] */, const double* red_ssq,
+                          int nblk, T* H, T* Hraw, int64_t ldh, T* g, T* cs, T* sn, int k,
+                          double* est_out, GmDev* st, double tol, int64_t total_before,
+                          int64_t cap, Gate gate) {
+  if (gated(gate)) return;
+  __shared__ double sm[64];
+  Ssq q{0.0, 0.0};
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x)
+    q = ssq_merge(q, Ssq{red_ssq[2 * i], red_ssq[2 * i + 1]});
+  q = block_ssq(q, sm);
+  const double hk1 = ssq_norm(q.scale, q.ssq);
+  const bool happy = hk1 == 0.0;
+  if (!happy) {
+    const T s = (T)(1.0 / hk1);  // scal(1.0/hk1, w) (krylov.py:143-144)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+      w[i] = mul_rn(s, w[i]);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    T* Hk = H + (int64_t)k * ldh;
+    T* Hr = Hraw + (int64_t)k * ldh;
+    Hk[k + 1] = (T)hk1;
+    for (int j = 0; j <= k + 1; ++j) Hr[j] = Hk[j];  // Hraw[:,k] = H[:,k] (krylov.py:141)
+    for (int j = 0; j < k; ++j) {                     // krylov.py:147-150
+      const T t = add_rn(mul_rn(cs[j], Hk[j]), mul_rn(sn[j], Hk[j + 1]));
+      Hk[j + 1] = add_rn(mul_rn(-sn[j], Hk[j]), mul_rn(cs[j], Hk[j + 1]));
+      Hk[j] = t;
+    }
+    const T denom = sizeof(T) == 8 ? (T)hypot((double)Hk[k], (double)Hk[k + 1])
+                                   : (T)hypotf((float)Hk[k], (float)Hk[k + 1]);  // np.hypot
+    cs[k] = div_rn(Hk[k], denom);
+    sn[k] = div_rn(Hk[k + 1], denom);
+    Hk[k] = denom;
+    Hk[k + 1] = T(0);
+    g[k + 1] = mul_rn(-sn[k], g[k]);
+    g[k] = mul_rn(cs[k], g[k]);
+    const double est = fabs((double)g[k + 1]) / st->bnorm;  // krylov.py:160
+    est_out[k] = est;
+    const int64_t total = total_before + k + 1;
+    if (happy) st->happy = 1;
+    if (happy || est <= tol || total >= cap) st->stop_k = k + 1;  // krylov.py:162-163
+  }
+}
+
+// y = H[:inner,:inner]^-1 g[:inner] (backward_substitution, direct.py:139-152), one thread
+template <typename T>
+__global__ void gm_lsq_kernel(const T* H, int64_t ldh, const T* g, int inner, T* y, GmDev* st) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int i = 0; i < inner; ++i) y[i] = g[i];
+  for (int i = inner - 1; i >= 0; --i) {
+    if (i + 1 < inner) {
+      double s = 0.0;
+      for (int j = i + 1; j < inner; ++j) s = fma((double)H[i + (int64_t)j * ldh], (double)y[j], s);
+      y[i] = sub_rn(y[i], (T)s);
+    }
+    const T d = H[i + (int64_t)i * ldh];
+    if (d == T(0)) {
+      st->status = DS_ESINGULAR;
+      st->bad_row = i;
+      return;
+    }
+    y[i] = div_rn(y[i], d);
+  }
+}
+
+// cycle start: V[:,0] = scal(1/beta, r); g = beta e1 (krylov.py:116-123)
+template <typename T>
+__global__ void gm_cycle_start_kernel(int64_t n, const T* __restrict__ r, T* __restrict__ v0,
+                                      double beta, T* g) {
+  const T s = (T)(1.0 / beta);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v0[i] = mul_rn(s, r[i]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) g[0] = (T)beta;
+}
+
+__global__ void finish_resid_kernel(const double* red, int nblk, double* out) {
+  // out[0] = nrm2 (scaled, Backend.nrm2), out[1] = plain sum of squares
+  __shared__ double sm[64];
+  Ssq q{0.0, 0.0};
+  double s2 = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    q = ssq_merge(q, Ssq{red[2 * i], red[2 * i + 1]});
+    s2 += red[2 * nblk + i];
+  }
+  q = block_ssq(q, sm);
+  s2 = block_sum(s2, sm);
+  if (threadIdx.x == 0) {
+    out[0] = ssq_norm(q.scale, q.ssq);
+    out[1] = s2;
+  }
+}
+
+template <typename T>
+int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, const T* x0, T* x,
+               double tol, int64_t cap, int64_t m, int orth, double* h_hist, int64_t hist_cap,
+               int64_t* h_cycles, int64_t cycles_cap, ds_sink_fn sink, void* sink_user,
+               ds_solve_info* info) {
+  const int64_t launches0 = ctx->launches;
+  const double u = (sizeof(T) == 8 ? 1.1102230246251565e-16 : 5.960464477539063e-08);
+  if (m > 62) {
+    // the on-device Givens/multi-dot kernels keep <= 64 coefficients in shared memory
+    set_error("restart_m = %lld exceeds the device limit of 62", (long long)m);
+    return DS_EINVAL;
+  }
+  const GemvPlan gp = gemv_plan(ctx, n, n, sizeof(T));
+  const int rblocks = (int)ceil_div(std::max<int64_t>(n, 1), 256);
+  const int vg = vec_grid(ctx, n);
+  const int mdb = (int)ceil_div(std::max<int64_t>(n, 1), kT);  // multidot blocks
+  const int64_t ldv = ceil_div(std::max<int64_t>(n, 1), 4) * 4;
+  const int64_t ldh = m + 1;
+  const int ldp = 64;
+  size_t need = gp.part_bytes + (size_t)ldv * (m + 1) * sizeof(T) + (size_t)n * sizeof(T) +
+                (size_t)(ldh * m * 2 + 3 * (m + 2) + 64) * sizeof(T) +
+                ((size_t)mdb * ldp + (size_t)rblocks * 3 + (size_t)vg * 2 + 512) * sizeof(double) +
+                sizeof(GmDev) + 16 * 256;
+  void* ws = nullptr;
+  DS_TRY(ctx_workspace(ctx, need, &ws));
+  Carver cv{(char*)ws};
+  double* part = cv.take<double>(gp.part_bytes);
+  T* V = cv.take<T>((size_t)ldv * (m + 1) * sizeof(T));
+  T* r = cv.take<T>((size_t)n * sizeof(T));
+  T* H = cv.take<T>((size_t)ldh * m * sizeof(T));
+  T* Hraw = cv.take<T>((size_t)ldh * m * sizeof(T));
+  T* g = cv.take<T>((size_t)(m + 2) * sizeof(T));
+  T* cs = cv.take<T>((size_t)(m + 2) * sizeof(T));
+  T* sn = cv.take<T>((size_t)(m + 2) * sizeof(T));
+  T* y = cv.take<T>((size_t)64 * sizeof(T));
+  double* mpart = cv.take<double>((size_t)mdb * ldp * sizeof(double));
+  double* red_a = cv.take<double>(((size_t)rblocks * 3 + 64) * sizeof(double));
+  double* red_b = cv.take<double>(((size_t)std::max(vg, rblocks) * 2 + 64) * sizeof(double));
+  double* hsave = cv.take<double>(64 * sizeof(double));
+  double* est = cv.take<double>(64 * sizeof(double));
+  double* scal = cv.take<double>(64 * sizeof(double));
+  GmDev* st = cv.take<GmDev>(sizeof(GmDev));
+
+  double* hbuf = nullptr;
+  DS_TRY(ctx_hostbuf(ctx, 4096, (void**)&hbuf));
+
+  // ||b|| via nrm2 (krylov.py:87) and the plain ||b|| of relative_residual (core.py:207)
+  int nb = 0;
+  DS_TRY(ssq_launch<T>(ctx, n, b, red_b, &nb));
+  DS_TRY(finish_ssq(ctx, red_b, nb, scal));
+  int nb2 = 0;
+  DS_TRY(dot_launch<T>(ctx, n, b, b, red_a, &nb2));
+  DS_TRY(finish_sum(ctx, red_a, nb2, scal + 1));
+  DS_CUDA(cudaMemcpyAsync(hbuf, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  const double bnorm = hbuf[0];
+  const double bnorm_plain = sqrt(hbuf[1]);
+  if (bnorm == 0.0) {
+    set_error("||b|| = 0");
+    return DS_EDEGRHS;
+  }
+  if (x != x0) DS_CUDA(cudaMemcpyAsync(x, x0, n * sizeof(T), cudaMemcpyDeviceToDevice, ctx->stream));
+
+  std::vector<double> history;
+  std::vector<int64_t> cycles;
+  int64_t total_it = 0;
+  int breakdown = DS_BREAKDOWN_NONE;
+  bool converged = false;
+  std::vector<T> hV, hH;
+
+  auto finish = [&](bool conv, int bd) {
+    converged = conv;
+    breakdown = bd;
+  };
+
+  int64_t residual_evals = 0;
+  while (true) {
+    // r = b - A x ; beta = nrm2(r)   (krylov.py:104-106)
+    ++residual_evals;
+    int rb = 0;
+    DS_TRY(gemv_launch<T>(ctx, gp, A, lda, x, r, part, EPI_RESID, b, red_a, &rb));
+    finish_resid_kernel<<<1, 256, 0, ctx->stream>>>(red_a, rb, scal + 2);
+    count_launch(ctx);
+    DS_CUDA(cudaMemcpyAsync(hbuf, scal + 2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    DS_CUDA(cudaStreamSynchronize(ctx->stream));
+    const double beta = hbuf[0];
+    const double relres = beta / bnorm;
+    if (total_it == 0) history.push_back(relres);
+    if (relres <= tol) {
+      finish(true, DS_BREAKDOWN_NONE);
+      break;
+    }
+    if (total_it >= cap) {
+      finish(false, DS_BREAKDOWN_NONE);
+      break;
+    }
+    cycles.push_back(total_it);
+    const double cycle_start_res = relres;
+
+    // fresh cycle state (krylov.py:116-123)
+    DS_CUDA(cudaMemsetAsync(V, 0, (size_t)ldv * (m + 1) * sizeof(T), ctx->stream));
+    DS_CUDA(cudaMemsetAsync(H, 0, (size_t)ldh * m * sizeof(T), ctx->stream));
+    DS_CUDA(cudaMemsetAsync(Hraw, 0, (size_t)ldh * m * sizeof(T), ctx->stream));
+    DS_CUDA(cudaMemsetAsync(g, 0, (size_t)(m + 2) * sizeof(T) * 3, ctx->stream));
+    GmDev init{};
+    init.stop_k = m;
+    init.beta = beta;
+    init.bnorm = bnorm;
+    init.bad_row = -1;
+    DS_CUDA(cudaMemcpyAsync(st, &init, sizeof(GmDev), cudaMemcpyHostToDevice, ctx->stream));
+    gm_cycle_start_kernel<T><<<vg, kT, 0, ctx->stream>>>(n, r, V, beta, g);
+    count_launch(ctx);
+    DS_CHECK_LAUNCH();
+
+    // inner Arnoldi steps, enqueued in chunks behind the device gate
+    int64_t k = 0, chunk = 4;
+    int64_t stop_k = m;
+    while (true) {
+      if (k > 0) {
+        DS_CUDA(cudaMemcpyAsync(hbuf, &st->stop_k, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+        DS_CUDA(cudaStreamSynchronize(ctx->stream));
+        stop_k = *reinterpret_cast<int64_t*>(hbuf);
+        if (stop_k <= k || k >= m) break;
+      }
+      const int64_t kend = std::min<int64_t>(m, k + chunk);
+      for (; k < kend; ++k) {
+        const Gate gt{&st->stop_k, k};
+        T* vk = V + k * ldv;
+        T* w = V + (k + 1) * ldv;
+        const int kc = (int)k + 1;
+        DS_TRY(gemv_launch<T>(ctx, gp, A, lda, vk, w, part, EPI_STORE, nullptr, nullptr, nullptr,
+                              gt));
+        const int passes = orth == DS_ORTH_CLASSICAL ? 1 : 2;
+        for (int ps = 0; ps < passes; ++ps) {
+          multidot_kernel<T><<<mdb, kT, 0, ctx->stream>>>(n, V, ldv, kc, w, mpart, ldp, gt);
+          cgs_update_kernel<T><<<vg, kT, 0, ctx->stream>>>(
+              n, V, ldv, kc, w, mpart, ldp, mdb, H + k * ldh, hsave, ps,
+              ps == passes - 1 ? red_b : nullptr, gt);
+          count_launch(ctx, 2);
+        }
+        gm_step_finish_kernel<T><<<vg, kT, 0, ctx->stream>>>(n, w, red_b, vg, H, Hraw, ldh, g, cs,
+                                                             sn, (int)k, est, st, tol, total_it,
+                                                             cap, gt);
+        count_launch(ctx);
+      }
+      DS_CHECK_LAUNCH();
+      chunk = std::min<int64_t>(chunk * 2, 32);
+    }
+    GmDev hst;
+    DS_CUDA(cudaMemcpyAsync(&hst, st, sizeof(GmDev), cudaMemcpyDeviceToHost, ctx->stream));
+    DS_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int inner = (int)std::min<int64_t>(hst.stop_k, m);
+    const bool happy = hst.happy != 0;
+    {
+      std::vector<double> e(inner);
+      if (inner > 0) {
+        DS_CUDA(cudaMemcpyAsync(e.data(), est, inner * sizeof(double), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+        DS_CUDA(cudaStreamSynchronize(ctx->stream));
+      }
+      for (int i = 0; i < inner; ++i) history.push_back(e[i]);
+    }
+    total_it += inner;
+
+    // cycle end: y = H^-1 g ; x += V y   (krylov.py:166-167)
+    gm_lsq_kernel<T><<<1, 32, 0, ctx->stream>>>(H, ldh, g, inner, y, st);
+    count_launch(ctx);
+    {
+      const GemvPlan gp2 = gemv_plan(ctx, n, inner, sizeof(T));
+      if (gp2.part_bytes > gp.part_bytes) {
+        set_error("internal: gemv workspace");
+        return DS_ECUDA;
+      }
+      DS_TRY(gemv_launch<T>(ctx, gp2, V, ldv, y, x, part, EPI_AXPY_INTO, nullptr, nullptr,
+                            nullptr));
+    }
+    DS_CUDA(cudaMemcpyAsync(&hst, st, sizeof(GmDev), cudaMemcpyDeviceToHost, ctx->stream));
+    DS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hst.status == DS_ESINGULAR) {
+      set_error("zero diagonal at row %lld", (long long)hst.bad_row);
+      info->error_index = hst.bad_row;
+      return DS_ESINGULAR;
+    }
+    if (sink) {  // krylov.py:168-169
+      hV.resize((size_t)n * (m + 1));
+      hH.resize((size_t)ldh * m);
+      DS_CUDA(cudaMemcpy2DAsync(hV.data(), n * sizeof(T), V, ldv * sizeof(T), n * sizeof(T), m + 1,
+                                cudaMemcpyDeviceToHost, ctx->stream));
+      DS_CUDA(cudaMemcpyAsync(hH.data(), Hraw, (size_t)ldh * m * sizeof(T),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+      DS_CUDA(cudaStreamSynchronize(ctx->stream));
+      sink(sink_user, hV.data(), hH.data(), inner, beta);
+    }
+    // true residual (core.relative_residual, uncounted A @ x; krylov.py:171)
+    {
+      int rb2 = 0;
+      DS_TRY(gemv_launch<T>(ctx, gp, A, lda, x, r, part, EPI_RESID, b, red_a, &rb2));
+      finish_resid_kernel<<<1, 256, 0, ctx->stream>>>(red_a, rb2, scal + 4);
+      count_launch(ctx);
+      DS_CUDA(cudaMemcpyAsync(hbuf, scal + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                              ctx->stream));
+      DS_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    const double true_res = sqrt(hbuf[1]) / bnorm_plain;
+    if (happy || history.back() <= tol || true_res <= tol) {  // krylov.py:172-175
+      history.back() = true_res;
+      if (true_res <= tol || happy) {
+        finish(true, happy ? DS_BREAKDOWN_HAPPY : DS_BREAKDOWN_NONE);
+        break;
+      }
+    }
+    if (total_it >= cap) {  // krylov.py:176-178
+      history.back() = true_res;
+      finish(false, DS_BREAKDOWN_NONE);
+      break;
+    }
+    if (inner == m && true_res >= cycle_start_res * (1.0 - u)) {  // stagnation :180-182
+      history.back() = true_res;
+      finish(false, DS_BREAKDOWN_NONE);
+      break;
+    }
+  }
+  const int64_t hl = std::min<int64_t>((int64_t)history.size(), hist_cap);
+  for (int64_t i = 0; i < hl; ++i) h_hist[i] = history[i];
+  const int64_t cl = std::min<int64_t>((int64_t)cycles.size(), cycles_cap);
+  for (int64_t i = 0; i < cl; ++i) h_cycles[i] = cycles[i];
+  info->converged = converged;
+  info->breakdown = breakdown;
+  info->iterations = total_it;
+  info->final_relative_residual = history.back();
+  info->history_len = (int64_t)history.size();
+  info->cycles_len = (int64_t)cycles.size();
+  info->residual_evals = residual_evals;
+  info->kernel_launches = ctx->launches - launches0;
+  return DS_OK;
+}
+
+}  // namespace ds
+
+using namespace ds;
+
+extern "C" {
+
+int ds_cg(ds_ctx* ctx, int dtype, int64_t n, const void* A, int64_t lda, const void* b,
+          const void* x0, void* x, double tol, int64_t max_it, int check_sym, double* h_hist,
+          int64_t hist_cap, ds_solve_info* info) {
+  DS_TRY(ctx_begin(ctx));
+  *info = ds_solve_info{};
+  info->error_index = -1;
+  if (n <= 0) {
+    set_error("matrix must be square and non-empty, got n=%lld", (long long)n);
+    return DS_EDIM;
+  }
+  if (!(tol > 0)) {
+    set_error("tolerance must be > 0");
+    return DS_EINVAL;
+  }
+  if (max_it < 1) {
+    set_error("max_iterations must be >= 1");
+    return DS_EINVAL;
+  }
+  DS_DISPATCH(dtype, T,
+              return cg_impl<T>(ctx, n, (const T*)A, lda, (const T*)b, (const T*)x0, (T*)x, tol,
+                                max_it, check_sym, h_hist, hist_cap, info));
+}
+
+int ds_gmres(ds_ctx* ctx, int dtype, int64_t n, const void* A, int64_t lda, const void* b,
+             const void* x0, void* x, double tol, int64_t max_it, int64_t restart_m, int orth,
+             double* h_hist, int64_t hist_cap, int64_t* h_cycles, int64_t cycles_cap,
+             ds_sink_fn sink, void* sink_user, ds_solve_info* info) {
+  DS_TRY(ctx_begin(ctx));
+  *info = ds_solve_info{};
+  info->error_index = -1;
+  if (n <= 0) {
+    set_error("matrix must be square and non-empty, got n=%lld", (long long)n);
+    return DS_EDIM;
+  }
+  if (!(tol > 0) || restart_m < 1 || max_it < 1 ||
+      (orth != DS_ORTH_MODIFIED && orth != DS_ORTH_CLASSICAL)) {
+    set_error("invalid GMRES configuration");
+    return DS_EINVAL;
+  }
+  DS_DISPATCH(dtype, T,
+              return gmres_impl<T>(ctx, n, (const T*)A, lda, (const T*)b, (const T*)x0, (T*)x, tol,
+                                   max_it, restart_m, orth, h_hist, hist_cap, h_cycles, cycles_cap,
+                                   sink, sink_user, info));
+}
+
+}  // extern "C"

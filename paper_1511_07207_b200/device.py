@@ -1,0 +1,188 @@
+"""Device-resident operands: the staging seam of the Backend contract.
+
+The reference keeps ``Backend.stage_in`` / ``stage_out`` as identity hooks
+"preserved for a future accelerator backend" (backends.py:94-100);
+here they are real host<->device transfers.  ``DeviceArray`` is a column-major
+(F-order) device buffer with a leading dimension padded to a multiple of 4
+elements so every column starts 32-byte aligned (128-bit vector loads in the
+GEMV, 16-byte cp.async in the GEMM).  Solver entry points accept either NumPy
+arrays (uploaded per call, like the reference's per-call arrays) or
+``DeviceArray`` handles (no transfer).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import weakref
+from ctypes import c_double, c_int64, c_void_p
+
+import numpy as np
+
+from . import _lib, core
+
+LD_ALIGN = 4
+
+
+def _padded_ld(rows: int) -> int:
+    return max(LD_ALIGN, (rows + LD_ALIGN - 1) // LD_ALIGN * LD_ALIGN)
+
+
+class DeviceArray:
+    """A 1-d vector or 2-d column-major matrix in device memory."""
+
+    __slots__ = ("ctx", "shape", "dtype", "ld", "ptr", "_fin", "__weakref__")
+
+    def __init__(self, ctx: _lib.Context, shape, dtype, ld: int | None = None):
+        self.ctx = ctx
+        self.shape = tuple(int(s) for s in shape)
+        self.dtype = np.dtype(dtype)
+        _lib.dtype_code(self.dtype)
+        if len(self.shape) == 1:
+            self.ld = max(self.shape[0], 1)
+            nbytes = self.shape[0] * self.dtype.itemsize
+        elif len(self.shape) == 2:
+            self.ld = ld if ld is not None else _padded_ld(self.shape[0])
+            nbytes = self.ld * max(self.shape[1], 1) * self.dtype.itemsize
+        else:
+            raise core.DimensionError(f"device arrays are 1-d or 2-d, got shape {self.shape}")
+        p = c_void_p()
+        _lib.check(ctx.lib.ds_malloc(ctx.handle, max(nbytes, 16), ctypes.byref(p)))
+        self.ptr = p.value
+        self._fin = weakref.finalize(self, ctx.lib.ds_free, ctx.handle, c_void_p(self.ptr))
+
+    # -- numpy-like metadata used by the validators -------------------------------------
+    @property
+    def ndim(self) -> int:
+        return len(self.shape)
+
+    @property
+    def nbytes(self) -> int:
+        if self.ndim == 1:
+            return self.shape[0] * self.dtype.itemsize
+        return self.ld * self.shape[1] * self.dtype.itemsize
+
+    @property
+    def dcode(self) -> int:
+        return _lib.dtype_code(self.dtype)
+
+    def free(self):
+        self._fin()
+
+    def __repr__(self):
+        return f"DeviceArray(shape={self.shape}, dtype={self.dtype}, ld={self.ld}, device={self.ctx.device})"
+
+    # -- transfers -------------------------------------------------------------------------
+    @classmethod
+    def empty(cls, shape, dtype, ctx: _lib.Context | None = None):
+        return cls(ctx or _lib.context(), shape, dtype)
+
+    @classmethod
+    def from_host(cls, a, ctx: _lib.Context | None = None):
+        ctx = ctx or _lib.context()
+        a = np.asarray(a)
+        _lib.dtype_code(a.dtype)
+        out = cls(ctx, a.shape, a.dtype)
+        out.upload(a)
+        return out
+
+    def upload(self, a):
+        a = np.asarray(a)
+        if a.shape != self.shape or a.dtype != self.dtype:
+            raise core.DimensionError(f"upload of {a.shape}/{a.dtype} into {self.shape}/{self.dtype}")
+        lib, h = self.ctx.lib, self.ctx.handle
+        if self.ndim == 1:
+            a = np.ascontiguousarray(a)
+            _lib.check(lib.ds_memcpy_h2d(h, c_void_p(self.ptr), a.ctypes.data_as(c_void_p), a.nbytes))
+            return
+        rows, cols = self.shape
+        if a.flags.f_contiguous:
+            order, ld_host = 0, rows
+        elif a.flags.c_contiguous:
+            order, ld_host = 1, cols
+        else:
+            a = np.asfortranarray(a)
+            order, ld_host = 0, rows
+        _lib.check(lib.ds_upload_matrix(h, self.dcode, a.ctypes.data_as(c_void_p), rows, cols,
+                                        max(ld_host, 1), order, c_void_p(self.ptr), self.ld))
+
+    def to_host(self, out: np.ndarray | None = None) -> np.ndarray:
+        lib, h = self.ctx.lib, self.ctx.handle
+        if self.ndim == 1:
+            if out is None:
+                out = np.empty(self.shape, dtype=self.dtype)
+            _lib.check(lib.ds_memcpy_d2h(h, out.ctypes.data_as(c_void_p), c_void_p(self.ptr), out.nbytes))
+            return out
+        rows, cols = self.shape
+        if out is None:
+            out = np.empty((rows, cols), dtype=self.dtype, order="F")
+        assert out.flags.f_contiguous
+        _lib.check(lib.ds_download_matrix(h, self.dcode, c_void_p(self.ptr), rows, cols, self.ld,
+                                          out.ctypes.data_as(c_void_p), max(rows, 1)))
+        return out
+
+    def copy(self) -> "DeviceArray":
+        out = DeviceArray(self.ctx, self.shape, self.dtype, ld=self.ld)
+        _lib.check(self.ctx.lib.ds_memcpy_d2d(self.ctx.handle, c_void_p(out.ptr), c_void_p(self.ptr),
+                                              self.nbytes))
+        return out
+
+    def col_ptr(self, j: int) -> int:
+        return self.ptr + j * self.ld * self.dtype.itemsize
+
+
+def to_device(a, ctx: _lib.Context | None = None) -> DeviceArray:
+    """Stage a host operand (no-op for a DeviceArray on the same context)."""
+    ctx = ctx or _lib.context()
+    if isinstance(a, DeviceArray):
+        if a.ctx is not ctx:
+            raise ValueError("operand lives on another device context")
+        return a
+    return DeviceArray.from_host(a, ctx)
+
+
+def is_device(a) -> bool:
+    return isinstance(a, DeviceArray)
+
+
+# ---- pinned host memory (for end-to-end transfers at full PCIe rate) ---------------------
+class _PinnedOwner:
+    def __init__(self, ptr, lib):
+        self.ptr = ptr
+        self._fin = weakref.finalize(self, lib.ds_host_free, c_void_p(ptr))
+
+
+def pinned_empty(shape, dtype, order="F") -> np.ndarray:
+    """A NumPy array backed by page-locked host memory."""
+    lib = _lib.load_library()
+    dt = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dt.itemsize
+    p = c_void_p()
+    _lib.check(lib.ds_host_alloc(max(nbytes, 16), ctypes.byref(p)))
+    owner = _PinnedOwner(p.value, lib)
+    buf = (ctypes.c_char * max(nbytes, 16)).from_address(p.value)
+    arr = np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape, order=order)
+    # keep the owner alive with the array
+    arr_base = arr
+    _pinned_keepalive[id(arr_base)] = owner
+    weakref.finalize(arr_base, _pinned_keepalive.pop, id(arr_base), None)
+    return arr
+
+
+_pinned_keepalive: dict = {}
+
+
+def relative_residual_device(A, x, b) -> float:
+    ctx = A.ctx if isinstance(A, DeviceArray) else _lib.context()
+    dA, dx, db = to_device(A, ctx), to_device(x, ctx), to_device(b, ctx)
+    out = c_double(0.0)
+    _lib.check(ctx.lib.ds_relative_residual(ctx.handle, dA.dcode, dA.shape[0], c_void_p(dA.ptr), dA.ld,
+                                            c_void_p(dx.ptr), c_void_p(db.ptr), ctypes.byref(out)))
+    return float(out.value)
+
+
+def launches(ctx: _lib.Context | None = None) -> int:
+    return (ctx or _lib.context()).launches()
+
+
+__all__ = ["DeviceArray", "to_device", "is_device", "pinned_empty", "relative_residual_device",
+           "launches", "c_int64"]
