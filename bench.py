@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 densolve hot path (BASELINE.json metric).
+
+Headline (``value``): CG iterations/s on a dense SPD n=32768 fp64 system
+(config C4) with A resident in HBM; one *step* = one ``cg_solve`` call with
+tolerance 1e-300 and max_iterations=ITERS (the reference's own fixed-iteration
+idiom, tests/test_krylov.py:188-191), i.e. symmetry gate + setup + ITERS
+iterations.  ``e2e`` is the same metric through the public API with pinned
+HOST buffers (A, b, x0 uploaded and x downloaded inside every step).
+``components`` adds GMRES(30) n=4096 fp64 (C2, one full cycle per step) and
+blocked LU (b=64) fp64 GFLOP/s.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+--impl reference times the reference CPU path (the NumPy restatement in
+oracle/, which makes the same NumPy/BLAS calls as the reference package) on
+the host cores, same metric and workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BASELINE_METRIC = "CG/GMRES iters/sec & HBM GB/s; LU GFLOP/s at n=32768, 1/2/4/8 B200 vs CPU"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d.get("hbm_gbs", 6551.0)), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+FP64_PEAK_TFLOPS = 37.1  # DMMA/DFMA measured on this pool (profiles/fp64_peak_r01.txt)
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([s.strip() for s in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                smax = float(r[1])
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- helpers
+def spd_fast_device(n, seed, torch, device):
+    """Synthetic dense SPD: A = (R + R^T)/2 + sqrt(n) I, R ~ U[-1,1] (seeded, on the GPU).
+    The symmetric part has a semicircle spectrum of radius ~0.82 sqrt(n), so
+    lambda(A) in ~[0.18, 1.82] sqrt(n): SPD with kappa ~ 10, which keeps a
+    fixed 100-iteration CG far from underflow (rate ~0.5 per iteration)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    A = torch.rand((n, n), dtype=torch.float64, device=device, generator=g)
+    A.mul_(2.0).sub_(1.0)
+    A.add_(A.t().clone()).mul_(0.5)
+    A.diagonal().add_(float(n) ** 0.5)
+    xt = torch.rand(n, dtype=torch.float64, device=device, generator=g).mul_(2.0).sub_(1.0)
+    b = A @ xt
+    return A, b
+
+
+def spd_fast_host(n, seed):
+    rng = np.random.default_rng([seed, n, 2])
+    A = rng.uniform(-1.0, 1.0, size=(n, n))
+    A += A.T.copy()
+    A *= 0.5
+    A[np.diag_indices(n)] += float(n) ** 0.5
+    xt = rng.uniform(-1.0, 1.0, size=n)
+    return np.asfortranarray(A), A @ xt
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import densolve_oracle as O
+
+    n, iters = args.n, args.iters
+    cores = os.cpu_count() or 1
+    A, b = spd_fast_host(n, 0)
+    x0 = np.zeros(n)
+    times = []
+    for k in range(min(args.warmup, 1) + args.steps):
+        t0 = time.perf_counter()
+        O.cg(A, b, x0, 1e-300, iters, O.Ops(threads=cores))
+        dt = time.perf_counter() - t0
+        if k >= min(args.warmup, 1):
+            times.append(dt)
+    tot = sum(times)
+    val = iters * len(times) / tot
+    line = {"impl": "reference", "metric": BASELINE_METRIC, "value": val,
+            "unit": f"CG iters/s (n={n} fp64)", "n_gpus": ws, "steps": args.steps,
+            "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"C4 CG dense SPD n={n} fp64, fixed {iters} iterations per step",
+                       "n": n, "iters_per_step": iters},
+            "cpu_baseline": {"value": val, "unit": f"CG iters/s (n={n} fp64)", "cores": cores, "kind": "port",
+                             "sample": f"oracle.cg (NumPy/OpenBLAS restatement of krylov.cg_solve incl. "
+                                       f"symmetry gate), n={n}, {iters} iterations per step"},
+            "e2e": {"value": val, "unit": f"CG iters/s (n={n} fp64)", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- B200 arm
+def cpu_baseline_sample(n, iters):
+    from oracle import densolve_oracle as O
+
+    cores = os.cpu_count() or 1
+    A, b = spd_fast_host(n, 0)
+    t0 = time.perf_counter()
+    O.cg(A, b, np.zeros(n), 1e-300, iters, O.Ops(threads=cores))
+    dt = time.perf_counter() - t0
+    del A
+    return {"value": iters / dt, "unit": f"CG iters/s (n={n} fp64)", "cores": cores, "kind": "port",
+            "sample": f"one step: oracle.cg (NumPy/OpenBLAS restatement of krylov.cg_solve incl. symmetry "
+                      f"gate) at n={n}, {iters} iterations, {dt:.1f} s"}
+
+
+def run_b200(args):
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_1511_07207_b200 import (SolverConfig, cg_solve, get_backend, gmres_solve,
+                                       lu_factor_blocked, pinned_empty)
+    from paper_1511_07207_b200.device import DeviceArray
+    from paper_1511_07207_b200.harness import ProblemSpec, generate_problem
+
+    be = get_backend("b200", device=local)
+    ctx = be.ctx
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)  # all library work on torch's stream: events see it
+    hbm_peak, peak_src = _peaks()
+    n, iters = args.n, args.iters
+    cfg = SolverConfig(tolerance=1e-300, max_iterations=iters)
+
+    if ws > 1:
+        from paper_1511_07207_b200 import distributed as D
+        return D.bench_sharded_cg(args, torch, dev, be)
+
+    # ---- inputs: synthetic SPD generated on the device, staged into a DeviceArray
+    At, bt = spd_fast_device(n, 0, torch, dev)
+    dA = DeviceArray(ctx, (n, n), np.float64)
+    assert dA.ld == n
+    ctx.lib.ds_memcpy_d2d(ctx.handle, dA.ptr, At.data_ptr(), 8 * n * n)
+    db = DeviceArray(ctx, (n,), np.float64)
+    ctx.lib.ds_memcpy_d2d(ctx.handle, db.ptr, bt.data_ptr(), 8 * n)
+    dx0 = DeviceArray(ctx, (n,), np.float64)
+    ctx.lib.ds_memset(ctx.handle, dx0.ptr, 0, 8 * n)
+    # host copies (pinned) for the end-to-end arm
+    A_h = pinned_empty((n, n), np.float64, order="F")
+    A_h_t = torch.from_numpy(A_h.reshape(-1, order="F").view(np.float64))
+    A_h_t.copy_(At.reshape(-1))  # A is symmetric: row-major bytes == column-major bytes
+    b_h = pinned_empty((n,), np.float64)
+    b_h[:] = bt.cpu().numpy()
+    x0_h = pinned_empty((n,), np.float64)
+    x0_h[:] = 0.0
+    del At
+    torch.cuda.synchronize()
+
+    # ---- headline: device-resident fixed-iteration CG steps
+    for _ in range(args.warmup):
+        cg_solve(dA, db, dx0, cfg, be)
+    torch.cuda.synchronize()
+    l0 = ctx.launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            x, rep = cg_solve(dA, db, dx0, cfg, be)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = ctx.launches() - l0
+    ms = e0.elapsed_time(e1)
+    assert rep.iterations == iters
+    value = iters * args.steps / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (GEMV stream of A): timed alone, same stream
+    from ctypes import c_void_p
+    from paper_1511_07207_b200 import _lib
+    dy = DeviceArray(ctx, (n,), np.float64)
+    R = 20
+
+    def gemv():
+        _lib.check(ctx.lib.ds_gemv(ctx.handle, _lib.DS_F64, n, n, c_void_p(dA.ptr), dA.ld,
+                                   c_void_p(db.ptr), c_void_p(dy.ptr)))
+
+    for _ in range(3):
+        gemv()
+    torch.cuda.synchronize()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record(stream)
+    for _ in range(R):
+        gemv()
+    g1.record(stream)
+    torch.cuda.synchronize()
+    gemv_ms = g0.elapsed_time(g1) / R
+    gemv_bytes = 8.0 * (n * n + 2 * n)
+    achieved = gemv_bytes / (gemv_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_gemv_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                "kernel": "gemv_partial_kernel<double,2,8> + gemv_reduce (ds_gemv)",
+                "algorithmic_bytes_per_launch": gemv_bytes, "avg_launch_ms": round(gemv_ms, 4),
+                "peak_source": peak_src,
+                "cg_iteration_GBps": round(8.0 * (n * n + 10 * n) / (ms / 1e3 / (iters * args.steps)) / 1e9, 1)}
+
+    # ---- end to end through the public API with pinned host buffers
+    for _ in range(max(1, min(args.warmup, 2))):
+        cg_solve(A_h, b_h, x0_h, cfg, be)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        x_h, rep_h = cg_solve(A_h, b_h, x0_h, cfg, be)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max(f0.elapsed_time(f1), 1e3 * (time.perf_counter() - t0))
+    e2e = {"value": iters * args.steps / (e2e_ms / 1e3), "unit": f"CG iters/s (n={n} fp64)",
+           "h2d_bytes_per_step": int(A_h.nbytes + b_h.nbytes + x0_h.nbytes),
+           "d2h_bytes_per_step": int(x_h.nbytes + 8 * (iters + 1)),
+           "ms_per_step": e2e_ms / args.steps}
+    del dA, A_h, A_h_t
+    torch.cuda.empty_cache()
+
+    components = {}
+    if not args.only_cg:
+        components["gmres"] = bench_gmres(args, torch, stream, be, generate_problem, ProblemSpec,
+                                          gmres_solve, SolverConfig)
+        components["lu"] = bench_lu(args, torch, dev, stream, be, lu_factor_blocked)
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(n, iters)
+
+    line = {"metric": BASELINE_METRIC, "value": round(value, 3), "unit": f"CG iters/s (n={n} fp64)",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded dense SPD A=(R+R^T)/2+sqrt(n)I, R~U[-1,1], kappa~10, generated on device)",
+            "config": {"workload": f"C4: CG dense SPD n={n} fp64, fixed {iters} iterations per step "
+                                   f"(tolerance 1e-300), 1 GPU", "n": n, "iters_per_step": iters,
+                       "l2_policy": f"inputs larger than L2 (A = {8 * n * n / 2**30:.1f} GiB >> 126 MB L2)",
+                       "parallelism": f"rows{ws}"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "components": components}
+    print(json.dumps(line), flush=True)
+
+
+def bench_gmres(args, torch, stream, be, generate_problem, ProblemSpec, gmres_solve, SolverConfig):
+    n, m = 4096, 30
+    A, b, _ = generate_problem(ProblemSpec(kind="general_nonsymmetric", n=n, seed=0))
+    dA, db, dx0 = be.stage_in(A, b, np.zeros_like(b))
+    cfg = SolverConfig(tolerance=1e-300, restart_m=m, max_iterations=m)
+    for _ in range(3):
+        gmres_solve(dA, db, dx0, cfg, be)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 10
+    e0.record(stream)
+    for _ in range(reps):
+        x, rep = gmres_solve(dA, db, dx0, cfg, be)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    return {"workload": f"C2: GMRES({m}) general_nonsymmetric n={n} fp64, one full cycle per step "
+                        "(residual + 30 Arnoldi steps + update + true residual)",
+            "value": round(rep.iterations / (ms / 1e3), 1), "unit": "inner iters/s", "ms_per_step": round(ms, 4)}
+
+
+def bench_lu(args, torch, dev, stream, be, lu_factor_blocked):
+    from paper_1511_07207_b200.device import DeviceArray
+
+    n = args.lu_n
+    ctx = be.ctx
+    g = torch.Generator(device=dev)
+    g.manual_seed(1)
+    At = torch.rand((n, n), dtype=torch.float64, device=dev, generator=g).mul_(2.0).sub_(1.0)
+    dA = DeviceArray(ctx, (n, n), np.float64)
+    ctx.lib.ds_memcpy_d2d(ctx.handle, dA.ptr, At.data_ptr(), 8 * n * n)
+    del At
+    torch.cuda.synchronize()
+    f = lu_factor_blocked(dA, 64, be)  # warm-up
+    del f
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    f = lu_factor_blocked(dA, 64, be)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    flops = 2.0 * n ** 3 / 3.0
+    tf = flops / (ms / 1e3) / 1e12
+    return {"workload": f"blocked LU b=64, uniform U[-1,1] n={n} fp64 (pivoting family), device-resident",
+            "value": round(tf * 1e3, 1), "unit": "GFLOP/s", "ms": round(ms, 2),
+            "fp64_peak_tflops": FP64_PEAK_TFLOPS, "frac_of_fp64_peak": round(tf / FP64_PEAK_TFLOPS, 4)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--iters", type=int, default=100)
+    ap.add_argument("--lu-n", type=int, default=16384)
+    ap.add_argument("--only-cg", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()
