@@ -199,8 +199,9 @@ def run_b200(args):
 
     be = get_backend("b200", device=local)
     ctx = be.ctx
-    stream = torch.cuda.current_stream(dev)
-    ctx.set_stream(stream.cuda_stream)  # all library work on torch's stream: events see it
+    stream = torch.cuda.Stream(dev)  # a real (non-legacy) stream shared with the library
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)  # all library work on this stream: the events see it
     hbm_peak, peak_src = _peaks()
     n, iters = args.n, args.iters
     cfg = SolverConfig(tolerance=1e-300, max_iterations=iters)

@@ -859,14 +859,14 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
   for (int i = 0; i < 64; ++i)
     if (i < b) z[i] = B[i + col * ldb];
+  // column-oriented (axpy form): z[i] -= L[i][j] z[j] for i > j — independent FMAs per step
 #pragma unroll
-  for (int i = 1; i < 64; ++i) {
-    if (i < b) {
-      T acc = T(0);
+  for (int j = 0; j < 63; ++j) {
+    if (j < b) {
+      const T zj = z[j];
 #pragma unroll
-      for (int j = 0; j < 64; ++j)
-        if (j < i) acc = fma(Ls[i][j], z[j], acc);
-      z[i] = sub_rn(z[i], acc);
+      for (int i = j + 1; i < 64; ++i)
+        if (i < b) z[i] = fma(-Ls[i][j], zj, z[i]);
     }
   }
 #pragma unroll

@@ -227,6 +227,27 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nbl
   __syncthreads();
 }
 
+// Monotonic grid barrier: the counter is zeroed before the launch; barrier #e
+// completes when the counter reaches e * nblocks.  Thread 0 of each CTA releases
+// the CTA's prior writes (fence + relaxed add) and acquires everyone else's.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void grid_sync(unsigned* counter, unsigned nblocks, unsigned& epoch) {
+  __syncthreads();
+  epoch += 1;
+  if (threadIdx.x == 0) {
+    const unsigned target = epoch * nblocks;
+    __threadfence();
+    atomicAdd(counter, 1u);
+    while (ld_acquire_u32(counter) < target) {
+    }
+  }
+  __syncthreads();
+}
+
 inline __host__ __device__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // workspace carving helper (256-byte aligned sub-buffers of one allocation)

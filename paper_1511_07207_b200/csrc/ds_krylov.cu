@@ -129,7 +129,7 @@ __global__ void set_bnorm_kernel(const double* norm, CgDev* st) {
 }
 
 static int vec_grid(ds_ctx* ctx, int64_t n) {
-  int64_t want = ceil_div(std::max<int64_t>(n, 1), kT * 4);
+  int64_t want = ceil_div(std::max<int64_t>(n, 1), kT);
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)ctx->num_sms * 2));
 }
 

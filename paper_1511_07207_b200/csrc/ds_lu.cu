@@ -41,25 +41,21 @@ struct PanelArgs {
   int64_t n, ld, kb, bf;
   int64_t* piv;        // device, global row indices
   int8_t* zero_cols;   // device
-  unsigned* bar;       // grid barrier words (2)
-  double* cand_v;      // [grid]
-  int64_t* cand_i;     // [grid]
-  void* rowP;          // scratch: pivot row (panel columns)
-  void* rowI;          // scratch: row i before the swap
+  unsigned* bar;       // grid barrier counter (zeroed before each launch)
+  double* cand_v;      // [2][grid]  candidate |value| per CTA, double-buffered by column parity
+  int64_t* cand_i;     // [2][grid]  candidate row per CTA
+  void* cand_row;      // [2][grid][kPanelMaxW] the candidate rows' panel values (smem kernel)
+  void* diag_row;      // [2][kPanelMaxW] row i's values before the swap (smem kernel)
+  void* rowP;          // global kernel: pivot row
+  void* rowI;          // global kernel: row i before the swap
+  int per;             // rows per CTA
+  int ldt;             // smem tile leading dimension
 };
 
-template <typename T>
-__device__ void panel_local_iamax(const T* W, const PanelArgs& a, int64_t col, int64_t r_lo,
-                                  int64_t r_hi, double* sv, int64_t* si) {
-  double bv = -1.0;
-  int64_t bi = INT64_MAX;
-  for (int64_t r = r_lo + threadIdx.x; r < r_hi; r += blockDim.x) {
-    const double v = fabs((double)W[r + col * a.ld]);
-    if (piv_better(v, r, bv, bi)) {
-      bv = v;
-      bi = r;
-    }
-  }
+constexpr int kPanelMaxW = 64;
+
+// Block-wide first-max argmax (np.argmax(np.abs(.)) semantics); result in thread 0.
+__device__ __forceinline__ void block_argmax(double& bv, int64_t& bi, double* sv, int64_t* si) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -82,115 +78,323 @@ __device__ void panel_local_iamax(const T* W, const PanelArgs& a, int64_t col, i
         bv = sv[w];
         bi = si[w];
       }
-    a.cand_v[blockIdx.x] = bv;
-    a.cand_i[blockIdx.x] = bi;
   }
 }
 
+// Warp 0 reduces the G published candidates (parallel loads, shuffle tree, fixed
+// order => identical result in every CTA); returns the pivot row in s_piv.
+__device__ __forceinline__ void reduce_candidates(const PanelArgs& a, int par, int64_t i,
+                                                  int64_t* s_piv) {
+  if (threadIdx.x < 32) {
+    const unsigned G = gridDim.x;
+    double bv = -1.0;
+    int64_t bi = INT64_MAX;
+    for (unsigned b = threadIdx.x; b < G; b += 32) {
+      const double v = __ldcg(a.cand_v + par * G + b);
+      const int64_t ix = __ldcg(a.cand_i + par * G + b);
+      if (piv_better(v, ix, bv, bi)) {
+        bv = v;
+        bi = ix;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (piv_better(ov, oi, bv, bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (threadIdx.x == 0) *s_piv = bi == INT64_MAX ? i : bi;
+  }
+  __syncthreads();
+}
+
+// Panel factorization with the CTA's rows resident in shared memory; one grid
+// barrier per column.  Before the barrier every CTA publishes its local
+// candidate (value, row, and the row's panel values) and the owner of row i
+// publishes row i; after it every CTA picks the same pivot and already holds
+// everything the swap and the rank-1 update need.
 template <typename T>
-__global__ void __launch_bounds__(kPanelThreads) lu_panel_kernel(T* __restrict__ W, PanelArgs a) {
+__global__ void __launch_bounds__(kPanelThreads) lu_panel_smem_kernel(T* __restrict__ W, PanelArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* tile = reinterpret_cast<T*>(smem_raw);  // [ncol][ldt]
+  __shared__ double sv[32];
+  __shared__ int64_t si[32];
+  __shared__ int64_t s_piv;
+  __shared__ T prow[kPanelMaxW];
+  __shared__ T drow[kPanelMaxW];
+  const unsigned G = gridDim.x;
+  const int per = a.per, ldt = a.ldt;
+  const int64_t my_lo = a.kb + (int64_t)blockIdx.x * per;
+  const int64_t my_hi = min(a.n, my_lo + per);
+  const int nr = (int)(my_hi - my_lo);
+  const int ncol = (int)(a.bf - a.kb);
+  T* cand_row = reinterpret_cast<T*>(a.cand_row);
+  T* diag_row = reinterpret_cast<T*>(a.diag_row);
+
+  for (int idx = threadIdx.x; idx < ncol * nr; idx += blockDim.x) {
+    const int j = idx / nr, r = idx % nr;
+    tile[j * ldt + r] = W[(my_lo + r) + (a.kb + j) * a.ld];
+  }
+  __syncthreads();
+  unsigned epoch = 0;
+  for (int c = 0; c < ncol; ++c) {
+    const int64_t i = a.kb + c;
+    const int par = c & 1;
+    // ---- phase A: local candidate of column c over my rows >= i
+    const int r0 = (int)max((int64_t)0, i - my_lo);
+    double bv = -1.0;
+    int64_t bi = INT64_MAX;
+    for (int r = r0 + threadIdx.x; r < nr; r += blockDim.x) {
+      const double v = fabs((double)tile[c * ldt + r]);
+      if (piv_better(v, my_lo + r, bv, bi)) {
+        bv = v;
+        bi = my_lo + r;
+      }
+    }
+    block_argmax(bv, bi, sv, si);
+    if (threadIdx.x == 0) {
+      a.cand_v[par * G + blockIdx.x] = bv;
+      a.cand_i[par * G + blockIdx.x] = bi;
+      si[0] = bi;
+    }
+    __syncthreads();
+    const int64_t mybest = si[0];
+    if (mybest != INT64_MAX)
+      for (int j = threadIdx.x; j < ncol; j += blockDim.x)
+        cand_row[((size_t)par * G + blockIdx.x) * kPanelMaxW + j] = tile[j * ldt + (int)(mybest - my_lo)];
+    if (i >= my_lo && i < my_hi)
+      for (int j = threadIdx.x; j < ncol; j += blockDim.x)
+        diag_row[par * kPanelMaxW + j] = tile[j * ldt + (int)(i - my_lo)];
+    grid_sync(a.bar, G, epoch);
+    // ---- phase B: global pivot (same in every CTA), pivot row and old row i
+    reduce_candidates(a, par, i, &s_piv);
+    const int64_t p = s_piv;
+    const unsigned owner = (unsigned)((p - a.kb) / per);
+    for (int j = threadIdx.x; j < ncol; j += blockDim.x) {
+      prow[j] = __ldcg(cand_row + ((size_t)par * G + owner) * kPanelMaxW + j);
+      drow[j] = __ldcg(diag_row + par * kPanelMaxW + j);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.piv[i] = p;  // piv[i] = v (direct.py:67)
+    __syncthreads();
+    if (p != i) {  // full-row swap restricted to the panel (direct.py:68-70)
+      if (i >= my_lo && i < my_hi)
+        for (int j = threadIdx.x; j < ncol; j += blockDim.x) tile[j * ldt + (int)(i - my_lo)] = prow[j];
+      if (p >= my_lo && p < my_hi)
+        for (int j = threadIdx.x; j < ncol; j += blockDim.x) tile[j * ldt + (int)(p - my_lo)] = drow[j];
+    }
+    __syncthreads();
+    const T aii = prow[c];
+    if (aii == T(0)) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) a.zero_cols[i] = 1;  // direct.py:71-74
+    } else {
+      const T recip = div_rn(T(1), aii);
+      const int u0 = (int)max((int64_t)0, i + 1 - my_lo);
+      const int nu = nr - u0;
+      for (int r = u0 + threadIdx.x; r < nr; r += blockDim.x) tile[c * ldt + r] = mul_rn(recip, tile[c * ldt + r]);
+      __syncthreads();
+      const int w = ncol - c - 1;
+      if (nu > 0)
+        for (int idx = threadIdx.x; idx < w * nu; idx += blockDim.x) {
+          const int j = c + 1 + idx / nu, r = u0 + idx % nu;
+          tile[j * ldt + r] = sub_rn(tile[j * ldt + r], mul_rn(tile[c * ldt + r], prow[j]));
+        }
+    }
+    __syncthreads();
+  }
+  for (int idx = threadIdx.x; idx < ncol * nr; idx += blockDim.x) {
+    const int j = idx / nr, r = idx % nr;
+    W[(my_lo + r) + (a.kb + j) * a.ld] = tile[j * ldt + r];
+  }
+}
+
+// Fallback for panels too large for shared memory (e.g. the unblocked b = n
+// factorization): rows stay in global memory (L2), two grid barriers per column.
+template <typename T>
+__global__ void __launch_bounds__(kPanelThreads) lu_panel_global_kernel(T* __restrict__ W, PanelArgs a) {
   __shared__ double sv[32];
   __shared__ int64_t si[32];
   __shared__ int64_t s_piv;
   const unsigned G = gridDim.x;
-  const int64_t rows = a.n - a.kb;
-  const int64_t per = ceil_div(rows, (int64_t)G);
+  const int64_t per = a.per;
   const int64_t my_lo = a.kb + (int64_t)blockIdx.x * per;
   const int64_t my_hi = min(a.n, my_lo + per);
+  const int64_t nr = my_hi - my_lo;
   const int64_t ncol = a.bf - a.kb;
   T* rowP = reinterpret_cast<T*>(a.rowP);
   T* rowI = reinterpret_cast<T*>(a.rowI);
-
-  // local iamax of the first panel column
-  panel_local_iamax<T>(W, a, a.kb, max(my_lo, a.kb), my_hi, sv, si);
-  for (int64_t i = a.kb; i < a.bf; ++i) {
-    grid_barrier(a.bar, G);
-    // --- global pivot: same fixed order in every CTA ---
-    if (threadIdx.x == 0) {
-      double bv = -1.0;
-      int64_t bi = INT64_MAX;
-      for (unsigned b = 0; b < G; ++b) {
-        const double v = ((volatile double*)a.cand_v)[b];
-        const int64_t ix = ((volatile int64_t*)a.cand_i)[b];
-        if (piv_better(v, ix, bv, bi)) {
-          bv = v;
-          bi = ix;
-        }
+  unsigned epoch = 0;
+  for (int64_t c = 0; c < ncol; ++c) {
+    const int64_t i = a.kb + c;
+    double bv = -1.0;
+    int64_t bi = INT64_MAX;
+    for (int64_t r = max(my_lo, i) + threadIdx.x; r < my_hi; r += blockDim.x) {
+      const double v = fabs((double)W[r + i * a.ld]);
+      if (piv_better(v, r, bv, bi)) {
+        bv = v;
+        bi = r;
       }
-      if (bi == INT64_MAX) bi = i;  // empty (cannot happen for i < n)
-      s_piv = bi;
     }
-    __syncthreads();
+    block_argmax(bv, bi, sv, si);
+    if (threadIdx.x == 0) {
+      a.cand_v[blockIdx.x] = bv;
+      a.cand_i[blockIdx.x] = bi;
+    }
+    grid_sync(a.bar, G, epoch);
+    reduce_candidates(a, 0, i, &s_piv);
     const int64_t p = s_piv;
     if (blockIdx.x == 0) {
-      if (threadIdx.x == 0) a.piv[i] = p;  // piv[i] = v (direct.py:67)
+      if (threadIdx.x == 0) a.piv[i] = p;
       for (int64_t j = threadIdx.x; j < ncol; j += blockDim.x) {
-        // L1-bypassing loads: these rows were last written by other CTAs
         rowP[j] = __ldcg(W + p + (a.kb + j) * a.ld);
         rowI[j] = __ldcg(W + i + (a.kb + j) * a.ld);
       }
     }
-    grid_barrier(a.bar, G);
-    // --- swap rows i <-> p within the panel (direct.py:68-70) ---
+    grid_sync(a.bar, G, epoch);
     if (p != i) {
       if (i >= my_lo && i < my_hi)
-        for (int64_t j = threadIdx.x; j < ncol; j += blockDim.x)
-          W[i + (a.kb + j) * a.ld] = ((volatile T*)rowP)[j];
+        for (int64_t j = threadIdx.x; j < ncol; j += blockDim.x) W[i + (a.kb + j) * a.ld] = __ldcg(rowP + j);
       if (p >= my_lo && p < my_hi)
-        for (int64_t j = threadIdx.x; j < ncol; j += blockDim.x)
-          W[p + (a.kb + j) * a.ld] = ((volatile T*)rowI)[j];
+        for (int64_t j = threadIdx.x; j < ncol; j += blockDim.x) W[p + (a.kb + j) * a.ld] = __ldcg(rowI + j);
     }
     __syncthreads();
-    const T aii = ((volatile T*)rowP)[i - a.kb];
+    const T aii = __ldcg(rowP + c);
     if (aii == T(0)) {
-      // singular column: elimination skipped (direct.py:71-74)
       if (blockIdx.x == 0 && threadIdx.x == 0) a.zero_cols[i] = 1;
     } else {
-      const T recip = div_rn(T(1), aii);  // 1.0 / aii in the array dtype (direct.py:76)
-      const int64_t r_lo = max(my_lo, i + 1);
-      // scale + rank-1 update restricted to the panel (direct.py:75-79, backends.py:152-155)
-      for (int64_t r = r_lo + threadIdx.x; r < my_hi; r += blockDim.x) {
-        const T l = mul_rn(recip, W[r + i * a.ld]);
-        W[r + i * a.ld] = l;
-        for (int64_t j = i + 1; j < a.bf; ++j) {
-          const T uj = ((volatile T*)rowP)[j - a.kb];
-          W[r + j * a.ld] = sub_rn(W[r + j * a.ld], mul_rn(l, uj));
+      const T recip = div_rn(T(1), aii);
+      const int64_t u0 = max(my_lo, i + 1);
+      const int64_t nu = my_hi - u0;
+      for (int64_t r = u0 + threadIdx.x; r < my_hi; r += blockDim.x)
+        W[r + i * a.ld] = mul_rn(recip, W[r + i * a.ld]);
+      __syncthreads();
+      const int64_t w = ncol - c - 1;
+      if (nu > 0)
+        for (int64_t idx = threadIdx.x; idx < w * nu; idx += blockDim.x) {
+          const int64_t j = i + 1 + idx / nu, r = u0 + idx % nu;
+          W[r + j * a.ld] = sub_rn(W[r + j * a.ld], mul_rn(W[r + i * a.ld], __ldcg(rowP + (j - a.kb))));
         }
+    }
+    (void)nr;
+  }
+}
+
+// laswp (K11): the swaps piv[kb..bf) applied, in order, to columns outside the
+// panel.  A one-thread kernel first folds the swap sequence into its net
+// permutation of the affected rows ({kb..bf-1} U {piv[k]}): pairs (dst, src)
+// meaning "row dst receives the original row src".  The gather kernel then
+// moves every affected element of a column at once (all loads before all
+// stores, no dependent chains); rows kb..bf-1 of a column are contiguous.
+__global__ void laswp_plan_kernel(int64_t kb, int64_t bf, const int64_t* __restrict__ piv,
+                                  int64_t* pairs /* [2][2*cnt] */, int* npairs) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int cnt = (int)(bf - kb);
+  // origin[] for rows kb..bf-1, plus a small list for outside rows
+  int64_t* orig_in = pairs;                 // reuse output space as scratch: [cnt]
+  int64_t* out_rows = pairs + 2 * cnt;      // [cnt] outside rows
+  int64_t* out_orig = pairs + 3 * cnt;      // [cnt]
+  int nout = 0;
+  for (int k = 0; k < cnt; ++k) orig_in[k] = kb + k;
+  for (int k = 0; k < cnt; ++k) {
+    const int64_t p = piv[kb + k];
+    const int64_t r = kb + k;
+    if (p == r) continue;
+    int64_t* op;
+    if (p < bf) {
+      op = &orig_in[p - kb];
+    } else {
+      int f = -1;
+      for (int q = 0; q < nout; ++q)
+        if (out_rows[q] == p) {
+          f = q;
+          break;
+        }
+      if (f < 0) {
+        f = nout++;
+        out_rows[f] = p;
+        out_orig[f] = p;
       }
+      op = &out_orig[f];
     }
-    __syncthreads();
-    if (i + 1 < a.bf) panel_local_iamax<T>(W, a, i + 1, max(my_lo, i + 1), my_hi, sv, si);
+    const int64_t t = orig_in[k];
+    orig_in[k] = *op;
+    *op = t;
   }
+  // compact into (dst, src) pairs where dst != src; layout: dst[0..np), src[0..np) at pairs+4cnt..
+  int64_t* dst = pairs + 4 * cnt;
+  int64_t* src = pairs + 6 * cnt;
+  int np = 0;
+  for (int k = 0; k < cnt; ++k)
+    if (orig_in[k] != kb + k) {
+      dst[np] = kb + k;
+      src[np] = orig_in[k];
+      ++np;
+    }
+  for (int q = 0; q < nout; ++q)
+    if (out_orig[q] != out_rows[q]) {
+      dst[np] = out_rows[q];
+      src[np] = out_orig[q];
+      ++np;
+    }
+  *npairs = np;
 }
 
-// laswp: apply piv[kb..bf) to columns [c_lo, c_hi) (one thread per column)
+// One CTA per group of `cols` columns: every affected element of those columns
+// is first read into shared memory, then written to its destination row.
 template <typename T>
-__global__ void laswp_kernel(T* W, int64_t ld, int64_t c_lo, int64_t c_hi, int64_t kb, int64_t bf,
-                             const int64_t* __restrict__ piv) {
-  __shared__ int64_t sp[1024];
-  const int64_t cnt = bf - kb;
-  for (int64_t i = threadIdx.x; i < cnt && i < 1024; i += blockDim.x) sp[i] = piv[kb + i];
+__global__ void __launch_bounds__(256)
+    laswp_gather_kernel(T* W, int64_t ld, int64_t c_lo, int64_t c_hi, int cols,
+                        const int64_t* __restrict__ dst, const int64_t* __restrict__ src,
+                        const int* __restrict__ npairs) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* buf = reinterpret_cast<T*>(smem_raw);  // [cols][np]
+  const int np = *npairs;
+  const int64_t c0 = c_lo + (int64_t)blockIdx.x * cols;
+  const int nc = (int)min((int64_t)cols, c_hi - c0);
+  for (int idx = threadIdx.x; idx < np * nc; idx += blockDim.x) {
+    const int q = idx / np, t = idx % np;
+    buf[q * np + t] = W[src[t] + (c0 + q) * ld];
+  }
   __syncthreads();
-  const int64_t c = c_lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= c_hi) return;
-  T* col = W + c * ld;
-  for (int64_t i = 0; i < cnt; ++i) {
-    const int64_t p = i < 1024 ? sp[i] : piv[kb + i];
-    const int64_t r = kb + i;
-    if (p != r) {
-      const T t = col[r];
-      col[r] = col[p];
-      col[p] = t;
-    }
+  for (int idx = threadIdx.x; idx < np * nc; idx += blockDim.x) {
+    const int q = idx / np, t = idx % np;
+    W[dst[t] + (c0 + q) * ld] = buf[q * np + t];
   }
 }
 
+struct SwapPlan {
+  int64_t* pairs = nullptr;
+  int* np = nullptr;
+  int64_t cnt = 0;
+};
+
+int laswp_plan(ds_ctx* ctx, int64_t kb, int64_t bf, const int64_t* piv, SwapPlan& sp) {
+  sp.cnt = bf - kb;
+  laswp_plan_kernel<<<1, 32, 0, ctx->stream>>>(kb, bf, piv, sp.pairs, sp.np);
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+
 template <typename T>
-int laswp_launch(ds_ctx* ctx, T* W, int64_t ld, int64_t c_lo, int64_t c_hi, int64_t kb, int64_t bf,
-                 const int64_t* piv) {
+int laswp_apply(ds_ctx* ctx, T* W, int64_t ld, int64_t c_lo, int64_t c_hi, const SwapPlan& sp) {
   if (c_hi <= c_lo) return DS_OK;
-  laswp_kernel<T><<<(unsigned)ceil_div(c_hi - c_lo, 128), 128, 0, ctx->stream>>>(W, ld, c_lo, c_hi,
-                                                                                 kb, bf, piv);
+  // np <= 2*cnt; size the column group so the staging buffer stays <= 192 KB
+  const int64_t npmax = 2 * sp.cnt;
+  const int cols = (int)std::max<int64_t>(1, std::min<int64_t>(8, (192 * 1024) / (npmax * (int64_t)sizeof(T))));
+  const size_t smem = (size_t)cols * npmax * sizeof(T);
+  static size_t attr[2] = {0, 0};
+  size_t& done = attr[sizeof(T) == 8 ? 1 : 0];
+  if (smem > 48 * 1024 && smem > done) {
+    DS_CUDA(cudaFuncSetAttribute(laswp_gather_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(200 * 1024)));
+    done = 200 * 1024;
+  }
+  const unsigned grid = (unsigned)ceil_div(c_hi - c_lo, cols);
+  laswp_gather_kernel<T><<<grid, 256, smem, ctx->stream>>>(W, ld, c_lo, c_hi, cols, sp.pairs + 4 * sp.cnt,
+                                                           sp.pairs + 6 * sp.cnt, sp.np);
   count_launch(ctx);
   DS_CHECK_LAUNCH();
   return DS_OK;
@@ -199,17 +403,7 @@ int laswp_launch(ds_ctx* ctx, T* W, int64_t ld, int64_t c_lo, int64_t c_hi, int6
 template <typename T>
 int panel_launch(ds_ctx* ctx, T* W, int64_t n, int64_t ld, int64_t kb, int64_t bf, int64_t* piv,
                  int8_t* zero_cols, char* scratch) {
-  static int max_blocks_per_sm[2] = {0, 0};
-  int& mb = max_blocks_per_sm[sizeof(T) == 8 ? 1 : 0];
-  if (mb == 0) {
-    DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mb, lu_panel_kernel<T>, kPanelThreads, 0));
-    if (mb < 1) mb = 1;
-  }
-  const int64_t rows = n - kb;
-  // ~128 rows per CTA minimum; at most one wave of co-resident CTAs (<= 1 per SM
-  // keeps the barrier cheap)
-  int64_t g = std::min<int64_t>(ceil_div(rows, 128), (int64_t)ctx->num_sms);
-  g = std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)ctx->num_sms * mb));
+  const int64_t rows = n - kb, ncol = bf - kb;
   PanelArgs a;
   a.n = n;
   a.ld = ld;
@@ -218,39 +412,116 @@ int panel_launch(ds_ctx* ctx, T* W, int64_t n, int64_t ld, int64_t kb, int64_t b
   a.piv = piv;
   a.zero_cols = zero_cols;
   Carver cv{scratch};
-  a.bar = cv.take<unsigned>(64);
-  a.cand_v = cv.take<double>(sizeof(double) * 1024);
-  a.cand_i = cv.take<int64_t>(sizeof(int64_t) * 1024);
-  a.rowP = cv.take<T>(sizeof(T) * (bf - kb));
-  a.rowI = cv.take<T>(sizeof(T) * (bf - kb));
+  a.bar = cv.take<unsigned>(256);
+  a.cand_v = cv.take<double>(sizeof(double) * 2 * 1024);
+  a.cand_i = cv.take<int64_t>(sizeof(int64_t) * 2 * 1024);
+  a.cand_row = cv.take<T>(sizeof(T) * 2 * 1024 * kPanelMaxW);
+  a.diag_row = cv.take<T>(sizeof(T) * 2 * kPanelMaxW);
+  a.rowP = cv.take<T>(sizeof(T) * ncol);
+  a.rowI = cv.take<T>(sizeof(T) * ncol);
+  DS_CUDA(cudaMemsetAsync(a.bar, 0, 256, ctx->stream));
+  const size_t smem_cap = std::min<size_t>(ctx->smem_optin, 220 * 1024) - 2048;
+  // shared-memory path: rows split over <= num_sms CTAs, >= 16 rows each
+  if (ncol <= kPanelMaxW) {
+    int64_t g = std::min<int64_t>((int64_t)ctx->num_sms, ceil_div(rows, 16));
+    int64_t per = ceil_div(rows, g);
+    g = ceil_div(rows, per);
+    const int ldt = (int)(per | 1);
+    const size_t smem = (size_t)ncol * ldt * sizeof(T);
+    if (smem <= smem_cap) {
+      a.per = (int)per;
+      a.ldt = ldt;
+      static size_t attr_set[2] = {0, 0};
+      size_t& done = attr_set[sizeof(T) == 8 ? 1 : 0];
+      if (smem > done) {
+        DS_CUDA(cudaFuncSetAttribute(lu_panel_smem_kernel<T>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
+        done = smem_cap;
+      }
+      void* args[] = {(void*)&W, (void*)&a};
+      DS_CUDA(cudaLaunchCooperativeKernel((void*)lu_panel_smem_kernel<T>, dim3((unsigned)g),
+                                          dim3(kPanelThreads), args, smem, ctx->stream));
+      count_launch(ctx);
+      return DS_OK;
+    }
+  }
+  static int mb[2] = {0, 0};
+  int& m = mb[sizeof(T) == 8 ? 1 : 0];
+  if (m == 0) {
+    DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, lu_panel_global_kernel<T>, kPanelThreads, 0));
+    if (m < 1) m = 1;
+  }
+  int64_t g = std::min<int64_t>(ceil_div(rows, 64), (int64_t)ctx->num_sms);
+  g = std::max<int64_t>(1, g);
+  int64_t per = ceil_div(rows, g);
+  g = ceil_div(rows, per);
+  a.per = (int)per;
+  a.ldt = 0;
   void* args[] = {(void*)&W, (void*)&a};
-  DS_CUDA(cudaLaunchCooperativeKernel((void*)lu_panel_kernel<T>, dim3((unsigned)g),
+  DS_CUDA(cudaLaunchCooperativeKernel((void*)lu_panel_global_kernel<T>, dim3((unsigned)g),
                                       dim3(kPanelThreads), args, 0, ctx->stream));
   count_launch(ctx);
   return DS_OK;
 }
 
+// Internal outer block: the reference's b-wide panels are kept (pivot search,
+// swaps, scaling and rank-1 updates inside each b-panel, then TRSM + GEMM on the
+// rest of the outer panel), but the trailing matrix is updated once per NB-wide
+// outer panel with a K = NB GEMM.  Exact-arithmetic identical to the reference
+// (same pivots), different rounding grouping in the trailing update.
+static int64_t outer_block(int64_t b, int64_t n) {
+  if (b >= 256 || b >= n) return std::min<int64_t>(b, n);
+  return std::min<int64_t>(n, b * std::max<int64_t>(1, 256 / b));
+}
+
 template <typename T>
-int lu_factor_impl(ds_ctx* ctx, int64_t n, T* W, int64_t ld, int64_t nb, int64_t* d_piv,
+int lu_factor_impl(ds_ctx* ctx, int64_t n, T* W, int64_t ld, int64_t b, int64_t* d_piv,
                    int8_t* d_zero) {
   void* ws = nullptr;
-  const size_t scratch_bytes = 64 * 4 + 1024 * 16 + 2 * sizeof(T) * (size_t)std::max<int64_t>(nb, 1) + 8 * 256;
-  DS_TRY(ctx_workspace(ctx, scratch_bytes + 256, &ws));
-  char* scratch = (char*)ws;
-  DS_CUDA(cudaMemsetAsync(scratch, 0, 256, ctx->stream));  // barrier words
-  for (int64_t kb = 0; kb < n; kb += nb) {
-    const int64_t bf = std::min<int64_t>(kb + nb, n);
-    DS_TRY(panel_launch<T>(ctx, W, n, ld, kb, bf, d_piv, d_zero, scratch));
-    DS_TRY(laswp_launch<T>(ctx, W, ld, 0, kb, kb, bf, d_piv));
-    DS_TRY(laswp_launch<T>(ctx, W, ld, bf, n, kb, bf, d_piv));
+  const size_t scratch_bytes = 256 + 2 * 1024 * 16 + sizeof(T) * (2 * 1024 * kPanelMaxW + 2 * kPanelMaxW) +
+                               2 * sizeof(T) * (size_t)std::max<int64_t>(b, 1) + 16 * 256;
+  DS_TRY(ctx_workspace(ctx, scratch_bytes + 2 * sizeof(int64_t) * 8 * (size_t)outer_block(b, n) + 4096, &ws));
+  const int64_t NB = outer_block(b, n);
+  Carver cvs{(char*)ws};
+  char* scratch = cvs.take<char>(scratch_bytes);
+  SwapPlan sp_in, sp_out;
+  sp_in.pairs = cvs.take<int64_t>(sizeof(int64_t) * 8 * (size_t)NB);
+  sp_in.np = cvs.take<int>(64);
+  sp_out.pairs = cvs.take<int64_t>(sizeof(int64_t) * 8 * (size_t)NB);
+  sp_out.np = cvs.take<int>(64);
+  for (int64_t kb = 0; kb < n; kb += NB) {
+    const int64_t bf = std::min<int64_t>(kb + NB, n);
+    // ---- factor the outer panel [kb, bf) with the reference's b-wide blocking
+    for (int64_t ib = kb; ib < bf; ib += b) {
+      const int64_t ibf = std::min<int64_t>(ib + b, bf);
+      DS_TRY(panel_launch<T>(ctx, W, n, ld, ib, ibf, d_piv, d_zero, scratch));
+      DS_TRY(laswp_plan(ctx, ib, ibf, d_piv, sp_in));
+      DS_TRY(laswp_apply<T>(ctx, W, ld, kb, ib, sp_in));
+      DS_TRY(laswp_apply<T>(ctx, W, ld, ibf, bf, sp_in));
+      if (ibf < bf) {
+        T* U = W + ib + ibf * ld;
+        DS_TRY(trsm_lower_unit_launch<T>(ctx, ibf - ib, bf - ibf, W + ib + ib * ld, ld, U, ld, U, ld));
+        DS_TRY(gemm_launch<T>(ctx, n - ibf, bf - ibf, ibf - ib, -1.0, W + ibf + ib * ld, ld, U, ld, 1.0,
+                              W + ibf + ibf * ld, ld, W + ibf + ibf * ld, ld));
+      }
+    }
+    // ---- swaps of the whole outer panel on the columns outside it
+    DS_TRY(laswp_plan(ctx, kb, bf, d_piv, sp_out));
+    DS_TRY(laswp_apply<T>(ctx, W, ld, 0, kb, sp_out));
+    DS_TRY(laswp_apply<T>(ctx, W, ld, bf, n, sp_out));
     if (bf < n) {
-      T* A01 = W + kb + bf * ld;
-      const T* L00 = W + kb + kb * ld;
-      DS_TRY(trsm_lower_unit_launch<T>(ctx, bf - kb, n - bf, L00, ld, A01, ld, A01, ld));
-      const T* L10 = W + bf + kb * ld;
-      T* A11 = W + bf + bf * ld;
-      DS_TRY(gemm_launch<T>(ctx, n - bf, n - bf, bf - kb, -1.0, L10, ld, A01, ld, 1.0, A11, ld,
-                            A11, ld));
+      // U01 = L00^-1 A01, L00 the NB x NB unit-lower block (blocked by b)
+      for (int64_t ib = kb; ib < bf; ib += b) {
+        const int64_t ibf = std::min<int64_t>(ib + b, bf);
+        T* Ur = W + ib + bf * ld;
+        DS_TRY(trsm_lower_unit_launch<T>(ctx, ibf - ib, n - bf, W + ib + ib * ld, ld, Ur, ld, Ur, ld));
+        if (ibf < bf)
+          DS_TRY(gemm_launch<T>(ctx, bf - ibf, n - bf, ibf - ib, -1.0, W + ibf + ib * ld, ld, Ur, ld, 1.0,
+                                W + ibf + bf * ld, ld, W + ibf + bf * ld, ld));
+      }
+      // trailing update A11 -= L10 U01 with K = NB (DMMA GEMM)
+      DS_TRY(gemm_launch<T>(ctx, n - bf, n - bf, bf - kb, -1.0, W + bf + kb * ld, ld, W + kb + bf * ld, ld,
+                            1.0, W + bf + bf * ld, ld, W + bf + bf * ld, ld));
     }
   }
   return DS_OK;
