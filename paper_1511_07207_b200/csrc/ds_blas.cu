@@ -649,12 +649,28 @@ __global__ void __launch_bounds__(gemm64::THREADS, 2)
   const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
   const int g = lane >> 2, t = lane & 3;
 
+  // MODE 1 (out = C - A B, the LU update): the accumulators start from C (loaded
+  // before the main loop, so its latency hides under the cp.async prologue) and
+  // the A fragments are negated, making the epilogue store-only.
   double acc[8][4][2];
+  if (MODE == 1) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < 8; ++i) {
+      const int64_t r = m0 + wm * 64 + i * 8 + g;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t c = n0 + wn * 32 + j * 8 + 2 * t + e;
+          acc[i][j][e] = (r < m && c < n) ? C[r + c * ldc] : 0.0;
+        }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  }
   const int64_t ktiles = ceil_div(k, BK);
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
@@ -681,7 +697,7 @@ __global__ void __launch_bounds__(gemm64::THREADS, 2)
     for (int kk = 0; kk < BK; kk += 4) {
       double a[8], b[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = as[(kk + t) * LDA_S + i * 8];
+      for (int i = 0; i < 8; ++i) a[i] = MODE == 1 ? -as[(kk + t) * LDA_S + i * 8] : as[(kk + t) * LDA_S + i * 8];
 #pragma unroll
       for (int j = 0; j < 4; ++j) b[j] = bs[j * 8 * LDB_S + kk];
 #pragma unroll
@@ -691,24 +707,35 @@ __global__ void __launch_bounds__(gemm64::THREADS, 2)
     }
   }
   cp_async_wait<0>();
-  // epilogue: out = beta*C + alpha*acc (NumPy rounding, backends.py:244); MODE 1 = C - acc
+  // epilogue.  MODE 1: acc already holds C - A B.  MODE 0: out = beta*C + alpha*acc
+  // with NumPy's rounding (backends.py:244); C is read in one batch per row group
+  // before any store so the loads overlap.
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const int64_t r = m0 + wm * 64 + i * 8 + g;
     if (r >= m) continue;
+    double cv[4][2];
+    if (MODE == 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t c = n0 + wn * 32 + j * 8 + 2 * t + e;
+          cv[j][e] = (c < n && beta != 0.0) ? C[r + c * ldc] : 0.0;
+        }
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int64_t c = n0 + wn * 32 + j * 8 + 2 * t + e;
         if (c >= n) continue;
-        const double v = acc[i][j][e];
         double o;
         if (MODE == 1) {
-          o = __dsub_rn(C[r + c * ldc], v);
+          o = acc[i][j][e];
         } else {
-          const double cb = beta == 0.0 ? 0.0 : __dmul_rn(beta, C[r + c * ldc]);
-          o = __dadd_rn(cb, __dmul_rn(alpha, v));
+          const double cb = beta == 0.0 ? 0.0 : __dmul_rn(beta, cv[j][e]);
+          o = __dadd_rn(cb, __dmul_rn(alpha, acc[i][j][e]));
         }
         out[r + c * ldo] = o;
       }
@@ -859,14 +886,18 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
   for (int i = 0; i < 64; ++i)
     if (i < b) z[i] = B[i + col * ldb];
-  // column-oriented (axpy form): z[i] -= L[i][j] z[j] for i > j — independent FMAs per step
+  // z_i = b_i - (L[i,:i] . z[:i])  (dot form of backends.py:184-185); two partial
+  // accumulators halve the dependent FMA chain
 #pragma unroll
-  for (int j = 0; j < 63; ++j) {
-    if (j < b) {
-      const T zj = z[j];
+  for (int i = 1; i < 64; ++i) {
+    if (i < b) {
+      T acc0 = T(0), acc1 = T(0);
 #pragma unroll
-      for (int i = j + 1; i < 64; ++i)
-        if (i < b) z[i] = fma(-Ls[i][j], zj, z[i]);
+      for (int j = 0; j + 1 < 64; j += 2) {
+        if (j < i) acc0 = fma(Ls[i][j], z[j], acc0);
+        if (j + 1 < i) acc1 = fma(Ls[i][j + 1], z[j + 1], acc1);
+      }
+      z[i] = sub_rn(z[i], acc0 + acc1);
     }
   }
 #pragma unroll

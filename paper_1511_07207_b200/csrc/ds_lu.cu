@@ -288,57 +288,72 @@ __global__ void __launch_bounds__(kPanelThreads) lu_panel_global_kernel(T* __res
 // moves every affected element of a column at once (all loads before all
 // stores, no dependent chains); rows kb..bf-1 of a column are contiguous.
 __global__ void laswp_plan_kernel(int64_t kb, int64_t bf, const int64_t* __restrict__ piv,
-                                  int64_t* pairs /* [2][2*cnt] */, int* npairs) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+                                  int64_t* pairs /* [8*cnt] */, int* npairs) {
+  // one warp; the working maps live in shared memory (cnt <= kLaswpSmem), else in `pairs`
+  extern __shared__ int64_t sm[];
   const int cnt = (int)(bf - kb);
-  // origin[] for rows kb..bf-1, plus a small list for outside rows
-  int64_t* orig_in = pairs;                 // reuse output space as scratch: [cnt]
-  int64_t* out_rows = pairs + 2 * cnt;      // [cnt] outside rows
-  int64_t* out_orig = pairs + 3 * cnt;      // [cnt]
-  int nout = 0;
-  for (int k = 0; k < cnt; ++k) orig_in[k] = kb + k;
+  const int lane = threadIdx.x;
+  const bool in_smem = cnt <= 1024;
+  int64_t* orig_in = in_smem ? sm : pairs;                 // [cnt]
+  int64_t* out_rows = in_smem ? sm + cnt : pairs + 2 * cnt;  // [cnt]
+  int64_t* out_orig = in_smem ? sm + 2 * cnt : pairs + 3 * cnt;
+  __shared__ int s_nout;
+  __shared__ int64_t s_piv[1024];
+  for (int k = lane; k < cnt && k < 1024; k += 32) s_piv[k] = piv[kb + k];
+  for (int k = lane; k < cnt; k += 32) orig_in[k] = kb + k;
+  if (lane == 0) s_nout = 0;
+  __syncwarp();
   for (int k = 0; k < cnt; ++k) {
-    const int64_t p = piv[kb + k];
-    const int64_t r = kb + k;
-    if (p == r) continue;
+    const int64_t p = k < 1024 ? s_piv[k] : piv[kb + k];
+    if (p == kb + k) continue;
     int64_t* op;
     if (p < bf) {
       op = &orig_in[p - kb];
     } else {
+      const int nout = s_nout;
       int f = -1;
-      for (int q = 0; q < nout; ++q)
-        if (out_rows[q] == p) {
-          f = q;
-          break;
-        }
+      for (int q0 = 0; q0 < nout && f < 0; q0 += 32) {
+        const int q = q0 + lane;
+        const unsigned m = __ballot_sync(0xffffffffu, q < nout && out_rows[q] == p);
+        if (m) f = q0 + __ffs(m) - 1;
+      }
       if (f < 0) {
-        f = nout++;
-        out_rows[f] = p;
-        out_orig[f] = p;
+        f = nout;
+        if (lane == 0) {
+          out_rows[f] = p;
+          out_orig[f] = p;
+          s_nout = nout + 1;
+        }
       }
       op = &out_orig[f];
     }
-    const int64_t t = orig_in[k];
-    orig_in[k] = *op;
-    *op = t;
+    __syncwarp();
+    if (lane == 0) {
+      const int64_t t = orig_in[k];
+      orig_in[k] = *op;
+      *op = t;
+    }
+    __syncwarp();
   }
-  // compact into (dst, src) pairs where dst != src; layout: dst[0..np), src[0..np) at pairs+4cnt..
-  int64_t* dst = pairs + 4 * cnt;
-  int64_t* src = pairs + 6 * cnt;
-  int np = 0;
-  for (int k = 0; k < cnt; ++k)
-    if (orig_in[k] != kb + k) {
-      dst[np] = kb + k;
-      src[np] = orig_in[k];
-      ++np;
-    }
-  for (int q = 0; q < nout; ++q)
-    if (out_orig[q] != out_rows[q]) {
-      dst[np] = out_rows[q];
-      src[np] = out_orig[q];
-      ++np;
-    }
-  *npairs = np;
+  // compact into (dst, src) pairs: dst at pairs+4cnt, src at pairs+6cnt
+  if (lane == 0) {
+    int64_t* dst = pairs + 4 * cnt;
+    int64_t* src = pairs + 6 * cnt;
+    int np = 0;
+    for (int k = 0; k < cnt; ++k)
+      if (orig_in[k] != kb + k) {
+        dst[np] = kb + k;
+        src[np] = orig_in[k];
+        ++np;
+      }
+    for (int q = 0; q < s_nout; ++q)
+      if (out_orig[q] != out_rows[q]) {
+        dst[np] = out_rows[q];
+        src[np] = out_orig[q];
+        ++np;
+      }
+    *npairs = np;
+  }
 }
 
 // One CTA per group of `cols` columns: every affected element of those columns
@@ -372,7 +387,8 @@ struct SwapPlan {
 
 int laswp_plan(ds_ctx* ctx, int64_t kb, int64_t bf, const int64_t* piv, SwapPlan& sp) {
   sp.cnt = bf - kb;
-  laswp_plan_kernel<<<1, 32, 0, ctx->stream>>>(kb, bf, piv, sp.pairs, sp.np);
+  const size_t smem = sp.cnt <= 1024 ? (size_t)3 * sp.cnt * sizeof(int64_t) : 0;
+  laswp_plan_kernel<<<1, 32, smem, ctx->stream>>>(kb, bf, piv, sp.pairs, sp.np);
   count_launch(ctx);
   DS_CHECK_LAUNCH();
   return DS_OK;

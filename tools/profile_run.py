@@ -35,6 +35,15 @@ elif what == "lu":
     dA = be.stage_in(A)
     lu_factor_blocked(dA, 64, be)
     ctx.synchronize()
+elif what == "gemm":
+    m, n, k = (int(v) for v in sys.argv[2:5])
+    A = np.asfortranarray(rng.uniform(-1, 1, (m, k)))
+    B = np.asfortranarray(rng.uniform(-1, 1, (k, n)))
+    C = np.asfortranarray(rng.uniform(-1, 1, (m, n)))
+    dA, dB, dC = be.stage_in(A, B, C)
+    for _ in range(3):
+        be.gemm(-1.0, dA, dB, 1.0, dC, out=dC)
+    ctx.synchronize()
 elif what == "gmres":
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
     A, b, _ = generate_problem(ProblemSpec("general_nonsymmetric", n, 0))
