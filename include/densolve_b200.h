@@ -188,6 +188,58 @@ int ds_relative_residual(ds_ctx* ctx, int dtype, int64_t n, const void* d_A, int
 int ds_symmetry_check(ds_ctx* ctx, int dtype, int64_t n, const void* d_A, int64_t lda,
                       double* h_maxdiff, double* h_amax);
 
+/* ---- multi-GPU building blocks ---------------------------
+ * One process per GPU; the host driver (paper_1511_07207_b200/distributed.py)
+ * issues the collectives (torch.distributed / NCCL) between these calls.
+ * Row-sharded Krylov: every rank owns rows [r0, r0 + n_loc) of A (an
+ * n_loc x n column-major block) and of every vector.  Per-rank reduction
+ * partials are 3-double records (sum x^2, scale, ssq); after an all-gather the
+ * nranks records are combined IN RANK ORDER on every rank, so all ranks hold
+ * bitwise-identical scalars.  d_state is a device double[8]:
+ *   [0] rho = r.r   [1] ||b||   [2] status (DS_*)   [3] stop index
+ *   [4] p'Ap on NotSpd / happy flag (GMRES)   [5] last residual / bad row. */
+#define DS_SHARD_STATE_LEN 8
+int ds_vec_parts(ds_ctx* ctx, int dtype, int64_t n, const void* d_x, double* d_out3);
+int ds_dot_dev(ds_ctx* ctx, int dtype, int64_t n, const void* d_x, const void* d_y, double* d_out);
+/* y += A x (krylov.py:167 form, x = axpy(1, gemv(V, y), x)) */
+int ds_gemv_acc(ds_ctx* ctx, int dtype, int64_t m, int64_t n, const void* d_A, int64_t lda,
+                const void* d_x, void* d_y);
+/* r = b - A x on a row shard (krylov.py:47,104) and the parts of r */
+int ds_resid_parts(ds_ctx* ctx, int dtype, int64_t m, int64_t n, const void* d_A, int64_t lda,
+                   const void* d_x, const void* d_b, void* d_r, double* d_out3);
+/* CG (krylov.py:45-67) on a row shard */
+int ds_cg_shard_init(ds_ctx* ctx, const double* d_bparts, const double* d_rparts, int nranks,
+                     double* d_state, double* d_hist, double tol, int64_t cap);
+int ds_cg_shard_update(ds_ctx* ctx, int dtype, int64_t n_loc, int nranks, const double* d_pap_parts,
+                       double* d_state, int64_t k, void* d_x, void* d_r, const void* d_p,
+                       const void* d_Ap, double* d_out3);
+int ds_cg_shard_finish(ds_ctx* ctx, int dtype, int64_t n_loc, int nranks, const double* d_parts3,
+                       double* d_state, int64_t k, const void* d_r, void* d_p, double* d_hist,
+                       double tol, int64_t cap);
+/* GMRES (krylov.py:116-163) on a row shard */
+int ds_multidot_dev(ds_ctx* ctx, int dtype, int64_t n_loc, const void* d_V, int64_t ldv, int kc,
+                    const void* d_w, double* d_out);
+int ds_cgs_update_shard(ds_ctx* ctx, int dtype, int64_t n_loc, const void* d_V, int64_t ldv, int kc,
+                        void* d_w, int nranks, const double* d_parts, void* d_Hcol, double* d_hsave,
+                        int pass, double* d_out3, const double* d_state, int64_t k);
+int ds_gmres_shard_start(ds_ctx* ctx, int dtype, int64_t n_loc, const void* d_r, void* d_v0,
+                         int nranks, const double* d_parts3, void* d_g, double* d_state);
+int ds_gmres_shard_step(ds_ctx* ctx, int dtype, int64_t n_loc, void* d_w, int nranks,
+                        const double* d_parts3, void* d_H, void* d_Hraw, int64_t ldh, void* d_g,
+                        void* d_cs, void* d_sn, int k, double* d_est, double* d_state, double tol,
+                        int64_t total_before, int64_t cap);
+int ds_gmres_lsq(ds_ctx* ctx, int dtype, const void* d_H, int64_t ldh, const void* d_g, int inner,
+                 void* d_y, double* d_state);
+/* symmetry gate on blocks: max|A[i,j] - B[j,i]| and max|A| (krylov.py:41-44) */
+int ds_absdiff_transposed(ds_ctx* ctx, int dtype, int64_t m, int64_t n, const void* d_A,
+                          int64_t lda, const void* d_B, int64_t ldb, double* h_out2);
+/* 1-D block-cyclic LU: tall-panel factorization (m >= w; pivots relative to the
+ * panel's first row) and a pivot range applied to ncols columns */
+int ds_lu_panel(ds_ctx* ctx, int dtype, int64_t m, int64_t w, void* d_P, int64_t ldp, int64_t b,
+                int64_t* d_piv, int8_t* d_zero);
+int ds_laswp(ds_ctx* ctx, int dtype, int64_t ncols, void* d_A, int64_t lda, int64_t k0, int64_t k1,
+             const int64_t* d_piv);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -103,6 +103,30 @@ _SIGNATURES = {
                                      c_void_p, POINTER(c_double)]),
     "ds_symmetry_check": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, POINTER(c_double),
                                   POINTER(c_double)]),
+    # multi-GPU building blocks
+    "ds_vec_parts": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p]),
+    "ds_dot_dev": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p, c_void_p]),
+    "ds_gemv_acc": (c_int, [c_void_p, c_int, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p]),
+    "ds_resid_parts": (c_int, [c_void_p, c_int, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
+                               c_void_p, c_void_p]),
+    "ds_cg_shard_init": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_double, c_int64]),
+    "ds_cg_shard_update": (c_int, [c_void_p, c_int, c_int64, c_int, c_void_p, c_void_p, c_int64, c_void_p,
+                                   c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ds_cg_shard_finish": (c_int, [c_void_p, c_int, c_int64, c_int, c_void_p, c_void_p, c_int64, c_void_p,
+                                   c_void_p, c_void_p, c_double, c_int64]),
+    "ds_multidot_dev": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_int, c_void_p, c_void_p]),
+    "ds_cgs_update_shard": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_int, c_void_p, c_int,
+                                    c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_int64]),
+    "ds_gmres_shard_start": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
+                                     c_void_p]),
+    "ds_gmres_shard_step": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int, c_void_p, c_void_p, c_void_p,
+                                    c_int64, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_double,
+                                    c_int64, c_int64]),
+    "ds_gmres_lsq": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_void_p, c_int, c_void_p, c_void_p]),
+    "ds_absdiff_transposed": (c_int, [c_void_p, c_int, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_int64,
+                                      c_void_p]),
+    "ds_lu_panel": (c_int, [c_void_p, c_int, c_int64, c_int64, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
+    "ds_laswp": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)

@@ -490,14 +490,16 @@ static int64_t outer_block(int64_t b, int64_t n) {
   return std::min<int64_t>(n, b * std::max<int64_t>(1, 256 / b));
 }
 
+// Factor the m x w (m >= w) column-major panel W in place: rows [0, m), columns
+// [0, w).  m == w is the square factorization of ds_lu_factor.
 template <typename T>
-int lu_factor_impl(ds_ctx* ctx, int64_t n, T* W, int64_t ld, int64_t b, int64_t* d_piv,
+int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t b, int64_t* d_piv,
                    int8_t* d_zero) {
   void* ws = nullptr;
+  const int64_t NB = outer_block(b, w);
   const size_t scratch_bytes = 256 + 2 * 1024 * 16 + sizeof(T) * (2 * 1024 * kPanelMaxW + 2 * kPanelMaxW) +
                                2 * sizeof(T) * (size_t)std::max<int64_t>(b, 1) + 16 * 256;
-  DS_TRY(ctx_workspace(ctx, scratch_bytes + 2 * sizeof(int64_t) * 8 * (size_t)outer_block(b, n) + 4096, &ws));
-  const int64_t NB = outer_block(b, n);
+  DS_TRY(ctx_workspace(ctx, scratch_bytes + 2 * sizeof(int64_t) * 8 * (size_t)NB + 4096, &ws));
   Carver cvs{(char*)ws};
   char* scratch = cvs.take<char>(scratch_bytes);
   SwapPlan sp_in, sp_out;
@@ -505,43 +507,60 @@ int lu_factor_impl(ds_ctx* ctx, int64_t n, T* W, int64_t ld, int64_t b, int64_t*
   sp_in.np = cvs.take<int>(64);
   sp_out.pairs = cvs.take<int64_t>(sizeof(int64_t) * 8 * (size_t)NB);
   sp_out.np = cvs.take<int>(64);
-  for (int64_t kb = 0; kb < n; kb += NB) {
-    const int64_t bf = std::min<int64_t>(kb + NB, n);
+  for (int64_t kb = 0; kb < w; kb += NB) {
+    const int64_t bf = std::min<int64_t>(kb + NB, w);
     // ---- factor the outer panel [kb, bf) with the reference's b-wide blocking
     for (int64_t ib = kb; ib < bf; ib += b) {
       const int64_t ibf = std::min<int64_t>(ib + b, bf);
-      DS_TRY(panel_launch<T>(ctx, W, n, ld, ib, ibf, d_piv, d_zero, scratch));
+      DS_TRY(panel_launch<T>(ctx, W, m, ld, ib, ibf, d_piv, d_zero, scratch));
       DS_TRY(laswp_plan(ctx, ib, ibf, d_piv, sp_in));
       DS_TRY(laswp_apply<T>(ctx, W, ld, kb, ib, sp_in));
       DS_TRY(laswp_apply<T>(ctx, W, ld, ibf, bf, sp_in));
       if (ibf < bf) {
         T* U = W + ib + ibf * ld;
         DS_TRY(trsm_lower_unit_launch<T>(ctx, ibf - ib, bf - ibf, W + ib + ib * ld, ld, U, ld, U, ld));
-        DS_TRY(gemm_launch<T>(ctx, n - ibf, bf - ibf, ibf - ib, -1.0, W + ibf + ib * ld, ld, U, ld, 1.0,
+        DS_TRY(gemm_launch<T>(ctx, m - ibf, bf - ibf, ibf - ib, -1.0, W + ibf + ib * ld, ld, U, ld, 1.0,
                               W + ibf + ibf * ld, ld, W + ibf + ibf * ld, ld));
       }
     }
     // ---- swaps of the whole outer panel on the columns outside it
     DS_TRY(laswp_plan(ctx, kb, bf, d_piv, sp_out));
     DS_TRY(laswp_apply<T>(ctx, W, ld, 0, kb, sp_out));
-    DS_TRY(laswp_apply<T>(ctx, W, ld, bf, n, sp_out));
-    if (bf < n) {
+    DS_TRY(laswp_apply<T>(ctx, W, ld, bf, w, sp_out));
+    if (bf < w) {
       // U01 = L00^-1 A01, L00 the NB x NB unit-lower block (blocked by b)
       for (int64_t ib = kb; ib < bf; ib += b) {
         const int64_t ibf = std::min<int64_t>(ib + b, bf);
         T* Ur = W + ib + bf * ld;
-        DS_TRY(trsm_lower_unit_launch<T>(ctx, ibf - ib, n - bf, W + ib + ib * ld, ld, Ur, ld, Ur, ld));
+        DS_TRY(trsm_lower_unit_launch<T>(ctx, ibf - ib, w - bf, W + ib + ib * ld, ld, Ur, ld, Ur, ld));
         if (ibf < bf)
-          DS_TRY(gemm_launch<T>(ctx, bf - ibf, n - bf, ibf - ib, -1.0, W + ibf + ib * ld, ld, Ur, ld, 1.0,
+          DS_TRY(gemm_launch<T>(ctx, bf - ibf, w - bf, ibf - ib, -1.0, W + ibf + ib * ld, ld, Ur, ld, 1.0,
                                 W + ibf + bf * ld, ld, W + ibf + bf * ld, ld));
       }
       // trailing update A11 -= L10 U01 with K = NB (DMMA GEMM)
-      DS_TRY(gemm_launch<T>(ctx, n - bf, n - bf, bf - kb, -1.0, W + bf + kb * ld, ld, W + kb + bf * ld, ld,
+      DS_TRY(gemm_launch<T>(ctx, m - bf, w - bf, bf - kb, -1.0, W + bf + kb * ld, ld, W + kb + bf * ld, ld,
                             1.0, W + bf + bf * ld, ld, W + bf + bf * ld, ld));
     }
   }
   return DS_OK;
 }
+template int lu_factor_impl<double>(ds_ctx*, int64_t, int64_t, double*, int64_t, int64_t, int64_t*, int8_t*);
+template int lu_factor_impl<float>(ds_ctx*, int64_t, int64_t, float*, int64_t, int64_t, int64_t*, int8_t*);
+
+// apply swaps piv[k0..k1) (absolute rows) to ncols columns of W
+template <typename T>
+int laswp_range(ds_ctx* ctx, T* W, int64_t ld, int64_t ncols, int64_t k0, int64_t k1, const int64_t* d_piv) {
+  void* ws = nullptr;
+  DS_TRY(ctx_workspace(ctx, sizeof(int64_t) * 8 * (size_t)(k1 - k0) + 1024, &ws));
+  Carver cv{(char*)ws};
+  SwapPlan sp;
+  sp.pairs = cv.take<int64_t>(sizeof(int64_t) * 8 * (size_t)(k1 - k0));
+  sp.np = cv.take<int>(64);
+  DS_TRY(laswp_plan(ctx, k0, k1, d_piv, sp));
+  return laswp_apply<T>(ctx, W, ld, 0, ncols, sp);
+}
+template int laswp_range<double>(ds_ctx*, double*, int64_t, int64_t, int64_t, int64_t, const int64_t*);
+template int laswp_range<float>(ds_ctx*, float*, int64_t, int64_t, int64_t, int64_t, const int64_t*);
 
 // ----------------------------------------------------------------------------
 // pivots -> gather permutation: idx = apply_pivots(piv, arange(n))  (core.py:94-100)
@@ -767,7 +786,7 @@ int ds_lu_factor_dev(ds_ctx* ctx, int dtype, int64_t n, void* A, int64_t lda, in
   DS_CUDA(cudaMallocAsync((void**)&d_zero, (size_t)n, ctx->stream));
   DS_CUDA(cudaMemsetAsync(d_zero, 0, (size_t)n, ctx->stream));
   int rc = DS_OK;
-  DS_DISPATCH(dtype, T, rc = lu_factor_impl<T>(ctx, n, (T*)A, lda, nb, d_piv, d_zero));
+  DS_DISPATCH(dtype, T, rc = lu_factor_impl<T>(ctx, n, n, (T*)A, lda, nb, d_piv, d_zero));
   if (rc != DS_OK) return rc;
   std::vector<int8_t> hz((size_t)n);
   DS_CUDA(cudaMemcpyAsync(hz.data(), d_zero, (size_t)n, cudaMemcpyDeviceToHost, ctx->stream));
@@ -803,7 +822,7 @@ int ds_lu_factor(ds_ctx* ctx, int dtype, int64_t n, void* A, int64_t lda, int64_
   DS_CUDA(cudaMallocAsync((void**)&d_zero, (size_t)n, ctx->stream));
   DS_CUDA(cudaMemsetAsync(d_zero, 0, (size_t)n, ctx->stream));
   int rc = DS_OK;
-  DS_DISPATCH(dtype, T, rc = lu_factor_impl<T>(ctx, n, (T*)A, lda, nb, d_piv, d_zero));
+  DS_DISPATCH(dtype, T, rc = lu_factor_impl<T>(ctx, n, n, (T*)A, lda, nb, d_piv, d_zero));
   if (rc != DS_OK) return rc;
   std::vector<int8_t> hz((size_t)n);
   DS_CUDA(cudaMemcpyAsync(h_piv, d_piv, (size_t)n * sizeof(int64_t), cudaMemcpyDeviceToHost,
