@@ -283,6 +283,10 @@ struct ds_ctx {
   void* hbuf = nullptr;
   size_t hbuf_bytes = 0;
   int64_t launches = 0;
+  // LU look-ahead: a high-priority side stream for the next panel's factorization
+  cudaStream_t side = nullptr;
+  cudaStream_t aux = nullptr;  // low-priority stream for the swaps of already-factored L columns
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
 };
 
 namespace ds {

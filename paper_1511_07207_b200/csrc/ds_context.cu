@@ -139,6 +139,11 @@ int ds_ctx_destroy(ds_ctx* ctx) {
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->hbuf) cudaFreeHost(ctx->hbuf);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->ev_c) cudaEventDestroy(ctx->ev_c);
+  if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
+  if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
   delete ctx;
   return DS_OK;
 }

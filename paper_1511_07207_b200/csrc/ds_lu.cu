@@ -492,6 +492,18 @@ static int64_t outer_block(int64_t b, int64_t n) {
 
 // Factor the m x w (m >= w) column-major panel W in place: rows [0, m), columns
 // [0, w).  m == w is the square factorization of ds_lu_factor.
+//
+// Look-ahead: after panel k's swaps and U01 are formed, the next outer panel's
+// NB columns get their trailing update first; the factorization of panel k+1
+// (cooperative panel kernels, inner TRSM/GEMM) is then enqueued on a
+// high-priority side stream while the bulk trailing GEMM of panel k runs on the
+// main stream (disjoint columns), and the main stream waits for it before
+// applying panel k+1's swaps.
+static bool lu_lookahead_enabled() {
+  const char* e = getenv("DENSOLVE_LU_LOOKAHEAD");
+  return !(e && e[0] == '0');
+}
+
 template <typename T>
 int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t b, int64_t* d_piv,
                    int8_t* d_zero) {
@@ -507,9 +519,29 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
   sp_in.np = cvs.take<int>(64);
   sp_out.pairs = cvs.take<int64_t>(sizeof(int64_t) * 8 * (size_t)NB);
   sp_out.np = cvs.take<int>(64);
-  for (int64_t kb = 0; kb < w; kb += NB) {
-    const int64_t bf = std::min<int64_t>(kb + NB, w);
-    // ---- factor the outer panel [kb, bf) with the reference's b-wide blocking
+
+  const bool lookahead = lu_lookahead_enabled() && w > NB && m >= 2048;
+  if (lookahead && !ctx->side) {
+    int lo = 0, hi = 0;
+    DS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    DS_CUDA(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, hi));
+    DS_CUDA(cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, lo));
+    DS_CUDA(cudaEventCreateWithFlags(&ctx->ev_a, cudaEventDisableTiming));
+    DS_CUDA(cudaEventCreateWithFlags(&ctx->ev_b, cudaEventDisableTiming));
+    DS_CUDA(cudaEventCreateWithFlags(&ctx->ev_c, cudaEventDisableTiming));
+  }
+  // swap plans of the L-column swaps (aux stream): one per outer panel, kept
+  // alive until the aux stream drains
+  const int64_t nouter = ceil_div(w, NB);
+  int64_t* left_pairs = nullptr;
+  int* left_np = nullptr;
+  if (lookahead) {
+    DS_CUDA(cudaMallocAsync((void**)&left_pairs, sizeof(int64_t) * 8 * (size_t)NB * nouter, ctx->stream));
+    DS_CUDA(cudaMallocAsync((void**)&left_np, sizeof(int) * 64 * nouter, ctx->stream));
+  }
+
+  // factor the outer panel [kb, bf) with the reference's b-wide blocking
+  auto factor_outer = [&](int64_t kb, int64_t bf) -> int {
     for (int64_t ib = kb; ib < bf; ib += b) {
       const int64_t ibf = std::min<int64_t>(ib + b, bf);
       DS_TRY(panel_launch<T>(ctx, W, m, ld, ib, ibf, d_piv, d_zero, scratch));
@@ -523,24 +555,72 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
                               W + ibf + ibf * ld, ld, W + ibf + ibf * ld, ld));
       }
     }
-    // ---- swaps of the whole outer panel on the columns outside it
-    DS_TRY(laswp_plan(ctx, kb, bf, d_piv, sp_out));
-    DS_TRY(laswp_apply<T>(ctx, W, ld, 0, kb, sp_out));
-    DS_TRY(laswp_apply<T>(ctx, W, ld, bf, w, sp_out));
-    if (bf < w) {
-      // U01 = L00^-1 A01, L00 the NB x NB unit-lower block (blocked by b)
-      for (int64_t ib = kb; ib < bf; ib += b) {
-        const int64_t ibf = std::min<int64_t>(ib + b, bf);
-        T* Ur = W + ib + bf * ld;
-        DS_TRY(trsm_lower_unit_launch<T>(ctx, ibf - ib, w - bf, W + ib + ib * ld, ld, Ur, ld, Ur, ld));
-        if (ibf < bf)
-          DS_TRY(gemm_launch<T>(ctx, bf - ibf, w - bf, ibf - ib, -1.0, W + ibf + ib * ld, ld, Ur, ld, 1.0,
-                                W + ibf + bf * ld, ld, W + ibf + bf * ld, ld));
-      }
-      // trailing update A11 -= L10 U01 with K = NB (DMMA GEMM)
-      DS_TRY(gemm_launch<T>(ctx, m - bf, w - bf, bf - kb, -1.0, W + bf + kb * ld, ld, W + kb + bf * ld, ld,
-                            1.0, W + bf + bf * ld, ld, W + bf + bf * ld, ld));
+    return DS_OK;
+  };
+  // U01 = L00^-1 A01 and A11 -= L10 U01 for trailing columns [c0, c1)
+  auto outer_update = [&](int64_t kb, int64_t bf, int64_t c0, int64_t c1) -> int {
+    if (c1 <= c0) return DS_OK;
+    for (int64_t ib = kb; ib < bf; ib += b) {
+      const int64_t ibf = std::min<int64_t>(ib + b, bf);
+      T* Ur = W + ib + c0 * ld;
+      DS_TRY(trsm_lower_unit_launch<T>(ctx, ibf - ib, c1 - c0, W + ib + ib * ld, ld, Ur, ld, Ur, ld));
+      if (ibf < bf)
+        DS_TRY(gemm_launch<T>(ctx, bf - ibf, c1 - c0, ibf - ib, -1.0, W + ibf + ib * ld, ld, Ur, ld, 1.0,
+                              W + ibf + c0 * ld, ld, W + ibf + c0 * ld, ld));
     }
+    return gemm_launch<T>(ctx, m - bf, c1 - c0, bf - kb, -1.0, W + bf + kb * ld, ld, W + kb + c0 * ld, ld, 1.0,
+                          W + bf + c0 * ld, ld, W + bf + c0 * ld, ld);
+  };
+
+  DS_TRY(factor_outer(0, std::min<int64_t>(NB, w)));
+  for (int64_t kb = 0; kb < w; kb += NB) {
+    const int64_t bf = std::min<int64_t>(kb + NB, w);
+    // swaps of the whole outer panel on the columns outside it.  The L columns
+    // [0, kb) are never read again by the factorization, so with look-ahead
+    // their swaps run on the low-priority aux stream, overlapped with the GEMMs.
+    DS_TRY(laswp_plan(ctx, kb, bf, d_piv, sp_out));
+    if (lookahead && kb > 0) {
+      SwapPlan lp;
+      const int64_t kq = kb / NB;
+      lp.pairs = left_pairs + (size_t)kq * 8 * NB;
+      lp.np = left_np + kq * 64;
+      lp.cnt = bf - kb;
+      DS_TRY(laswp_plan(ctx, kb, bf, d_piv, lp));
+      DS_CUDA(cudaEventRecord(ctx->ev_c, ctx->stream));
+      DS_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_c, 0));
+      cudaStream_t main = ctx->stream;
+      ctx->stream = ctx->aux;
+      const int rc = laswp_apply<T>(ctx, W, ld, 0, kb, lp);
+      ctx->stream = main;
+      DS_TRY(rc);
+    } else {
+      DS_TRY(laswp_apply<T>(ctx, W, ld, 0, kb, sp_out));
+    }
+    DS_TRY(laswp_apply<T>(ctx, W, ld, bf, w, sp_out));
+    if (bf >= w) break;
+    const int64_t bf2 = std::min<int64_t>(bf + NB, w);
+    DS_TRY(outer_update(kb, bf, bf, bf2));  // look-ahead columns first
+    if (lookahead) {
+      DS_CUDA(cudaEventRecord(ctx->ev_a, ctx->stream));
+      DS_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_a, 0));
+      cudaStream_t main = ctx->stream;
+      ctx->stream = ctx->side;
+      const int rc = factor_outer(bf, bf2);
+      ctx->stream = main;
+      DS_TRY(rc);
+      DS_CUDA(cudaEventRecord(ctx->ev_b, ctx->side));
+      DS_TRY(outer_update(kb, bf, bf2, w));
+      DS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_b, 0));
+    } else {
+      DS_TRY(outer_update(kb, bf, bf2, w));
+      DS_TRY(factor_outer(bf, bf2));
+    }
+  }
+  if (lookahead) {
+    DS_CUDA(cudaEventRecord(ctx->ev_c, ctx->aux));
+    DS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_c, 0));
+    DS_CUDA(cudaFreeAsync(left_pairs, ctx->stream));
+    DS_CUDA(cudaFreeAsync(left_np, ctx->stream));
   }
   return DS_OK;
 }
