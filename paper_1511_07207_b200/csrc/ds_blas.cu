@@ -864,45 +864,43 @@ int gemm_launch<float>(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, double alph
 }
 
 // ============================================================================
-// TRSM (backends.py:176-200): one thread per right-hand-side column.
+// TRSM (backends.py:176-200).
 //   lower-unit: z_i = b_i - (L[i,:i] . z[:i])           (stored diagonal ignored)
 //   upper:      z_i = (b_i - U[i,i+1:] . z[i+1:]) / U_ii
-// b <= 64: L staged in shared memory, z in registers (fully unrolled);
-// b > 64: generic path working in place on Z.
+// b <= 64: shared-memory tile kernel; b > 64: generic path, one thread per column.
 // ============================================================================
+// Tile form for b <= 64 (the LU U-block-row solve): one CTA per 64 x 32 tile of
+// the right-hand side, L and the tile staged in shared memory, right-looking
+// column sweep (z_i -= L_ij z_j for all i > j and all 32 columns per step, one
+// fused multiply-add each), so the dependent chain is spread over 256 threads.
 template <typename T>
-__global__ void __launch_bounds__(128)
-    trsm_lower_unit_small(int b, int64_t m, const T* __restrict__ L, int64_t ldl,
-                          const T* __restrict__ B, int64_t ldb, T* Z, int64_t ldz) {
-  __shared__ T Ls[64][65];
-  for (int idx = threadIdx.x; idx < b * b; idx += blockDim.x) {
+__global__ void __launch_bounds__(256)
+    trsm_lower_unit_tile(int b, int64_t m, const T* __restrict__ L, int64_t ldl,
+                         const T* __restrict__ B, int64_t ldb, T* Z, int64_t ldz) {
+  __shared__ T Ls[63][64];  // Ls[j][i] = L[i, j] (column j contiguous; column b-1 unused)
+  __shared__ T Zs[32][65];  // Zs[c][i]
+  const int tid = threadIdx.x;
+  const int64_t c0 = (int64_t)blockIdx.x * 32;
+  const int nc = (int)min((int64_t)32, m - c0);
+  for (int idx = tid; idx < b * (b - 1); idx += blockDim.x) {
     const int i = idx % b, j = idx / b;
-    Ls[i][j] = L[i + (int64_t)j * ldl];
+    Ls[j][i] = L[i + (int64_t)j * ldl];
+  }
+  for (int idx = tid; idx < b * nc; idx += blockDim.x) {
+    const int i = idx % b, c = idx / b;
+    Zs[c][i] = B[i + (c0 + c) * ldb];
   }
   __syncthreads();
-  const int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= m) return;
-  T z[64];
-#pragma unroll
-  for (int i = 0; i < 64; ++i)
-    if (i < b) z[i] = B[i + col * ldb];
-  // z_i = b_i - (L[i,:i] . z[:i])  (dot form of backends.py:184-185); two partial
-  // accumulators halve the dependent FMA chain
-#pragma unroll
-  for (int i = 1; i < 64; ++i) {
-    if (i < b) {
-      T acc0 = T(0), acc1 = T(0);
-#pragma unroll
-      for (int j = 0; j + 1 < 64; j += 2) {
-        if (j < i) acc0 = fma(Ls[i][j], z[j], acc0);
-        if (j + 1 < i) acc1 = fma(Ls[i][j + 1], z[j + 1], acc1);
-      }
-      z[i] = sub_rn(z[i], acc0 + acc1);
-    }
+  const int c = tid & 31, rg = tid >> 5;
+  for (int j = 0; j + 1 < b; ++j) {
+    const T zj = Zs[c][j];
+    for (int i = j + 1 + rg; i < b; i += 8) Zs[c][i] = fma(-Ls[j][i], zj, Zs[c][i]);
+    __syncthreads();
   }
-#pragma unroll
-  for (int i = 0; i < 64; ++i)
-    if (i < b) Z[i + col * ldz] = z[i];
+  for (int idx = tid; idx < b * nc; idx += blockDim.x) {
+    const int i = idx % b, cc = idx / b;
+    Z[i + (c0 + cc) * ldz] = Zs[cc][i];
+  }
 }
 
 template <typename T>
@@ -943,7 +941,7 @@ int trsm_lower_unit_launch(ds_ctx* ctx, int64_t b, int64_t m, const T* L, int64_
                            int64_t ldb, T* Z, int64_t ldz) {
   if (b == 0 || m == 0) return DS_OK;
   if (b <= 64) {
-    trsm_lower_unit_small<T><<<(unsigned)ceil_div(m, 128), 128, 0, ctx->stream>>>(
+    trsm_lower_unit_tile<T><<<(unsigned)ceil_div(m, 32), 256, 0, ctx->stream>>>(
         (int)b, m, L, ldl, B, ldb, Z, ldz);
   } else {
     trsm_lower_unit_big<T><<<(unsigned)ceil_div(m, 128), 128, 0, ctx->stream>>>(b, m, L, ldl, B,

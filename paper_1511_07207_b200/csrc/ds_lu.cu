@@ -287,7 +287,108 @@ __global__ void __launch_bounds__(kPanelThreads) lu_panel_global_kernel(T* __res
 // meaning "row dst receives the original row src".  The gather kernel then
 // moves every affected element of a column at once (all loads before all
 // stores, no dependent chains); rows kb..bf-1 of a column are contiguous.
-__global__ void laswp_plan_kernel(int64_t kb, int64_t bf, const int64_t* __restrict__ piv,
+// Parallel plan for cnt <= kPlanMax (256 threads).  Swap k exchanges positions
+// k and s_k >= k, so position k is final after step k: the slots s_k are
+// resolved in parallel (rows outside the panel are deduplicated into compact
+// slots cnt + r, first occurrence first), only the swap replay itself is a
+// serial loop over shared memory, and the (dst, src) compaction is a warp
+// ballot scan.  Same output layout as the serial kernel.
+constexpr int kPlanMax = 512;
+__global__ void __launch_bounds__(256)
+    laswp_plan_kernel(int64_t kb, int64_t bf, const int64_t* __restrict__ piv, int64_t* pairs,
+                      int* npairs) {
+  __shared__ int64_t P[kPlanMax];         // pivot rows
+  __shared__ int64_t home[2 * kPlanMax];  // row label of each slot
+  __shared__ int64_t orig[2 * kPlanMax];  // content (original row) of each slot after the swaps
+  __shared__ int S[kPlanMax];             // slot swapped with position k
+  __shared__ int rank[kPlanMax];          // compact index of an outside row (first occurrence)
+  __shared__ int s_nout;
+  const int cnt = (int)(bf - kb);
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int k = tid; k < cnt; k += blockDim.x) P[k] = piv[kb + k];
+  __syncthreads();
+  // first occurrence of each outside row
+  for (int k = tid; k < cnt; k += blockDim.x) {
+    int f = 0;
+    if (P[k] >= bf) {
+      f = 1;
+      for (int j = 0; j < k; ++j)
+        if (P[j] == P[k]) {
+          f = 0;
+          break;
+        }
+    }
+    rank[k] = f;
+  }
+  __syncthreads();
+  if (tid < 32) {  // exclusive scan of the first-occurrence flags
+    int base = 0;
+    for (int k0 = 0; k0 < cnt; k0 += 32) {
+      const int k = k0 + lane;
+      const int f = k < cnt ? rank[k] : 0;
+      const unsigned m = __ballot_sync(0xffffffffu, f);
+      if (k < cnt) rank[k] = f ? base + __popc(m & ((1u << lane) - 1)) : -1;
+      base += __popc(m);
+    }
+    if (lane == 0) s_nout = base;
+  }
+  __syncthreads();
+  for (int k = tid; k < cnt; k += blockDim.x) {
+    const int64_t p = P[k];
+    int slot;
+    if (p < bf) {
+      slot = (int)(p - kb);
+    } else {
+      int r = rank[k];
+      if (r < 0) {
+        for (int j = 0; j < k; ++j)
+          if (P[j] == p) {
+            r = rank[j];
+            break;
+          }
+      } else {
+        home[cnt + r] = p;
+        orig[cnt + r] = p;
+      }
+      slot = cnt + r;
+    }
+    S[k] = slot;
+    home[k] = kb + k;
+    orig[k] = kb + k;
+  }
+  __syncthreads();
+  if (tid == 0) {  // replay the swaps (direct.py:68-70 applied to row labels)
+    for (int k = 0; k < cnt; ++k) {
+      const int sk = S[k];
+      if (sk != k) {
+        const int64_t t = orig[k];
+        orig[k] = orig[sk];
+        orig[sk] = t;
+      }
+    }
+  }
+  __syncthreads();
+  if (tid < 32) {  // compact the moved slots into (dst, src) pairs
+    const int tot = cnt + s_nout;
+    int64_t* dst = pairs + 4 * cnt;
+    int64_t* src = pairs + 6 * cnt;
+    int base = 0;
+    for (int q0 = 0; q0 < tot; q0 += 32) {
+      const int q = q0 + lane;
+      const bool mv = q < tot && orig[q] != home[q];
+      const unsigned m = __ballot_sync(0xffffffffu, mv);
+      if (mv) {
+        const int o = base + __popc(m & ((1u << lane) - 1));
+        dst[o] = home[q];
+        src[o] = orig[q];
+      }
+      base += __popc(m);
+    }
+    if (lane == 0) *npairs = base;
+  }
+}
+
+__global__ void laswp_plan_serial_kernel(int64_t kb, int64_t bf, const int64_t* __restrict__ piv,
                                   int64_t* pairs /* [8*cnt] */, int* npairs) {
   // one warp; the working maps live in shared memory (cnt <= kLaswpSmem), else in `pairs`
   extern __shared__ int64_t sm[];
@@ -387,8 +488,12 @@ struct SwapPlan {
 
 int laswp_plan(ds_ctx* ctx, int64_t kb, int64_t bf, const int64_t* piv, SwapPlan& sp) {
   sp.cnt = bf - kb;
-  const size_t smem = sp.cnt <= 1024 ? (size_t)3 * sp.cnt * sizeof(int64_t) : 0;
-  laswp_plan_kernel<<<1, 32, smem, ctx->stream>>>(kb, bf, piv, sp.pairs, sp.np);
+  if (sp.cnt <= kPlanMax) {
+    laswp_plan_kernel<<<1, 256, 0, ctx->stream>>>(kb, bf, piv, sp.pairs, sp.np);
+  } else {
+    const size_t smem = sp.cnt <= 1024 ? (size_t)3 * sp.cnt * sizeof(int64_t) : 0;
+    laswp_plan_serial_kernel<<<1, 32, smem, ctx->stream>>>(kb, bf, piv, sp.pairs, sp.np);
+  }
   count_launch(ctx);
   DS_CHECK_LAUNCH();
   return DS_OK;
@@ -545,6 +650,7 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
     for (int64_t ib = kb; ib < bf; ib += b) {
       const int64_t ibf = std::min<int64_t>(ib + b, bf);
       DS_TRY(panel_launch<T>(ctx, W, m, ld, ib, ibf, d_piv, d_zero, scratch));
+      if (ib == kb && ibf == bf) continue;  // no columns of the outer panel outside this b-panel
       DS_TRY(laswp_plan(ctx, ib, ibf, d_piv, sp_in));
       DS_TRY(laswp_apply<T>(ctx, W, ld, kb, ib, sp_in));
       DS_TRY(laswp_apply<T>(ctx, W, ld, ibf, bf, sp_in));
@@ -578,25 +684,25 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
     // swaps of the whole outer panel on the columns outside it.  The L columns
     // [0, kb) are never read again by the factorization, so with look-ahead
     // their swaps run on the low-priority aux stream, overlapped with the GEMMs.
-    DS_TRY(laswp_plan(ctx, kb, bf, d_piv, sp_out));
-    if (lookahead && kb > 0) {
-      SwapPlan lp;
+    SwapPlan op = sp_out;
+    if (lookahead && kb > 0) {  // per-panel plan buffer: the aux stream reads it later
       const int64_t kq = kb / NB;
-      lp.pairs = left_pairs + (size_t)kq * 8 * NB;
-      lp.np = left_np + kq * 64;
-      lp.cnt = bf - kb;
-      DS_TRY(laswp_plan(ctx, kb, bf, d_piv, lp));
+      op.pairs = left_pairs + (size_t)kq * 8 * NB;
+      op.np = left_np + kq * 64;
+    }
+    if (kb > 0 || bf < w) DS_TRY(laswp_plan(ctx, kb, bf, d_piv, op));
+    if (lookahead && kb > 0) {
       DS_CUDA(cudaEventRecord(ctx->ev_c, ctx->stream));
       DS_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->ev_c, 0));
       cudaStream_t main = ctx->stream;
       ctx->stream = ctx->aux;
-      const int rc = laswp_apply<T>(ctx, W, ld, 0, kb, lp);
+      const int rc = laswp_apply<T>(ctx, W, ld, 0, kb, op);
       ctx->stream = main;
       DS_TRY(rc);
     } else {
-      DS_TRY(laswp_apply<T>(ctx, W, ld, 0, kb, sp_out));
+      DS_TRY(laswp_apply<T>(ctx, W, ld, 0, kb, op));
     }
-    DS_TRY(laswp_apply<T>(ctx, W, ld, bf, w, sp_out));
+    DS_TRY(laswp_apply<T>(ctx, W, ld, bf, w, op));
     if (bf >= w) break;
     const int64_t bf2 = std::min<int64_t>(bf + NB, w);
     DS_TRY(outer_update(kb, bf, bf, bf2));  // look-ahead columns first

@@ -29,21 +29,24 @@ from .device import DeviceArray, is_device, to_device
 
 
 def _tally_lu(be, n: int, b: int, zero_cols: np.ndarray, blocked: bool):
+    """The reference's per-column / per-panel counter tallies (direct.py:66-83), in closed
+    form: scal and ger per non-zero pivot column, trsm and gemm per panel."""
     c = be.counters
-    for kb in range(0, n, b):
-        bf = min(kb + b, n)
-        c.iamax_calls += bf - kb
-        for i in range(kb, bf):
-            if zero_cols[i]:
-                continue
-            if i + 1 < n:
-                be.tally("scal", n - i - 1)
-                if i + 1 < bf:
-                    be.tally("ger", 2 * (n - i - 1) * (bf - i - 1))
-        if blocked and bf < n:
-            w = bf - kb
-            be.tally("trsm", w * (w - 1) * (n - bf))
-            be.tally("gemm", 2 * (n - bf) * (n - bf) * w)
+    c.iamax_calls += n
+    i = np.arange(n, dtype=np.int64)
+    bf = np.minimum((i // b + 1) * b, n)
+    live = (zero_cols[:n] == 0) & (i + 1 < n)
+    tail = n - i - 1
+    be.tally("scal", int(tail[live].sum()), calls=int(live.sum()))
+    g = live & (i + 1 < bf)
+    be.tally("ger", int((2 * tail[g] * (bf[g] - i[g] - 1)).sum()), calls=int(g.sum()))
+    if blocked:
+        for kb in range(0, n, b):
+            bf_ = min(kb + b, n)
+            if bf_ < n:
+                w = bf_ - kb
+                be.tally("trsm", w * (w - 1) * (n - bf_))
+                be.tally("gemm", 2 * (n - bf_) * (n - bf_) * w)
 
 
 def _factor(A, b: int, backend, blocked: bool) -> LuFactors:
