@@ -58,6 +58,9 @@ extern "C" {
 /* ---- GMRES breakdown tags (krylov.py:175) ------------------------------ */
 #define DS_BREAKDOWN_NONE 0
 #define DS_BREAKDOWN_HAPPY 1 /* "happy-breakdown" */
+/* ---- BiCGSTAB breakdown tags (krylov.py:213-238) ------------------------ */
+#define DS_BREAKDOWN_RHO 2   /* "rho-breakdown"   */
+#define DS_BREAKDOWN_OMEGA 3 /* "omega-breakdown" */
 
 typedef struct ds_ctx ds_ctx;
 
@@ -153,6 +156,15 @@ int ds_gmres(ds_ctx* ctx, int dtype, int64_t n, const void* d_A, int64_t lda, co
              const void* d_x0, void* d_x, double tol, int64_t max_it, int64_t restart_m,
              int orth, double* h_hist, int64_t hist_cap, int64_t* h_cycles, int64_t cycles_cap,
              ds_sink_fn sink, void* sink_user, ds_solve_info* info);
+
+/* BiCGSTAB: replaces krylov.bicgstab_solve (krylov.py:185-253).  Two streamed
+ * GEMVs per iteration with fused dots; breakdown tags DS_BREAKDOWN_RHO/OMEGA.
+ * info->error_index returns the loop-exit stage (1 rho test, 2 r0hat'v == 0,
+ * 3 omega test, 4 early exit on ||s||, 5 normal) so the host can tally the
+ * reference's logical op counters for the last iteration. */
+int ds_bicgstab(ds_ctx* ctx, int dtype, int64_t n, const void* d_A, int64_t lda,
+                const void* d_b, const void* d_x0, void* d_x, double tol, int64_t max_it,
+                double* h_hist, int64_t hist_cap, ds_solve_info* info);
 
 /* Blocked right-looking LU with partial pivoting, in place on d_A: replaces
  * direct.lu_factor_blocked (direct.py:50-84); nb == n gives

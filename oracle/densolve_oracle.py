@@ -413,3 +413,106 @@ def lu_backward_error(A, packed, pivots):
     np.fill_diagonal(L, 1.0)
     U = np.triu(packed).astype(np.float64)
     return float(np.linalg.norm(P @ A.astype(np.float64) - L @ U))
+
+
+# ---------------------------------------------------------------------------
+# BiCGSTAB (krylov.py:185-253)
+# ---------------------------------------------------------------------------
+def bicgstab(A, b, x0, tol: float, max_it: int | None = None, ops: Ops | None = None):
+    ops = ops or Ops()
+    n = A.shape[0]
+    cap = max_it if max_it is not None else 10 * n
+    u = unit_roundoff(A.dtype)
+    bnorm = ops.nrm2(b)  # _rhs_norm (krylov.py:29-33)
+    if bnorm == 0.0:
+        raise Degenerate("||b|| = 0")
+    x = x0.copy()
+    r = ops.axpy(-1.0, ops.gemv(A, x), b)
+    r0hat = r.copy()
+    r0hat_norm = float(np.linalg.norm(r0hat))
+    rho_prev, alpha, omega = 1.0, 1.0, 1.0
+    rho = ops.dot(r0hat, r)
+    p = np.zeros_like(b)
+    v = np.zeros_like(b)
+    res = ops.nrm2(r) / bnorm
+    hist = [res]
+    rnorm = res * bnorm
+    it = 0
+    breakdown = None
+    while res > tol and it < cap:  # krylov.py:212-245
+        if abs(rho) < u * r0hat_norm * rnorm:
+            breakdown = "rho-breakdown"
+            break
+        beta = (rho / rho_prev) * (alpha / omega)
+        p = ops.axpy(beta, ops.axpy(-omega, v, p), r)
+        v = ops.gemv(A, p)
+        rv = ops.dot(r0hat, v)
+        if rv == 0.0:
+            breakdown = "rho-breakdown"
+            break
+        alpha = rho / rv
+        s = ops.axpy(-alpha, v, r)
+        snorm = ops.nrm2(s)
+        if snorm / bnorm <= tol:
+            x = ops.axpy(alpha, p, x)
+            r = s
+            res = snorm / bnorm
+            hist.append(res)
+            it += 1
+            break
+        t = ops.gemv(A, s)
+        ts = ops.dot(t, s)
+        tt = ops.dot(t, t)
+        if tt == 0.0:
+            breakdown = "omega-breakdown"
+            break
+        omega = ts / tt
+        if abs(omega) < u:
+            breakdown = "omega-breakdown"
+            break
+        x = ops.axpy(omega, s, ops.axpy(alpha, p, x))
+        r = ops.axpy(-omega, t, s)
+        rho_prev, rho = rho, ops.dot(r0hat, r)
+        rnorm = ops.nrm2(r)
+        res = rnorm / bnorm
+        hist.append(res)
+        it += 1
+    return x, {"converged": res <= tol and breakdown is None, "iterations": it, "final": float(res),
+               "history": hist, "breakdown": breakdown}
+
+
+# ---------------------------------------------------------------------------
+# Cholesky (direct.py:87-120, 166-171)
+# ---------------------------------------------------------------------------
+def cholesky_factor(A, b: int, ops: Ops | None = None):
+    """Returns tril(W) (CholeskyFactor.l); raises NotSpd with .index on a bad pivot."""
+    ops = ops or Ops()
+    n = A.shape[0]
+    b = min(b, n)
+    u = unit_roundoff(A.dtype)
+    amax = float(np.max(np.abs(A))) if n else 0.0
+    if float(np.max(np.abs(A - A.T))) > 10.0 * u * amax:
+        raise NotSpd("matrix is not symmetric")
+    W = np.array(A, order="F", copy=True)
+    for kb in range(0, n, b):
+        bf = min(kb + b, n)
+        for i in range(kb, bf):
+            aii = W[i, i]
+            if not (aii > 0.0) or not np.isfinite(aii):
+                e = NotSpd(f"nonpositive pivot {aii} at index {i}")
+                e.index = i
+                raise e
+            W[i, i] = np.sqrt(aii)
+            if i + 1 < n:
+                W[i + 1:, i] = ops.scal(1.0 / W[i, i], W[i + 1:, i])
+                if i + 1 < bf:
+                    ops.ger_inplace(W[i + 1:, i + 1:bf], -1.0, W[i + 1:, i], W[i + 1:bf, i])
+        if bf < n:
+            L10 = W[bf:, kb:bf]
+            ops.gemm_inplace(-1.0, L10, np.asfortranarray(L10.T), 1.0, W[bf:, bf:])
+    return np.asfortranarray(np.tril(W))
+
+
+def cholesky_solve(L, b):  # direct.py:166-171
+    y = forward_substitution(L, b, unit_diagonal=False)
+    return backward_substitution(np.asfortranarray(L.T), y)

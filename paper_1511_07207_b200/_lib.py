@@ -26,7 +26,7 @@ LIB_PATH = os.path.join(_HERE, "libdensolve_b200.so")
 DS_OK, DS_EDIM, DS_EPREC, DS_EDEGRHS, DS_ESINGULAR, DS_ENOTSPD, DS_EINVAL, DS_ECUDA, DS_ENOMEM = range(9)
 DS_F32, DS_F64 = 0, 1
 DS_ORTH_MODIFIED, DS_ORTH_CLASSICAL = 0, 1
-DS_BREAKDOWN_NONE, DS_BREAKDOWN_HAPPY = 0, 1
+DS_BREAKDOWN_NONE, DS_BREAKDOWN_HAPPY, DS_BREAKDOWN_RHO, DS_BREAKDOWN_OMEGA = 0, 1, 2, 3
 
 
 class SolveInfo(ctypes.Structure):
@@ -89,6 +89,8 @@ _SIGNATURES = {
     "ds_gmres": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
                          c_void_p, c_double, c_int64, c_int64, c_int, c_void_p, c_int64,
                          c_void_p, c_int64, SINK_FN, c_void_p, POINTER(SolveInfo)]),
+    "ds_bicgstab": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
+                            c_double, c_int64, c_void_p, c_int64, POINTER(SolveInfo)]),
     "ds_lu_factor": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_int64, c_void_p,
                              c_void_p, POINTER(c_int32)]),
     "ds_lu_factor_dev": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_int64,

@@ -170,6 +170,19 @@ __global__ void __launch_bounds__(kRedThreads)
     }
     d = block_sum(d, sm);
     if (threadIdx.x == 0) red[blockIdx.x] = d;
+  } else if (EPI == EPI_DOT2) {
+    double d = 0.0, e = 0.0;
+    if (i < m) {
+      y[i] = yi;
+      d = (double)v[i] * (double)yi;
+      e = (double)yi * (double)yi;
+    }
+    d = block_sum(d, sm);
+    e = block_sum(e, sm);
+    if (threadIdx.x == 0) {
+      red[blockIdx.x] = d;
+      red[gridDim.x + blockIdx.x] = e;
+    }
   } else if (EPI == EPI_RESID) {
     // r = axpy(-1, A x, b) = b - A x  (krylov.py:47,104: one rounding, the -1 is exact)
     Ssq q{0.0, 0.0};
@@ -236,6 +249,10 @@ int gemv_launch(ds_ctx* ctx, const GemvPlan& p, const T* A, int64_t lda, const T
       break;
     case EPI_AXPY_INTO:
       gemv_reduce_kernel<T, EPI_AXPY_INTO>
+          <<<rblocks, kRedThreads, 0, ctx->stream>>>(part, m, nch, y, v, red, stop);
+      break;
+    case EPI_DOT2:
+      gemv_reduce_kernel<T, EPI_DOT2>
           <<<rblocks, kRedThreads, 0, ctx->stream>>>(part, m, nch, y, v, red, stop);
       break;
   }

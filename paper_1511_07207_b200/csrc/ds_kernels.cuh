@@ -16,6 +16,8 @@ enum GemvEpi : int {
   EPI_DOT = 1,        // y = A x ; block partial of dot(v, y) -> part (CG p'Ap)
   EPI_RESID = 2,      // y = b - A x (axpy(-1, Ax, b)); block partial (ssq of y, plain sum y^2)
   EPI_AXPY_INTO = 3,  // y = y + (A x)   (GMRES x += V y, krylov.py:167)
+  EPI_DOT2 = 4,       // y = A x ; block partials of dot(v, y) -> red[blk], dot(y, y) -> red[nblk + blk]
+                      //   (BiCGSTAB t's and t't, krylov.py:230-231)
 };
 
 // Device-side loop gate: solver kernels of iteration k return immediately once

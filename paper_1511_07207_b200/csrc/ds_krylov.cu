@@ -665,6 +665,324 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
   return DS_OK;
 }
 
+
+// ============================================================================
+// BiCGSTAB  (krylov.bicgstab_solve, krylov.py:185-253)
+//
+// One iteration = two half-iterations, each with its own gate index:
+//   half 2k   : p = r + beta (p - omega v) ; v = A p (+ r0hat'v) ; s = r - alpha v
+//               (+ ssq s) ; early exit x += alpha p, r = s when ||s||/||b|| <= tol
+//   half 2k+1 : t = A s (+ t's, t't) ; x = (x + alpha p) + omega s ;
+//               r = s - omega t (+ r0hat'r, ssq r) ; rho, history, stop
+// The device stop word counts completed half-iterations: breakdown at the top
+// of iteration k or inside it -> 2k, early exit -> 2k+1, normal end -> 2k+2;
+// iterations = ceil(stop / 2), exactly the reference's `it`.
+// ============================================================================
+struct BiDev {
+  int64_t stop_h;     // half-iteration index at which the loop stops
+  int32_t breakdown;  // DS_BREAKDOWN_NONE / DS_BREAKDOWN_RHO / DS_BREAKDOWN_OMEGA
+  int32_t stage;      // where the loop stopped (for the logical counter tally)
+  double bnorm, r0n, rnorm;
+  double rho, rho_prev, alpha, omega;
+};
+enum BiStage : int32_t {
+  BI_RUN = 0, BI_RHO_TOP = 1, BI_RV_ZERO = 2, BI_OMEGA = 3, BI_EARLY = 4, BI_DONE = 5
+};
+
+// setup (krylov.py:196-208): red = EPI_RESID partials of r0 = b - A x0
+__global__ void bi_init_kernel(const double* red, int nblk, BiDev* st, double* hist, double tol,
+                               int64_t cap) {
+  __shared__ double sm[64];
+  Ssq q{0.0, 0.0};
+  double s2 = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    q = ssq_merge(q, Ssq{red[2 * i], red[2 * i + 1]});
+    s2 += red[2 * nblk + i];
+  }
+  q = block_ssq(q, sm);
+  s2 = block_sum(s2, sm);
+  if (threadIdx.x == 0) {
+    const double res = ssq_norm(q.scale, q.ssq) / st->bnorm;  // nrm2(r)/bnorm (:206)
+    hist[0] = res;
+    st->r0n = sqrt(s2);           // np.linalg.norm(r0hat) (:199)
+    st->rho = s2;                 // dot(r0hat, r) with r0hat = r (:201)
+    st->rho_prev = 1.0;
+    st->alpha = 1.0;
+    st->omega = 1.0;
+    st->rnorm = res * st->bnorm;  // (:209)
+    st->breakdown = DS_BREAKDOWN_NONE;
+    st->stage = BI_RUN;
+    st->stop_h = (res > tol && 0 < cap) ? 2 * cap : 0;
+  }
+}
+
+// top of iteration k: rho-breakdown test, beta, p = axpy(beta, axpy(-omega, v, p), r)
+template <typename T>
+__global__ void __launch_bounds__(kT)
+    bi_p_kernel(int64_t n, T* __restrict__ p, const T* __restrict__ v, const T* __restrict__ r,
+                BiDev* st, double u, Gate gate) {
+  if (gated(gate)) return;
+  const double rho = st->rho;
+  if (fabs(rho) < u * st->r0n * st->rnorm) {  // krylov.py:213-215
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->breakdown = DS_BREAKDOWN_RHO;
+      st->stage = BI_RHO_TOP;
+      st->stop_h = gate.k;
+    }
+    return;
+  }
+  const double beta = (rho / st->rho_prev) * (st->alpha / st->omega);  // :216
+  const T bt = (T)beta, no = (T)(-st->omega);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T q = add_rn(p[i], mul_rn(no, v[i]));
+    p[i] = add_rn(r[i], mul_rn(bt, q));
+  }
+}
+
+// rv = r0hat'v ; alpha = rho/rv ; s = r - alpha v ; ssq(s) partials  (krylov.py:218-225)
+template <typename T>
+__global__ void __launch_bounds__(kT)
+    bi_s_kernel(int64_t n, T* __restrict__ s, const T* __restrict__ r, const T* __restrict__ v,
+                const double* __restrict__ red_rv, int nblk_rv, BiDev* st,
+                double* __restrict__ red_out, Gate gate) {
+  if (gated(gate)) return;
+  __shared__ double sm[64];
+  const double rv = reduce_sum_partials(red_rv, nblk_rv, sm);
+  if (rv == 0.0) {  // :220-222
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->breakdown = DS_BREAKDOWN_RHO;
+      st->stage = BI_RV_ZERO;
+      st->stop_h = gate.k;
+    }
+    return;
+  }
+  const double alpha = st->rho / rv;
+  const T na = (T)(-alpha);
+  Ssq q{0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T si = add_rn(r[i], mul_rn(na, v[i]));
+    s[i] = si;
+    q = ssq_add(q, (double)si);
+  }
+  q = block_ssq(q, sm);
+  if (threadIdx.x == 0) {
+    red_out[2 * blockIdx.x] = q.scale;
+    red_out[2 * blockIdx.x + 1] = q.ssq;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->alpha = alpha;
+}
+
+// ||s||/||b|| <= tol: x = axpy(alpha, p, x), r = s, history, stop (krylov.py:224-230)
+template <typename T>
+__global__ void __launch_bounds__(kT)
+    bi_early_kernel(int64_t n, T* __restrict__ x, T* __restrict__ r, const T* __restrict__ p,
+                    const T* __restrict__ s, const double* __restrict__ red_s, int nblk,
+                    BiDev* st, double* hist, double tol, Gate gate) {
+  if (gated(gate)) return;
+  __shared__ double sm[64];
+  Ssq q{0.0, 0.0};
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x)
+    q = ssq_merge(q, Ssq{red_s[2 * i], red_s[2 * i + 1]});
+  q = block_ssq(q, sm);
+  const double snorm = ssq_norm(q.scale, q.ssq);
+  if (!(snorm / st->bnorm <= tol)) return;
+  const T a = (T)st->alpha;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = add_rn(x[i], mul_rn(a, p[i]));
+    r[i] = s[i];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t k = gate.k / 2;
+    hist[k + 1] = snorm / st->bnorm;
+    st->stage = BI_EARLY;
+    st->stop_h = gate.k + 1;
+  }
+}
+
+// omega = t's / t't ; x = axpy(omega, s, axpy(alpha, p, x)) ; r = axpy(-omega, t, s);
+// partials of r0hat'r and ssq(r)   (krylov.py:230-245)
+template <typename T>
+__global__ void __launch_bounds__(kT)
+    bi_xr_kernel(int64_t n, T* __restrict__ x, T* __restrict__ r, const T* __restrict__ p,
+                 const T* __restrict__ s, const T* __restrict__ t, const T* __restrict__ r0hat,
+                 const double* __restrict__ red_t, int nblk_t, BiDev* st, double u,
+                 double* __restrict__ red_out, Gate gate) {
+  if (gated(gate)) return;
+  __shared__ double sm[64];
+  double ts = 0.0, tt = 0.0;
+  for (int i = threadIdx.x; i < nblk_t; i += blockDim.x) {
+    ts += red_t[i];
+    tt += red_t[nblk_t + i];
+  }
+  ts = block_sum(ts, sm);
+  tt = block_sum(tt, sm);
+  const double omega = tt == 0.0 ? 0.0 : ts / tt;
+  if (tt == 0.0 || fabs(omega) < u) {  // :232-238
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->breakdown = DS_BREAKDOWN_OMEGA;
+      st->stage = BI_OMEGA;
+      st->stop_h = gate.k - 1;  // = 2k: the iteration does not count
+    }
+    return;
+  }
+  const T a = (T)st->alpha, om = (T)omega, nom = (T)(-omega);
+  Ssq q{0.0, 0.0};
+  double d = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T x1 = add_rn(x[i], mul_rn(a, p[i]));
+    const T si = s[i];
+    x[i] = add_rn(x1, mul_rn(om, si));
+    const T ri = add_rn(si, mul_rn(nom, t[i]));
+    r[i] = ri;
+    d = fma((double)r0hat[i], (double)ri, d);
+    q = ssq_add(q, (double)ri);
+  }
+  q = block_ssq(q, sm);
+  d = block_sum(d, sm);
+  if (threadIdx.x == 0) {
+    red_out[blockIdx.x] = d;
+    red_out[gridDim.x + 2 * blockIdx.x] = q.scale;
+    red_out[gridDim.x + 2 * blockIdx.x + 1] = q.ssq;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->omega = omega;
+}
+
+// rho_prev, rho = rho, r0hat'r ; rnorm = nrm2(r) ; res ; history ; stop  (:240-245, loop test :212)
+__global__ void bi_finish_kernel(const double* red, int nblk, BiDev* st, double* hist, double tol,
+                                 int64_t cap, Gate gate) {
+  if (gated(gate)) return;
+  __shared__ double sm[64];
+  double d = 0.0;
+  Ssq q{0.0, 0.0};
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    d += red[i];
+    q = ssq_merge(q, Ssq{red[nblk + 2 * i], red[nblk + 2 * i + 1]});
+  }
+  d = block_sum(d, sm);
+  q = block_ssq(q, sm);
+  if (threadIdx.x == 0) {
+    const int64_t k = gate.k / 2;
+    st->rho_prev = st->rho;
+    st->rho = d;
+    const double rnorm = ssq_norm(q.scale, q.ssq);
+    st->rnorm = rnorm;
+    const double res = rnorm / st->bnorm;
+    hist[k + 1] = res;
+    if (!(res > tol) || k + 1 >= cap) {
+      st->stage = BI_DONE;
+      st->stop_h = gate.k + 1;
+    }
+  }
+}
+
+template <typename T>
+int bicgstab_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, const T* x0, T* x,
+                  double tol, int64_t cap, double* h_hist, int64_t hist_cap, ds_solve_info* info) {
+  const int64_t launches0 = ctx->launches;
+  const double u = (sizeof(T) == 8 ? 1.1102230246251565e-16 : 5.960464477539063e-08);
+  const GemvPlan gp = gemv_plan(ctx, n, n, sizeof(T));
+  const int rblocks = (int)ceil_div(std::max<int64_t>(n, 1), 256);
+  const int vg = vec_grid(ctx, n);
+  size_t need = gp.part_bytes + 256 + ((size_t)n * sizeof(T) + 256) * 6 +
+                ((size_t)rblocks * 3 + 64) * sizeof(double) * 2 +
+                ((size_t)vg * 3 + 64) * sizeof(double) * 2 + (size_t)(cap + 2) * sizeof(double) +
+                sizeof(BiDev) + 8 * 256;
+  void* ws = nullptr;
+  DS_TRY(ctx_workspace(ctx, need, &ws));
+  Carver cv{(char*)ws};
+  double* part = cv.take<double>(gp.part_bytes);
+  T* r = cv.take<T>((size_t)n * sizeof(T));
+  T* r0hat = cv.take<T>((size_t)n * sizeof(T));
+  T* p = cv.take<T>((size_t)n * sizeof(T));
+  T* v = cv.take<T>((size_t)n * sizeof(T));
+  T* s = cv.take<T>((size_t)n * sizeof(T));
+  T* t = cv.take<T>((size_t)n * sizeof(T));
+  double* red_a = cv.take<double>(((size_t)rblocks * 3 + 64) * sizeof(double));
+  double* red_b = cv.take<double>(((size_t)vg * 3 + 64) * sizeof(double));
+  double* red_c = cv.take<double>(((size_t)vg * 3 + 64) * sizeof(double));
+  double* hist = cv.take<double>((size_t)(cap + 2) * sizeof(double));
+  BiDev* st = cv.take<BiDev>(sizeof(BiDev));
+  double* scal = cv.take<double>(64);
+
+  // ||b|| (krylov.py:195 -> _rhs_norm :29-33)
+  int nb = 0;
+  DS_TRY(ssq_launch<T>(ctx, n, b, red_b, &nb));
+  DS_TRY(finish_ssq(ctx, red_b, nb, scal));
+  double bnorm = 0;
+  DS_CUDA(cudaMemcpyAsync(&bnorm, scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (bnorm == 0.0) {
+    set_error("||b|| = 0");
+    return DS_EDEGRHS;
+  }
+  BiDev init{};
+  init.bnorm = bnorm;
+  DS_CUDA(cudaMemcpyAsync(st, &init, sizeof(BiDev), cudaMemcpyHostToDevice, ctx->stream));
+  // x = x0.copy(); r = axpy(-1, A x, b); r0hat = r; p = v = 0  (krylov.py:196-203)
+  if (x != x0) DS_CUDA(cudaMemcpyAsync(x, x0, n * sizeof(T), cudaMemcpyDeviceToDevice, ctx->stream));
+  int rb = 0;
+  DS_TRY(gemv_launch<T>(ctx, gp, A, lda, x, r, part, EPI_RESID, b, red_a, &rb));
+  bi_init_kernel<<<1, 256, 0, ctx->stream>>>(red_a, rb, st, hist, tol, cap);
+  count_launch(ctx);
+  DS_CUDA(cudaMemcpyAsync(r0hat, r, n * sizeof(T), cudaMemcpyDeviceToDevice, ctx->stream));
+  DS_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), ctx->stream));
+  DS_CUDA(cudaMemsetAsync(v, 0, n * sizeof(T), ctx->stream));
+  DS_CHECK_LAUNCH();
+
+  int64_t* h_stop = nullptr;
+  DS_TRY(ctx_hostbuf(ctx, 64, (void**)&h_stop));
+  int64_t k = 0, chunk = 2;
+  while (true) {
+    DS_CUDA(cudaMemcpyAsync(h_stop, &st->stop_h, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    DS_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int64_t stop_h = *h_stop;
+    if (stop_h <= 2 * k || k >= cap) break;
+    const int64_t kend = std::min<int64_t>(cap, k + chunk);
+    for (; k < kend; ++k) {
+      const Gate g0{&st->stop_h, 2 * k}, g1{&st->stop_h, 2 * k + 1};
+      bi_p_kernel<T><<<vg, kT, 0, ctx->stream>>>(n, p, v, r, st, u, g0);
+      count_launch(ctx);
+      int rb1 = 0, rb2 = 0;
+      DS_TRY(gemv_launch<T>(ctx, gp, A, lda, p, v, part, EPI_DOT, r0hat, red_a, &rb1, g0));
+      bi_s_kernel<T><<<vg, kT, 0, ctx->stream>>>(n, s, r, v, red_a, rb1, st, red_b, g0);
+      bi_early_kernel<T><<<vg, kT, 0, ctx->stream>>>(n, x, r, p, s, red_b, vg, st, hist, tol, g0);
+      count_launch(ctx, 2);
+      DS_TRY(gemv_launch<T>(ctx, gp, A, lda, s, t, part, EPI_DOT2, s, red_a, &rb2, g1));
+      bi_xr_kernel<T><<<vg, kT, 0, ctx->stream>>>(n, x, r, p, s, t, r0hat, red_a, rb2, st, u,
+                                                  red_c, g1);
+      bi_finish_kernel<<<1, 256, 0, ctx->stream>>>(red_c, vg, st, hist, tol, cap, g1);
+      count_launch(ctx, 2);
+    }
+    DS_CHECK_LAUNCH();
+    chunk = std::min<int64_t>(chunk * 2, 64);
+  }
+  BiDev hst;
+  DS_CUDA(cudaMemcpyAsync(&hst, st, sizeof(BiDev), cudaMemcpyDeviceToHost, ctx->stream));
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  const int64_t iters = std::min<int64_t>((hst.stop_h + 1) / 2, cap);
+  const int64_t hl = std::min<int64_t>(iters + 1, hist_cap);
+  std::vector<double> hh((size_t)iters + 1);
+  DS_CUDA(cudaMemcpyAsync(hh.data(), hist, (iters + 1) * sizeof(double), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (h_hist)
+    for (int64_t i = 0; i < hl; ++i) h_hist[i] = hh[i];
+  const double res = hh[iters];
+  info->iterations = iters;
+  info->history_len = hl;
+  info->final_relative_residual = res;
+  info->breakdown = hst.breakdown;
+  info->converged = res <= tol && hst.breakdown == DS_BREAKDOWN_NONE;  // krylov.py:246
+  info->error_index = hst.stage;  // loop exit stage (BiStage), for the logical counter tally
+  info->kernel_launches = ctx->launches - launches0;
+  return DS_OK;
+}
+
 }  // namespace ds
 
 using namespace ds;
@@ -714,6 +1032,25 @@ int ds_gmres(ds_ctx* ctx, int dtype, int64_t n, const void* A, int64_t lda, cons
               return gmres_impl<T>(ctx, n, (const T*)A, lda, (const T*)b, (const T*)x0, (T*)x, tol,
                                    max_it, restart_m, orth, h_hist, hist_cap, h_cycles, cycles_cap,
                                    sink, sink_user, info));
+}
+
+int ds_bicgstab(ds_ctx* ctx, int dtype, int64_t n, const void* A, int64_t lda, const void* b,
+                const void* x0, void* x, double tol, int64_t max_it, double* h_hist,
+                int64_t hist_cap, ds_solve_info* info) {
+  DS_TRY(ctx_begin(ctx));
+  *info = ds_solve_info{};
+  info->error_index = -1;
+  if (n <= 0) {
+    set_error("matrix must be square and non-empty, got n=%lld", (long long)n);
+    return DS_EDIM;
+  }
+  if (!(tol > 0) || max_it < 1) {
+    set_error("invalid BiCGSTAB configuration");
+    return DS_EINVAL;
+  }
+  DS_DISPATCH(dtype, T,
+              return bicgstab_impl<T>(ctx, n, (const T*)A, lda, (const T*)b, (const T*)x0, (T*)x,
+                                      tol, max_it, h_hist, hist_cap, info));
 }
 
 }  // extern "C"

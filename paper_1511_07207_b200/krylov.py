@@ -138,3 +138,63 @@ def gmres_solve(A, b, x0, cfg: SolverConfig, backend=None, workspace_sink: list 
     report.wall_time = time.perf_counter() - t0
     report.kernel_launches = int(info.kernel_launches)
     return x, report
+
+
+# loop-exit stages reported by ds_bicgstab in SolveInfo.error_index
+_BI_RHO_TOP, _BI_RV_ZERO, _BI_OMEGA, _BI_EARLY, _BI_DONE = 1, 2, 3, 4, 5
+
+
+def _tally_bicgstab(be, n: int, iterations: int, stage: int):
+    """Logical op tallies of krylov.py:185-253 (setup :195-206, full iteration :216-245)."""
+    be.tally("nrm2", 2 * n)  # _rhs_norm
+    be.tally("gemv", 2 * n * n)
+    be.tally("axpy", 2 * n)
+    be.tally("dot", 2 * n)
+    be.tally("nrm2", 2 * n)
+    full = iterations - (1 if stage == _BI_EARLY else 0)
+    if full:
+        be.tally("gemv", 2 * n * n * 2 * full, 2 * full)
+        be.tally("dot", 2 * n * 4 * full, 4 * full)
+        be.tally("axpy", 2 * n * 6 * full, 6 * full)
+        be.tally("nrm2", 2 * n * 2 * full, 2 * full)
+    if stage in (_BI_RV_ZERO, _BI_OMEGA, _BI_EARLY):
+        # partial last pass: p update (2 axpy), v = A p, r0hat'v
+        be.tally("axpy", 2 * n * 2, 2)
+        be.tally("gemv", 2 * n * n)
+        be.tally("dot", 2 * n)
+    if stage in (_BI_OMEGA, _BI_EARLY):
+        be.tally("axpy", 2 * n)  # s
+        be.tally("nrm2", 2 * n)
+    if stage == _BI_OMEGA:
+        be.tally("gemv", 2 * n * n)
+        be.tally("dot", 2 * n * 2, 2)
+    if stage == _BI_EARLY:
+        be.tally("axpy", 2 * n)  # x += alpha p
+
+
+def bicgstab_solve(A, b, x0, cfg: SolverConfig, backend=None):
+    """BiCGSTAB with the shadow residual fixed at r0 (krylov.py:185-253): two streamed
+    matvecs per iteration with fused dot/norm epilogues, device-side breakdown tests."""
+    t0 = time.perf_counter()
+    be = as_b200(backend)
+    n = check_system(A, b, x0)
+    ctx = be.ctx
+    dA, db, dx0 = to_device(A, ctx), to_device(b, ctx), to_device(x0, ctx)
+    dx = DeviceArray(ctx, (n,), dA.dtype)
+    cap = int(cfg.iteration_cap(n))
+    hist = np.empty(cap + 1, dtype=np.float64)
+    info = _lib.SolveInfo()
+    st = ctx.lib.ds_bicgstab(ctx.handle, dA.dcode, n, c_void_p(dA.ptr), dA.ld, c_void_p(db.ptr),
+                             c_void_p(dx0.ptr), c_void_p(dx.ptr), float(cfg.tolerance), cap,
+                             hist.ctypes.data_as(c_void_p), cap + 1, ctypes.byref(info))
+    _lib.check(st)
+    _tally_bicgstab(be, n, int(info.iterations), int(info.error_index))
+    bd = {_lib.DS_BREAKDOWN_RHO: "rho-breakdown", _lib.DS_BREAKDOWN_OMEGA: "omega-breakdown"}
+    report = SolveReport(converged=bool(info.converged), iterations=int(info.iterations),
+                         final_relative_residual=float(info.final_relative_residual),
+                         residual_history=hist[: info.history_len].tolist(),
+                         breakdown=bd.get(int(info.breakdown)))
+    x = dx if is_device(x0) else dx.to_host()
+    report.wall_time = time.perf_counter() - t0
+    report.kernel_launches = int(info.kernel_launches)
+    return x, report

@@ -9,6 +9,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 GOLDEN = os.path.join(ROOT, "tests", "golden", "golden.npz")
+GOLDEN_NEXT = os.path.join(ROOT, "tests", "golden", "golden_next.npz")
 
 
 def pytest_configure(config):
@@ -19,6 +20,12 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def golden():
     return np.load(GOLDEN, allow_pickle=False)
+
+
+@pytest.fixture(scope="session")
+def golden_next():
+    """BiCGSTAB / Cholesky vectors from the reference (tests/golden/make_golden_next.py)."""
+    return np.load(GOLDEN_NEXT, allow_pickle=False)
 
 
 @pytest.fixture
