@@ -179,6 +179,19 @@ int ds_lu_factor(ds_ctx* ctx, int dtype, int64_t n, void* d_A, int64_t lda, int6
 int ds_lu_factor_dev(ds_ctx* ctx, int dtype, int64_t n, void* d_A, int64_t lda, int64_t nb,
                      int64_t* d_piv, int32_t* h_singular);
 
+/* Blocked Cholesky in place on d_A: replaces direct.cholesky_factor
+ * (direct.py:87-120).  On return the lower triangle holds L and the strict
+ * upper triangle is zero (CholeskyFactor.l, core.py:154-162).  DS_ENOTSPD on
+ * an asymmetric matrix (*h_bad_index = -1) or a non-positive / non-finite
+ * pivot (*h_bad_index = its index, NotSpdError.index). */
+int ds_cholesky_factor(ds_ctx* ctx, int dtype, int64_t n, void* d_A, int64_t lda, int64_t nb,
+                       int64_t* h_bad_index);
+
+/* cholesky_solve (direct.py:166-171): L y = b, then L^T x = y reading L in
+ * place.  DS_ESINGULAR (+ *h_bad_row) on a zero diagonal entry. */
+int ds_cholesky_solve(ds_ctx* ctx, int dtype, int64_t n, const void* d_L, int64_t ldl,
+                      const void* d_b, void* d_x, int64_t* h_bad_row);
+
 /* lu_solve: x = U^-1 L^-1 P b from packed factors (direct.py:155-163 with
  * core.apply_pivots core.py:94-100).  h_piv is the host pivot array. */
 int ds_lu_solve(ds_ctx* ctx, int dtype, int64_t n, const void* d_LU, int64_t lda,

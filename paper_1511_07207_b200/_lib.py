@@ -95,6 +95,9 @@ _SIGNATURES = {
                              c_void_p, POINTER(c_int32)]),
     "ds_lu_factor_dev": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_int64,
                                  c_void_p, POINTER(c_int32)]),
+    "ds_cholesky_factor": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_int64, POINTER(c_int64)]),
+    "ds_cholesky_solve": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
+                                  POINTER(c_int64)]),
     "ds_lu_solve": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
                             c_void_p]),
     "ds_forward_substitution": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_void_p,

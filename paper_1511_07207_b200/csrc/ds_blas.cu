@@ -656,8 +656,11 @@ template <bool VEC16, int MODE /*0: general, 1: out = C - AB*/>
 __global__ void __launch_bounds__(gemm64::THREADS, 2)
     gemm64_kernel(int64_t m, int64_t n, int64_t k, double alpha, const double* __restrict__ A,
                   int64_t lda, const double* __restrict__ B, int64_t ldb, double beta,
-                  const double* C, int64_t ldc, double* out, int64_t ldo) {
+                  const double* C, int64_t ldc, double* out, int64_t ldo, int tri) {
   using namespace gemm64;
+  // tri: only tiles holding some row >= column (the lower-triangle SYRK update of
+  // the Cholesky trailing matrix, direct.py:117-119); tiles strictly above exit
+  if (tri && (int64_t)(blockIdx.x + 1) * BM <= (int64_t)blockIdx.y * BN) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* As = reinterpret_cast<double*>(smem_raw);
   double* Bs = As + STAGES * A_STAGE;
@@ -765,7 +768,8 @@ template <int MODE>
 __global__ void __launch_bounds__(256)
     gemm32_kernel(int64_t m, int64_t n, int64_t k, float alpha, const float* __restrict__ A,
                   int64_t lda, const float* __restrict__ B, int64_t ldb, float beta, const float* C,
-                  int64_t ldc, float* out, int64_t ldo) {
+                  int64_t ldc, float* out, int64_t ldo, int tri) {
+  if (tri && (int64_t)(blockIdx.x + 1) * 64 <= (int64_t)blockIdx.y * 64) return;
   __shared__ float As[16][64 + 4];
   __shared__ float Bs[16][64 + 4];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -813,10 +817,9 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-template <>
-int gemm_launch<double>(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha,
-                        const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
-                        const double* C, int64_t ldc, double* out, int64_t ldo) {
+static int gemm_impl(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha,
+                     const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                     const double* C, int64_t ldc, double* out, int64_t ldo, int tri) {
   using namespace gemm64;
   if (m == 0 || n == 0) return DS_OK;
   static bool attr_done = false;
@@ -839,46 +842,67 @@ int gemm_launch<double>(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, double alp
     // out = beta*C (alpha*0 added)
     if (vec && sub)
       gemm64_kernel<true, 1><<<grid, THREADS, SMEM, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb,
-                                                                    beta, C, ldc, out, ldo);
+                                                                    beta, C, ldc, out, ldo, tri);
     else
       gemm64_kernel<false, 0><<<grid, THREADS, SMEM, ctx->stream>>>(m, n, k, alpha, A, lda, B,
-                                                                     ldb, beta, C, ldc, out, ldo);
+                                                                     ldb, beta, C, ldc, out, ldo, tri);
   } else if (vec) {
     if (sub)
       gemm64_kernel<true, 1><<<grid, THREADS, SMEM, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb,
-                                                                    beta, C, ldc, out, ldo);
+                                                                    beta, C, ldc, out, ldo, tri);
     else
       gemm64_kernel<true, 0><<<grid, THREADS, SMEM, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb,
-                                                                    beta, C, ldc, out, ldo);
+                                                                    beta, C, ldc, out, ldo, tri);
   } else {
     if (sub)
       gemm64_kernel<false, 1><<<grid, THREADS, SMEM, ctx->stream>>>(m, n, k, alpha, A, lda, B,
-                                                                     ldb, beta, C, ldc, out, ldo);
+                                                                     ldb, beta, C, ldc, out, ldo, tri);
     else
       gemm64_kernel<false, 0><<<grid, THREADS, SMEM, ctx->stream>>>(m, n, k, alpha, A, lda, B,
-                                                                     ldb, beta, C, ldc, out, ldo);
+                                                                     ldb, beta, C, ldc, out, ldo, tri);
   }
   count_launch(ctx);
   DS_CHECK_LAUNCH();
   return DS_OK;
 }
 
-template <>
-int gemm_launch<float>(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A,
-                       int64_t lda, const float* B, int64_t ldb, double beta, const float* C,
-                       int64_t ldc, float* out, int64_t ldo) {
+static int gemm_impl(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A,
+                     int64_t lda, const float* B, int64_t ldb, double beta, const float* C,
+                     int64_t ldc, float* out, int64_t ldo, int tri) {
   if (m == 0 || n == 0) return DS_OK;
   dim3 grid((unsigned)ceil_div(m, 64), (unsigned)ceil_div(n, 64));
   if (alpha == -1.0 && beta == 1.0)
     gemm32_kernel<1><<<grid, 256, 0, ctx->stream>>>(m, n, k, (float)alpha, A, lda, B, ldb,
-                                                    (float)beta, C, ldc, out, ldo);
+                                                    (float)beta, C, ldc, out, ldo, tri);
   else
     gemm32_kernel<0><<<grid, 256, 0, ctx->stream>>>(m, n, k, (float)alpha, A, lda, B, ldb,
-                                                    (float)beta, C, ldc, out, ldo);
+                                                    (float)beta, C, ldc, out, ldo, tri);
   count_launch(ctx);
   DS_CHECK_LAUNCH();
   return DS_OK;
 }
+
+template <>
+int gemm_launch<double>(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha,
+                        const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                        const double* C, int64_t ldc, double* out, int64_t ldo) {
+  return gemm_impl(ctx, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, out, ldo, 0);
+}
+template <>
+int gemm_launch<float>(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const float* A,
+                       int64_t lda, const float* B, int64_t ldb, double beta, const float* C,
+                       int64_t ldc, float* out, int64_t ldo) {
+  return gemm_impl(ctx, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, out, ldo, 0);
+}
+template <typename T>
+int gemm_sub_lower_launch(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, int64_t lda,
+                          const T* B, int64_t ldb, T* C, int64_t ldc) {
+  return gemm_impl(ctx, m, n, k, -1.0, A, lda, B, ldb, 1.0, C, ldc, C, ldc, 1);
+}
+template int gemm_sub_lower_launch<double>(ds_ctx*, int64_t, int64_t, int64_t, const double*, int64_t,
+                                           const double*, int64_t, double*, int64_t);
+template int gemm_sub_lower_launch<float>(ds_ctx*, int64_t, int64_t, int64_t, const float*, int64_t,
+                                          const float*, int64_t, float*, int64_t);
 
 // ============================================================================
 // TRSM (backends.py:176-200).

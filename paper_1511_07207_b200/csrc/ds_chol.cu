@@ -1,0 +1,301 @@
+// ds_chol.cu — blocked right-looking Cholesky and cholesky_solve on sm_100a.
+//
+// Restates direct.cholesky_factor (/root/reference/pkg/src/densolve/direct.py:87-120)
+// and direct.cholesky_solve (direct.py:166-171).
+//
+// The reference factors each b-wide panel column by column to full height
+// (sqrt, reciprocal scale, rank-1 update restricted to the panel columns) and
+// then applies one GEMM to the whole trailing square.  The column recurrence of
+// a panel separates by rows: the b x b diagonal block is factored first (one
+// CTA, chol_diag_kernel), after which every row below it runs the same column
+// sequence independently (chol_rows_kernel, one thread per row, the row's b
+// entries in registers).  Both kernels use the reference's rounding step for
+// step (reciprocal in the array dtype, product then subtract), so a panel is
+// bitwise the reference's; there is no grid-wide barrier at all.
+//
+// Trailing update: only the lower triangle of W is ever read again (the panel
+// reads W[i:, i]; the result is tril(W)), so the trailing square gets a
+// lower-tile SYRK on the FP64 DMMA GEMM (gemm_sub_lower_launch, tiles strictly
+// above the diagonal skipped: half the reference's GEMM flops).  As in the LU
+// path the b-panels are grouped into NB = 256 outer panels (K = NB trailing
+// update); exact-arithmetic identical, rounding grouped differently.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "ds_common.cuh"
+#include "ds_kernels.cuh"
+
+namespace ds {
+
+constexpr int kCholW = 64;  // widest b-panel factored by the exact column kernels
+
+__device__ __forceinline__ double sqrt_rn(double x) { return __dsqrt_rn(x); }
+__device__ __forceinline__ float sqrt_rn(float x) { return __fsqrt_rn(x); }
+
+// Factor the nbw x nbw diagonal block W[ib:ib+nbw, ib:ib+nbw] (lower part) with
+// the reference's column loop (direct.py:104-115).  err: first failing index.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    chol_diag_kernel(T* __restrict__ W, int64_t ld, int64_t ib, int nbw, long long* err) {
+  __shared__ T D[kCholW][kCholW + 1];  // D[r][c]
+  __shared__ T s_rinv;
+  __shared__ int s_fail;
+  if (*((volatile long long*)err) >= 0) return;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < nbw * nbw; e += blockDim.x) {
+    const int r = e % nbw, c = e / nbw;
+    if (r >= c) D[r][c] = W[(ib + r) + (ib + c) * ld];
+  }
+  if (tid == 0) s_fail = 0;
+  __syncthreads();
+  for (int i = 0; i < nbw; ++i) {
+    if (tid == 0) {
+      const T aii = D[i][i];
+      if (!(aii > T(0)) || !isfinite((double)aii)) {  // direct.py:106-107
+        s_fail = 1;
+        *err = (long long)(ib + i);
+      } else {
+        const T d = sqrt_rn(aii);      // W[i, i] = np.sqrt(aii)
+        D[i][i] = d;
+        s_rinv = div_rn(T(1), d);      // 1.0 / W[i, i] in the array dtype
+      }
+    }
+    __syncthreads();
+    if (s_fail) return;
+    const T rinv = s_rinv;
+    for (int r = i + 1 + tid; r < nbw; r += blockDim.x) D[r][i] = mul_rn(rinv, D[r][i]);  // scal
+    __syncthreads();
+    // ger restricted to the panel: W[r, j] += -1 * (W[r, i] * W[j, i]), i < j <= r
+    const int w = nbw - i - 1;
+    for (int e = tid; e < w * w; e += blockDim.x) {
+      const int r = i + 1 + e % w, j = i + 1 + e / w;
+      if (j <= r) D[r][j] = sub_rn(D[r][j], mul_rn(D[r][i], D[j][i]));
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < nbw * nbw; e += blockDim.x) {
+    const int r = e % nbw, c = e / nbw;
+    if (r >= c) W[(ib + r) + (ib + c) * ld] = D[r][c];
+  }
+}
+
+// Rows r in [r0, n): the same column sequence on W[r, ib:ib+nbw] given the
+// factored diagonal block (direct.py:110-115 restricted to row r).
+template <typename T>
+__global__ void __launch_bounds__(128)
+    chol_rows_kernel(T* __restrict__ W, int64_t ld, int64_t n, int64_t ib, int nbw, int64_t r0,
+                     const long long* err) {
+  __shared__ T Lc[kCholW][kCholW];  // Lc[i][j] = L[ib + j, ib + i] (column i contiguous)
+  __shared__ T rinv[kCholW];
+  if (*((volatile const long long*)err) >= 0) return;
+  for (int e = threadIdx.x; e < nbw * nbw; e += blockDim.x) {
+    const int j = e % nbw, i = e / nbw;
+    Lc[i][j] = j >= i ? W[(ib + j) + (ib + i) * ld] : T(0);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nbw; i += blockDim.x) rinv[i] = div_rn(T(1), Lc[i][i]);
+  __syncthreads();
+  const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  T x[kCholW];
+#pragma unroll
+  for (int i = 0; i < kCholW; ++i) x[i] = i < nbw ? W[r + (ib + i) * ld] : T(0);
+#pragma unroll
+  for (int i = 0; i < kCholW; ++i) {
+    if (i < nbw) {
+      const T l = mul_rn(rinv[i], x[i]);
+      x[i] = l;
+#pragma unroll
+      for (int j = i + 1; j < kCholW; ++j)
+        if (j < nbw) x[j] = sub_rn(x[j], mul_rn(l, Lc[i][j]));
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kCholW; ++i)
+    if (i < nbw) W[r + (ib + i) * ld] = x[i];
+}
+
+// out[c + k * ldo] = in[k + c * ldi]  for k < rows, c < cols  (32x32 smem tiles)
+template <typename T>
+__global__ void transpose_kernel(int64_t rows, int64_t cols, const T* __restrict__ in, int64_t ldi,
+                                 T* __restrict__ out, int64_t ldo) {
+  __shared__ T t[32][33];
+  const int64_t k0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int64_t k = k0 + threadIdx.x, c = c0 + j;
+    if (k < rows && c < cols) t[j][threadIdx.x] = in[k + c * ldi];
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int64_t c = c0 + threadIdx.x, k = k0 + j;
+    if (k < rows && c < cols) out[c + k * ldo] = t[threadIdx.x][j];
+  }
+}
+
+// np.tril: zero the strict upper triangle
+template <typename T>
+__global__ void tril_kernel(int64_t n, T* __restrict__ W, int64_t ld) {
+  const int64_t c = blockIdx.y;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < c && r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    W[r + c * ld] = T(0);
+}
+
+template <typename T>
+static int transpose_launch(ds_ctx* ctx, int64_t rows, int64_t cols, const T* in, int64_t ldi, T* out,
+                            int64_t ldo) {
+  if (rows == 0 || cols == 0) return DS_OK;
+  dim3 grid((unsigned)ceil_div(rows, 32), (unsigned)ceil_div(cols, 32));
+  transpose_kernel<T><<<grid, dim3(32, 8), 0, ctx->stream>>>(rows, cols, in, ldi, out, ldo);
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+
+template <typename T>
+int chol_factor_impl(ds_ctx* ctx, int64_t n, T* W, int64_t ld, int64_t b, long long* d_err) {
+  const int64_t NB = (b >= 256 || b >= n) ? std::min<int64_t>(b, n)
+                                          : std::min<int64_t>(n, b * std::max<int64_t>(1, 256 / b));
+  // scratch for the transposed L block (B operand of the SYRK): NB x n
+  void* ws = nullptr;
+  DS_TRY(ctx_workspace(ctx, (size_t)NB * (size_t)n * sizeof(T) + 4096, &ws));
+  T* Bt = (T*)ws;
+  for (int64_t kb = 0; kb < n; kb += NB) {
+    const int64_t bf = std::min<int64_t>(kb + NB, n);
+    for (int64_t ib = kb; ib < bf; ib += b) {
+      const int64_t ibf = std::min<int64_t>(ib + b, bf);
+      // a b-panel wider than kCholW is factored in kCholW-wide slices with a K-slice
+      // GEMM between them (exact-arithmetic identical to the panel's rank-1 sequence)
+      for (int64_t sb = ib; sb < ibf; sb += kCholW) {
+        const int64_t sbf = std::min<int64_t>(sb + kCholW, ibf);
+        const int nbw = (int)(sbf - sb);
+        chol_diag_kernel<T><<<1, 256, 0, ctx->stream>>>(W, ld, sb, nbw, d_err);
+        count_launch(ctx);
+        if (sbf < n) {
+          const int64_t rows = n - sbf;
+          chol_rows_kernel<T><<<(unsigned)ceil_div(rows, 128), 128, 0, ctx->stream>>>(W, ld, n, sb, nbw,
+                                                                                    sbf, d_err);
+          count_launch(ctx);
+        }
+        DS_CHECK_LAUNCH();
+        // rest of the panel / outer panel: W[sbf:, sbf:bf] -= W[sbf:, sb:sbf] W[sbf:bf, sb:sbf]^T
+        if (sbf < bf) {
+          const int64_t w = bf - sbf;
+          DS_TRY(transpose_launch<T>(ctx, nbw, w, W + sbf + sb * ld, ld, Bt, nbw));
+          DS_TRY(gemm_sub_lower_launch<T>(ctx, n - sbf, w, nbw, W + sbf + sb * ld, ld, Bt, nbw,
+                                          W + sbf + sbf * ld, ld));
+        }
+      }
+    }
+    if (bf < n) {  // trailing SYRK (direct.py:117-119), lower tiles only
+      const int64_t K = bf - kb, m = n - bf;
+      DS_TRY(transpose_launch<T>(ctx, K, m, W + bf + kb * ld, ld, Bt, K));
+      DS_TRY(gemm_sub_lower_launch<T>(ctx, m, m, K, W + bf + kb * ld, ld, Bt, K, W + bf + bf * ld, ld));
+    }
+  }
+  dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 64)), (unsigned)n);
+  tril_kernel<T><<<g, 256, 0, ctx->stream>>>(n, W, ld);
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+
+template <typename T>
+__global__ void diag_zero_first_kernel(int64_t n, const T* M, int64_t ld, long long* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (M[i + i * ld] == T(0)) atomicMin(out, (long long)i);
+}
+
+template <typename T>
+int chol_solve_impl(ds_ctx* ctx, int64_t n, const T* L, int64_t ld, const T* b, T* x, int64_t* bad) {
+  void* ws = nullptr;
+  const size_t sc = (size_t)(ceil_div(n, 64) + 128) * 4;
+  DS_TRY(ctx_workspace(ctx, (size_t)n * sizeof(T) + sc + 1024, &ws));
+  Carver cv{(char*)ws};
+  long long* d_bad = cv.take<long long>(sizeof(long long) * 2);
+  T* y = cv.take<T>((size_t)n * sizeof(T));
+  char* scratch = cv.take<char>(sc);
+  // forward_substitution(L, b) checks L[i, i] == 0 in sweep order (direct.py:130-134); the
+  // backward sweep on L^T sees the same diagonal
+  const long long init = INT64_MAX;
+  DS_CUDA(cudaMemcpyAsync(d_bad, &init, sizeof(long long), cudaMemcpyHostToDevice, ctx->stream));
+  diag_zero_first_kernel<T><<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 1024), 256, 0, ctx->stream>>>(
+      n, L, ld, d_bad);
+  count_launch(ctx);
+  long long hb = 0;
+  DS_CUDA(cudaMemcpyAsync(&hb, d_bad, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (hb != INT64_MAX) {
+    *bad = hb;
+    set_error("zero diagonal at row %lld", hb);
+    return DS_ESINGULAR;
+  }
+  DS_TRY(trsv_launch<T>(ctx, n, L, ld, b, y, true, false, scratch));       // L y = b
+  DS_TRY(trsv_upper_trans_launch<T>(ctx, n, L, ld, y, x, scratch));        // L^T x = y
+  return DS_OK;
+}
+
+}  // namespace ds
+
+using namespace ds;
+
+extern "C" {
+
+int ds_cholesky_factor(ds_ctx* ctx, int dtype, int64_t n, void* A, int64_t lda, int64_t nb,
+                       int64_t* h_bad_index) {
+  DS_TRY(ctx_begin(ctx));
+  if (h_bad_index) *h_bad_index = -1;
+  if (n < 0 || lda < std::max<int64_t>(n, 1)) {
+    set_error("cholesky: bad shape n=%lld lda=%lld", (long long)n, (long long)lda);
+    return DS_EDIM;
+  }
+  if (nb < 1) {
+    set_error("block size must be >= 1");
+    return DS_EINVAL;
+  }
+  if (n == 0) return DS_OK;
+  if (nb > n) nb = n;
+  // symmetric gate (direct.py:99-101)
+  double md = 0, am = 0;
+  DS_TRY(ds_symmetry_check(ctx, dtype, n, A, lda, &md, &am));
+  const double u = dtype == DS_F64 ? 1.1102230246251565e-16 : 5.960464477539063e-08;
+  if (md > 10.0 * u * am) {
+    set_error("matrix is not symmetric");
+    return DS_ENOTSPD;
+  }
+  long long* d_err = nullptr;
+  DS_CUDA(cudaMallocAsync((void**)&d_err, sizeof(long long), ctx->stream));
+  DS_CUDA(cudaMemsetAsync(d_err, 0xFF, sizeof(long long), ctx->stream));  // -1
+  int rc = DS_OK;
+  DS_DISPATCH(dtype, T, rc = chol_factor_impl<T>(ctx, n, (T*)A, lda, nb, d_err));
+  long long herr = -1;
+  DS_CUDA(cudaMemcpyAsync(&herr, d_err, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+  DS_CUDA(cudaFreeAsync(d_err, ctx->stream));
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (rc != DS_OK) return rc;
+  if (herr >= 0) {
+    if (h_bad_index) *h_bad_index = herr;
+    set_error("nonpositive pivot at index %lld", herr);
+    return DS_ENOTSPD;
+  }
+  return DS_OK;
+}
+
+int ds_cholesky_solve(ds_ctx* ctx, int dtype, int64_t n, const void* L, int64_t ldl, const void* b,
+                      void* x, int64_t* h_bad_row) {
+  DS_TRY(ctx_begin(ctx));
+  if (h_bad_row) *h_bad_row = -1;
+  if (n == 0) return DS_OK;
+  int64_t bad = -1;
+  int rc = DS_OK;
+  DS_DISPATCH(dtype, T, rc = chol_solve_impl<T>(ctx, n, (const T*)L, ldl, (const T*)b, (T*)x, &bad));
+  if (rc == DS_ESINGULAR && h_bad_row) *h_bad_row = bad;
+  if (rc != DS_OK) return rc;
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return DS_OK;
+}
+
+}  // extern "C"

@@ -85,6 +85,11 @@ template <typename T>
 int gemm_launch(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha, const T* A,
                 int64_t lda, const T* B, int64_t ldb, double beta, const T* C, int64_t ldc, T* out,
                 int64_t ldo);
+// C -= A B on the tiles of C holding some row >= column (C square-indexed from
+// its top-left corner): the lower-triangle SYRK update of the Cholesky path.
+template <typename T>
+int gemm_sub_lower_launch(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, const T* A, int64_t lda,
+                          const T* B, int64_t ldb, T* C, int64_t ldc);
 template <typename T>
 int trsm_lower_unit_launch(ds_ctx* ctx, int64_t b, int64_t m, const T* L, int64_t ldl, const T* B,
                            int64_t ldb, T* Z, int64_t ldz);
@@ -94,5 +99,14 @@ int trsm_upper_launch(ds_ctx* ctx, int64_t b, int64_t m, const T* U, int64_t ldu
 template <typename T>
 int ger_launch(ds_ctx* ctx, int64_t m, int64_t n, const T* A, int64_t lda, double alpha,
                const T* x, const T* y, T* out, int64_t ldo);
+
+// ---- triangular vector solves (ds_lu.cu) -------------------------------------
+// scratch: (ceil(n/64) + 64) ints
+template <typename T>
+int trsv_launch(ds_ctx* ctx, int64_t n, const T* M, int64_t ld, const T* rhs, T* out, bool lower,
+                bool unit, char* scratch);
+template <typename T>
+int trsv_upper_trans_launch(ds_ctx* ctx, int64_t n, const T* M, int64_t ld, const T* rhs, T* out,
+                            char* scratch);
 
 }  // namespace ds

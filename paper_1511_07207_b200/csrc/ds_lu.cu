@@ -789,7 +789,11 @@ __global__ void gather_kernel(int64_t n, const int* __restrict__ idx, const T* _
 constexpr int kTrsvNB = 64;
 constexpr int kTrsvThreads = 256;
 
-template <typename T, bool LOWER, bool UNIT>
+// TRANS (upper only): solve with U = M^T, i.e. U[i,j] = M[j + i*ld] (the
+// backward sweep of cholesky_solve on L^T, direct.py:166-171, without forming
+// L^T); the off-diagonal tiles are staged transposed through shared memory so
+// the loads stay coalesced.
+template <typename T, bool LOWER, bool UNIT, bool TRANS = false>
 __global__ void __launch_bounds__(kTrsvThreads)
     trsv_kernel(int64_t n, const T* __restrict__ M, int64_t ld, const T* __restrict__ rhs,
                 T* out, int* flags, int* ticket) {
@@ -797,6 +801,7 @@ __global__ void __launch_bounds__(kTrsvThreads)
   __shared__ double part[kTrsvThreads / kTrsvNB][kTrsvNB];
   __shared__ T xs[kTrsvNB];
   __shared__ T ysol[kTrsvNB];
+  __shared__ T tile[TRANS ? kTrsvNB : 1][TRANS ? kTrsvNB + 1 : 1];
   const int64_t nblk = ceil_div(n, kTrsvNB);
   if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1);
   __syncthreads();
@@ -817,10 +822,20 @@ __global__ void __launch_bounds__(kTrsvThreads)
     }
     __syncthreads();
     if (threadIdx.x < nc) xs[threadIdx.x] = ((volatile T*)out)[c0 + threadIdx.x];
+    if (TRANS) {
+      // tile[r][c] = U[r0 + r, c0 + c] = M[(c0 + c) + (r0 + r) * ld]; consecutive threads read
+      // consecutive c (contiguous in M)
+      for (int e = threadIdx.x; e < kTrsvNB * kTrsvNB; e += kTrsvThreads) {
+        const int c = e % kTrsvNB, r = e / kTrsvNB;
+        if (r < nr && c < nc) tile[r][c] = M[(c0 + c) + (r0 + r) * ld];
+      }
+    }
     __syncthreads();
     if (rr < nr)
-      for (int c = cg; c < nc; c += kTrsvThreads / kTrsvNB)
-        acc = fma((double)M[(r0 + rr) + (c0 + c) * ld], (double)xs[c], acc);
+      for (int c = cg; c < nc; c += kTrsvThreads / kTrsvNB) {
+        const T mv = TRANS ? tile[rr][c] : M[(r0 + rr) + (c0 + c) * ld];
+        acc = fma((double)mv, (double)xs[c], acc);
+      }
     __syncthreads();
   }
   part[cg][rr] = acc;
@@ -845,8 +860,10 @@ __global__ void __launch_bounds__(kTrsvThreads)
     } else {
       for (int r = nr - 1; r >= 0; --r) {
         double s = 0.0;
-        for (int c = r + 1 + lane; c < nr; c += 32)
-          s = fma((double)M[(r0 + r) + (r0 + c) * ld], (double)ysol[c], s);
+        for (int c = r + 1 + lane; c < nr; c += 32) {
+          const T mv = TRANS ? M[(r0 + c) + (r0 + r) * ld] : M[(r0 + r) + (r0 + c) * ld];
+          s = fma((double)mv, (double)ysol[c], s);
+        }
         s = warp_sum(s);
         if (lane == 0) {
           double off = s;
@@ -881,6 +898,25 @@ __global__ void diag_zero_kernel(int64_t n, const T* M, int64_t ld, int lower, l
 }
 
 template <typename T>
+int trsv_upper_trans_launch(ds_ctx* ctx, int64_t n, const T* M, int64_t ld, const T* rhs, T* out,
+                            char* scratch) {
+  if (n == 0) return DS_OK;
+  const int64_t nblk = ceil_div(n, kTrsvNB);
+  int* ticket = (int*)scratch;
+  int* flags = ticket + 64;
+  DS_CUDA(cudaMemsetAsync(scratch, 0, (64 + nblk) * sizeof(int), ctx->stream));
+  trsv_kernel<T, false, false, true><<<(unsigned)nblk, kTrsvThreads, 0, ctx->stream>>>(
+      n, M, ld, rhs, out, flags, ticket);
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+template int trsv_upper_trans_launch<double>(ds_ctx*, int64_t, const double*, int64_t, const double*,
+                                             double*, char*);
+template int trsv_upper_trans_launch<float>(ds_ctx*, int64_t, const float*, int64_t, const float*,
+                                            float*, char*);
+
+template <typename T>
 int trsv_launch(ds_ctx* ctx, int64_t n, const T* M, int64_t ld, const T* rhs, T* out, bool lower,
                 bool unit, char* scratch) {
   if (n == 0) return DS_OK;
@@ -901,6 +937,11 @@ int trsv_launch(ds_ctx* ctx, int64_t n, const T* M, int64_t ld, const T* rhs, T*
   DS_CHECK_LAUNCH();
   return DS_OK;
 }
+
+template int trsv_launch<double>(ds_ctx*, int64_t, const double*, int64_t, const double*, double*,
+                                 bool, bool, char*);
+template int trsv_launch<float>(ds_ctx*, int64_t, const float*, int64_t, const float*, float*, bool,
+                                bool, char*);
 
 template <typename T>
 int diag_check(ds_ctx* ctx, int64_t n, const T* M, int64_t ld, bool lower, int64_t* bad,

@@ -6,6 +6,8 @@
   lu_solve(f, b)                     direct.py:155-163
   forward_substitution(L, b, unit_diagonal=False)   direct.py:123-136
   backward_substitution(U, y)                        direct.py:139-152
+  cholesky_factor(A, b, backend)                     direct.py:87-120
+  cholesky_solve(f, b)                               direct.py:166-171
 
 Factorization runs in libdensolve_b200 (ds_lu_factor): cooperative panel kernel
 (first-max pivot search, swap, reciprocal scale, rank-1 panel update — NumPy
@@ -24,7 +26,8 @@ import numpy as np
 
 from . import _lib
 from .backends import as_b200
-from .core import (DimensionError, LuFactors, SingularMatrixError, check_precision, check_square)
+from .core import (CholeskyFactor, DimensionError, LuFactors, NotSpdError, SingularMatrixError,
+                   check_precision, check_square)
 from .device import DeviceArray, is_device, to_device
 
 
@@ -141,4 +144,59 @@ def lu_solve(f: LuFactors, b):
     piv = np.ascontiguousarray(np.asarray(f.pivots, dtype=np.int64))
     _lib.check(ctx.lib.ds_lu_solve(ctx.handle, dLU.dcode, f.n, c_void_p(dLU.ptr), dLU.ld,
                                    piv.ctypes.data_as(c_void_p), c_void_p(db.ptr), c_void_p(dx.ptr)))
+    return dx if is_device(b) else dx.to_host()
+
+
+def _tally_cholesky(be, n: int, b: int):
+    """direct.py:103-119 counter tallies: scal per column, ger inside the panel, one gemm per panel."""
+    i = np.arange(n, dtype=np.int64)
+    bf = np.minimum((i // b + 1) * b, n)
+    tail = n - i - 1
+    live = tail > 0
+    be.tally("scal", int(tail[live].sum()), calls=int(live.sum()))
+    g = i + 1 < bf
+    be.tally("ger", int((2 * tail[g] * (bf[g] - i[g] - 1)).sum()), calls=int(g.sum()))
+    for kb in range(0, n, b):
+        bf_ = min(kb + b, n)
+        if bf_ < n:
+            be.tally("gemm", 2 * (n - bf_) * (n - bf_) * (bf_ - kb))
+
+
+def cholesky_factor(A, b: int, backend=None) -> CholeskyFactor:
+    """Blocked right-looking Cholesky: exact panel kernels (diagonal block + per-row column
+    sweep) and a lower-tile FP64 DMMA SYRK for the trailing update."""
+    be = as_b200(backend)
+    n = check_square(A)
+    check_precision(A)
+    if b < 1:
+        raise ValueError("block size must be >= 1")
+    b = min(b, n)
+    ctx = be.ctx
+    src = to_device(A, ctx)
+    W = src.copy() if is_device(A) else src  # never mutate the caller's A (direct.py:102)
+    bad = c_int64(-1)
+    st = ctx.lib.ds_cholesky_factor(ctx.handle, W.dcode, n, c_void_p(W.ptr), W.ld, max(b, 1),
+                                    ctypes.byref(bad))
+    if st == _lib.DS_ENOTSPD:
+        idx = int(bad.value)
+        raise NotSpdError(_lib.last_error(), index=None if idx < 0 else idx)
+    _lib.check(st)
+    _tally_cholesky(be, n, max(b, 1))
+    return CholeskyFactor(l=W if is_device(A) else W.to_host(), device=W)
+
+
+def cholesky_solve(f: CholeskyFactor, b):
+    """Solve L y = b then L^T x = y (the transposed sweep reads L in place)."""
+    if tuple(b.shape) != (f.n,):
+        raise DimensionError(f"rhs shape {tuple(b.shape)} does not conform to n={f.n}")
+    check_precision(f.l, b)
+    dL = f.device if isinstance(f.device, DeviceArray) else None
+    ctx = dL.ctx if dL is not None else _solve_ctx(f.l, b)
+    if dL is None:
+        dL = to_device(f.l, ctx)
+    db = to_device(b, ctx)
+    dx = DeviceArray(ctx, (f.n,), dL.dtype)
+    bad = c_int64(-1)
+    _lib.check(ctx.lib.ds_cholesky_solve(ctx.handle, dL.dcode, f.n, c_void_p(dL.ptr), dL.ld,
+                                         c_void_p(db.ptr), c_void_p(dx.ptr), ctypes.byref(bad)))
     return dx if is_device(b) else dx.to_host()
