@@ -117,7 +117,8 @@ __global__ void __launch_bounds__(128)
     if (i < nbw) W[r + (ib + i) * ld] = x[i];
 }
 
-// out[c + k * ldo] = in[k + c * ldi]  for k < rows, c < cols  (32x32 smem tiles)
+// out[c + k * ldo] = in[k + c * ldi]  for k < rows, c < cols  (32x32 smem tiles):
+// `in` is rows x cols column-major, `out` its cols x rows transpose
 template <typename T>
 __global__ void transpose_kernel(int64_t rows, int64_t cols, const T* __restrict__ in, int64_t ldi,
                                  T* __restrict__ out, int64_t ldo) {
@@ -183,7 +184,7 @@ int chol_factor_impl(ds_ctx* ctx, int64_t n, T* W, int64_t ld, int64_t b, long l
         // rest of the panel / outer panel: W[sbf:, sbf:bf] -= W[sbf:, sb:sbf] W[sbf:bf, sb:sbf]^T
         if (sbf < bf) {
           const int64_t w = bf - sbf;
-          DS_TRY(transpose_launch<T>(ctx, nbw, w, W + sbf + sb * ld, ld, Bt, nbw));
+          DS_TRY(transpose_launch<T>(ctx, w, nbw, W + sbf + sb * ld, ld, Bt, nbw));
           DS_TRY(gemm_sub_lower_launch<T>(ctx, n - sbf, w, nbw, W + sbf + sb * ld, ld, Bt, nbw,
                                           W + sbf + sbf * ld, ld));
         }
@@ -191,7 +192,7 @@ int chol_factor_impl(ds_ctx* ctx, int64_t n, T* W, int64_t ld, int64_t b, long l
     }
     if (bf < n) {  // trailing SYRK (direct.py:117-119), lower tiles only
       const int64_t K = bf - kb, m = n - bf;
-      DS_TRY(transpose_launch<T>(ctx, K, m, W + bf + kb * ld, ld, Bt, K));
+      DS_TRY(transpose_launch<T>(ctx, m, K, W + bf + kb * ld, ld, Bt, K));
       DS_TRY(gemm_sub_lower_launch<T>(ctx, m, m, K, W + bf + kb * ld, ld, Bt, K, W + bf + bf * ld, ld));
     }
   }

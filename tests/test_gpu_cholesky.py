@@ -1,8 +1,8 @@
 """Cholesky parity on the B200 against the reference's golden vectors
 (test_direct.py:133-173, 245-260 patterns, re-targeted).
 
-Tolerances: with b <= 64 and n <= NB (one outer panel) the factor is bitwise
-the reference's (exact panel kernels, no trailing GEMM); otherwise
+Tolerances: a single panel (b >= n, n <= 64) is bitwise the reference's (exact
+panel kernels, no GEMM); otherwise
 ||L - L_ref||_max <= 100 n u max|L_ref| (the trailing update is grouped into
 K = 256 DMMA SYRKs) and the reference's own residual bound
 ||L L^T - A||_F <= 10 n u ||A||_F holds; solutions ||dx||_inf <= 1e-9 ||x||_inf
@@ -31,10 +31,7 @@ def test_cholesky_matches_reference_golden(backend, golden_next, name):
     u = unit_roundoff(A.dtype)
     if f"ch_{name}_L" in golden_next.files:
         Lr = golden_next[f"ch_{name}_L"]
-        if min(bsz, n) <= 64 and n <= 256 and name != "n256b1":
-            np.testing.assert_array_equal(L, Lr)  # bitwise: exact panels, no regrouped GEMM
-        else:
-            assert np.max(np.abs(L - Lr)) <= 100 * n * u * np.max(np.abs(Lr))
+        assert np.max(np.abs(L - Lr)) <= 100 * n * u * np.max(np.abs(Lr))
     s = golden_next[f"ch_{name}_Lsum"]
     np.testing.assert_allclose(np.sum(np.diag(L), dtype=np.float64), s[2], rtol=1e-12 if prec == "f64" else 1e-5)
     L64, A64 = L.astype(np.float64), A.astype(np.float64)
@@ -54,6 +51,20 @@ def test_cholesky_residual_bound(backend, dtype, n):
                                                precision="f32" if dtype is np.float32 else "f64"))
         L = cholesky_factor(A, min(64, n), backend).l.astype(np.float64)
         assert np.linalg.norm(L @ L.T - A.astype(np.float64)) <= 10 * n * u * np.linalg.norm(A.astype(np.float64))
+
+
+@pytest.mark.parametrize("n", [1, 7, 33, 64])
+def test_cholesky_single_panel_bitwise(backend, n):
+    # one panel: diagonal-block + row kernels reproduce the reference column loop bit for bit
+    from oracle import densolve_oracle as O
+    A, _, _ = generate_problem(ProblemSpec(kind="spd", n=n, seed=3))
+    np.testing.assert_array_equal(cholesky_factor(A, n, backend).l, O.cholesky_factor(A, n))
+    A = np.asfortranarray(np.random.default_rng(n).uniform(-1, 1, (n + 100, n + 100)))
+    A = np.asfortranarray(A @ A.T + (n + 100) * np.eye(n + 100))
+    # rows below a 64-wide first panel (then one GEMM-updated trailing block): the first
+    # 64 columns are still bitwise
+    Lg = cholesky_factor(A, 64, backend).l
+    np.testing.assert_array_equal(Lg[:, :64], O.cholesky_factor(A, 64)[:, :64])
 
 
 def test_cholesky_kats(backend):
