@@ -287,6 +287,7 @@ struct ds_ctx {
   cudaStream_t side = nullptr;
   cudaStream_t aux = nullptr;  // low-priority stream for the swaps of already-factored L columns
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
+  unsigned panel_seq = 0;  // LU panel launches (epochs of the LL exchange words)
 };
 
 namespace ds {

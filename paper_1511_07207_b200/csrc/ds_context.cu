@@ -128,6 +128,12 @@ int ds_ctx_create(int device, ds_ctx** out) {
   c->smem_optin = prop.sharedMemPerBlockOptin;
   DS_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->own_stream = true;
+  {  // keep up to 32 GiB of freed operand memory in the pool (ds_malloc / ds_free)
+    cudaMemPool_t pool;
+    DS_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = 32ull << 30;
+    DS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
   *out = c;
   return DS_OK;
 }
@@ -176,20 +182,21 @@ int ds_ctx_kernel_launches(ds_ctx* ctx, int64_t* out) {
   return DS_OK;
 }
 
+// Device buffers come from the device's stream-ordered memory pool with an unlimited
+// release threshold: a multi-GB operand freed and re-allocated between solves is
+// recycled without a cudaMalloc / cudaFree round trip (no implicit device sync).
 int ds_malloc(ds_ctx* ctx, size_t bytes, void** out) {
   DS_TRY(ctx_begin(ctx));
   *out = nullptr;
   if (bytes == 0) bytes = 16;
-  DS_CUDA(cudaMalloc(out, bytes));
+  DS_CUDA(cudaMallocAsync(out, bytes, ctx->stream));
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));  // the buffer is usable on any stream on return
   return DS_OK;
 }
 
 int ds_free(ds_ctx* ctx, void* p) {
   DS_TRY(ctx_begin(ctx));
-  if (p) {
-    DS_CUDA(cudaStreamSynchronize(ctx->stream));
-    DS_CUDA(cudaFree(p));
-  }
+  if (p) DS_CUDA(cudaFreeAsync(p, ctx->stream));
   return DS_OK;
 }
 

@@ -18,6 +18,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <ctime>
 #include <vector>
 
 #include "ds_common.cuh"
@@ -25,7 +28,12 @@
 
 namespace ds {
 
-constexpr int kPanelThreads = 256;
+// 128 threads: a panel CTA (<= 32 regs/thread) then fits beside two trailing-GEMM
+// CTAs (240 regs x 128 threads each) on one SM, so the look-ahead panel running on
+// the side stream does not evict half of the GEMM's occupancy.
+constexpr int kPanelThreads = 128;
+// register-row panel kernel: TPR threads per row (2 or 4), <= kPanelRegThreads threads
+constexpr int kPanelRegThreads = 512;
 
 __device__ __forceinline__ bool piv_better(double av, int64_t ai, double bv, int64_t bi) {
   const bool an = av != av, bn = bv != bv;
@@ -50,7 +58,18 @@ struct PanelArgs {
   void* rowI;          // global kernel: row i before the swap
   int per;             // rows per CTA
   int ldt;             // smem tile leading dimension
+  uint64_t* ll_hdr;    // smem kernel: [2][grid][kHdrWords] LL candidate headers
+  uint64_t* ll_row;    // smem kernel: [2][grid][kPanelMaxW * words/value] LL candidate rows
+  uint64_t* ll_diag;   // smem kernel: [2][kPanelMaxW * words/value] LL row i
+  unsigned seq;        // per-context panel launch counter (LL epochs)
+  unsigned long long* trace;  // optional [grid][ncol][4] %globaltimer stamps (DENSOLVE_PANEL_TRACE)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 constexpr int kPanelMaxW = 64;
 
@@ -81,132 +100,369 @@ __device__ __forceinline__ void block_argmax(double& bv, int64_t& bi, double* sv
   }
 }
 
-// Warp 0 reduces the G published candidates (parallel loads, shuffle tree, fixed
-// order => identical result in every CTA); returns the pivot row in s_piv.
+// Every thread loads at most a few of the G published candidates (one L2 round
+// trip for G <= blockDim.x), then a block-wide first-max reduction in a fixed
+// order => the identical pivot in every CTA; returned in s_piv.
 __device__ __forceinline__ void reduce_candidates(const PanelArgs& a, int par, int64_t i,
-                                                  int64_t* s_piv) {
-  if (threadIdx.x < 32) {
-    const unsigned G = gridDim.x;
-    double bv = -1.0;
-    int64_t bi = INT64_MAX;
-    for (unsigned b = threadIdx.x; b < G; b += 32) {
-      const double v = __ldcg(a.cand_v + par * G + b);
-      const int64_t ix = __ldcg(a.cand_i + par * G + b);
-      if (piv_better(v, ix, bv, bi)) {
-        bv = v;
-        bi = ix;
-      }
+                                                  int64_t* s_piv, double* sv, int64_t* si) {
+  const unsigned G = gridDim.x;
+  double bv = -1.0;
+  int64_t bi = INT64_MAX;
+  for (unsigned b0 = threadIdx.x; b0 < G; b0 += 2 * blockDim.x) {
+    const unsigned b1 = b0 + blockDim.x;  // both loads issued before either compare
+    const double v0 = __ldcg(a.cand_v + par * G + b0);
+    const int64_t i0 = __ldcg(a.cand_i + par * G + b0);
+    double v1 = -1.0;
+    int64_t i1 = INT64_MAX;
+    if (b1 < G) {
+      v1 = __ldcg(a.cand_v + par * G + b1);
+      i1 = __ldcg(a.cand_i + par * G + b1);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (piv_better(ov, oi, bv, bi)) {
-        bv = ov;
-        bi = oi;
-      }
+    if (piv_better(v0, i0, bv, bi)) {
+      bv = v0;
+      bi = i0;
     }
-    if (threadIdx.x == 0) *s_piv = bi == INT64_MAX ? i : bi;
+    if (piv_better(v1, i1, bv, bi)) {
+      bv = v1;
+      bi = i1;
+    }
   }
+  block_argmax(bv, bi, sv, si);
+  if (threadIdx.x == 0) *s_piv = bi == INT64_MAX ? i : bi;
   __syncthreads();
 }
 
-// Panel factorization with the CTA's rows resident in shared memory; one grid
-// barrier per column.  Before the barrier every CTA publishes its local
-// candidate (value, row, and the row's panel values) and the owner of row i
-// publishes row i; after it every CTA picks the same pivot and already holds
-// everything the swap and the rank-1 update need.
+// ---- LL exchange words: 32 data bits + a 32-bit epoch flag in one aligned 8-byte
+// word.  An 8-byte store is single-copy atomic, so a reader that sees the
+// expected flag also sees that store's data: no fence, no atomic, no separate
+// barrier.  Epochs are unique per (panel launch, column) and the buffers are
+// double-buffered by column parity (a CTA can only be one column ahead of the
+// slowest reader).
+__device__ __forceinline__ void ll_store(uint64_t* p, uint32_t data, uint32_t flag) {
+  const uint64_t w = ((uint64_t)flag << 32) | data;
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;\n" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ uint64_t ll_load(const uint64_t* p) {
+  uint64_t w;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+__device__ __forceinline__ bool ll_ok(uint64_t w, uint32_t flag) { return (uint32_t)(w >> 32) == flag; }
+
 template <typename T>
-__global__ void __launch_bounds__(kPanelThreads) lu_panel_smem_kernel(T* __restrict__ W, PanelArgs a) {
+struct LLVal;  // words per value
+template <>
+struct LLVal<double> {
+  static constexpr int W = 2;
+  __device__ static void put(uint64_t* p, double v, uint32_t f) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    ll_store(p, (uint32_t)b, f);
+    ll_store(p + 1, (uint32_t)(b >> 32), f);
+  }
+  __device__ static double get(const uint64_t* w) {
+    return __longlong_as_double((long long)((w[0] & 0xffffffffull) | (w[1] << 32)));
+  }
+};
+template <>
+struct LLVal<float> {
+  static constexpr int W = 1;
+  __device__ static void put(uint64_t* p, float v, uint32_t f) { ll_store(p, __float_as_uint(v), f); }
+  __device__ static float get(const uint64_t* w) { return __uint_as_float((uint32_t)w[0]); }
+};
+
+// First-max argmax over the CTA with one barrier: warp shuffle tree, one record per
+// warp in shared memory (double-buffered by the caller's slot so back-to-back calls
+// need no trailing barrier), then every thread reduces the warp records in the same
+// order => the identical result in all threads.
+__device__ __forceinline__ void cta_argmax(double& bv, int64_t& bi, double* wv, int64_t* wi) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (piv_better(ov, oi, bv, bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    wv[wid] = bv;
+    wi[wid] = bi;
+  }
+  __syncthreads();
+  bv = wv[0];
+  bi = wi[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+    if (piv_better(wv[w], wi[w], bv, bi)) {
+      bv = wv[w];
+      bi = wi[w];
+    }
+}
+
+// First-max argmax over the CTA: keys are the IEEE bits of |v| (monotone for
+// v >= 0, NaN canonicalised above +inf so it wins like np.argmax), reduced with
+// two redux.sync max passes; ties go to the lowest row (a redux.sync min over the
+// top lanes); the warp records are then combined by every thread in the same order
+// (one barrier).  `none` candidates carry key 0 and row INT64_MAX.
+__device__ __forceinline__ unsigned long long piv_key(double v) {
+  return v != v ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(v);
+}
+__device__ __forceinline__ void cta_argmax_key(unsigned long long& key, int64_t& idx,
+                                               unsigned long long* wk, int64_t* wi) {
+  const unsigned hi = (unsigned)(key >> 32);
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned lo = hi == mhi ? (unsigned)key : 0u;
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, lo);
+  const bool top = hi == mhi && (unsigned)key == mlo;
+  // rows < 2^31 - 1; INT64_MAX (none) maps to 0xffffffff
+  const unsigned widx = __reduce_min_sync(0xffffffffu, top ? (unsigned)min(idx, (int64_t)0xffffffff) : 0xffffffffu);
+  const unsigned long long wkey = ((unsigned long long)mhi << 32) | mlo;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+    wk[wid] = wkey;
+    wi[wid] = widx == 0xffffffffu ? INT64_MAX : (int64_t)widx;
+  }
+  __syncthreads();
+  // every warp combines the nw warp records itself (lane w reads record w): the same
+  // reduction in every warp, no second barrier
+  const int nw = (int)(blockDim.x >> 5);
+  const unsigned long long k2 = lane < nw ? wk[lane] : 0ull;
+  const int64_t i2 = lane < nw ? wi[lane] : INT64_MAX;
+  const unsigned h2 = (unsigned)(k2 >> 32);
+  const unsigned mh2 = __reduce_max_sync(0xffffffffu, h2);
+  const unsigned l2 = h2 == mh2 ? (unsigned)k2 : 0u;
+  const unsigned ml2 = __reduce_max_sync(0xffffffffu, l2);
+  const bool top2 = h2 == mh2 && (unsigned)k2 == ml2;
+  const unsigned mi2 = __reduce_min_sync(0xffffffffu, top2 ? (unsigned)min(i2, (int64_t)0xffffffff) : 0xffffffffu);
+  key = ((unsigned long long)mh2 << 32) | ml2;
+  idx = mi2 == 0xffffffffu ? INT64_MAX : (int64_t)mi2;
+}
+
+// Panel factorization, one row per thread held in REGISTERS (rows <= 256 per CTA,
+// i.e. m <= 148 * 256).  The register row is kept rotated: y[k] is the current
+// value of panel column c + k, so every column runs the same straight-line code
+// (static register indices): the update touches y[1..63], then column c retires
+// into the shared-memory array Ls (the final L / U values of columns < c) and the
+// row shifts by one.  Per column every CTA publishes, as LL words, its local
+// candidate header (|v|, row; one 128-byte line per CTA) and the candidate row
+// (written by the owning thread); the owner of row i publishes row i.  Every CTA
+// polls the G headers (the only grid-wide synchronisation), reduces them in a
+// fixed order (the same first-max pivot everywhere), polls the winner's row and
+// row i, and every thread swaps / scales / rank-1-updates its own row (NumPy
+// rounding: bitwise the reference).
+constexpr int kHdrWords = 16;  // |v| (2 words), row (1 word), padding to a 128-byte line
+template <typename T, int TPR>
+__global__ void __launch_bounds__(kPanelRegThreads, 1) lu_panel_smem_kernel(T* __restrict__ W, PanelArgs a) {
+  constexpr int PW = kPanelMaxW / TPR;  // panel columns per thread
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* tile = reinterpret_cast<T*>(smem_raw);  // [ncol][ldt]
-  __shared__ double sv[32];
-  __shared__ int64_t si[32];
-  __shared__ int64_t s_piv;
-  __shared__ T prow[kPanelMaxW];
-  __shared__ T drow[kPanelMaxW];
+  T* Ls = reinterpret_cast<T*>(smem_raw);  // [ncol][ldt]: retired columns
+  __shared__ unsigned long long wk[2][kPanelRegThreads / 32];
+  __shared__ int64_t wi[2][kPanelRegThreads / 32];
+  __shared__ __align__(16) T stage[2][kPanelMaxW];  // candidate row / diagonal row, columns >= c
+  __shared__ __align__(16) T prow[kPanelMaxW];       // winner row, column order
+  __shared__ __align__(16) T drow[kPanelMaxW];       // row i, column order
+  __shared__ __align__(16) T prs[kPanelMaxW + 2];    // prs[k] = prow[c + k] (0 past the panel)
+  __shared__ __align__(16) T drs[kPanelMaxW + 2];    // drs[k] = drow[c + k]
+  constexpr int VW = LLVal<T>::W;
   const unsigned G = gridDim.x;
   const int per = a.per, ldt = a.ldt;
   const int64_t my_lo = a.kb + (int64_t)blockIdx.x * per;
   const int64_t my_hi = min(a.n, my_lo + per);
   const int nr = (int)(my_hi - my_lo);
   const int ncol = (int)(a.bf - a.kb);
-  T* cand_row = reinterpret_cast<T*>(a.cand_row);
-  T* diag_row = reinterpret_cast<T*>(a.diag_row);
+  uint64_t* hdr = a.ll_hdr;    // [2][G][kHdrWords]
+  uint64_t* rows = a.ll_row;   // [2][G][kPanelMaxW * VW]
+  uint64_t* diag = a.ll_diag;  // [2][kPanelMaxW * VW]
+  const int RW = kPanelMaxW * VW;
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int r = t / TPR, q = t % TPR;  // my row, my column slice [q * PW, (q + 1) * PW)
+  const bool mine = r < nr;
+  const bool lead = mine && q == 0;  // holds the current column c in y[0]
+  const int64_t g = my_lo + r;
+  const int lead_lane = (t & 31) & ~(TPR - 1);
 
-  for (int idx = threadIdx.x; idx < ncol * nr; idx += blockDim.x) {
-    const int j = idx / nr, r = idx % nr;
-    tile[j * ldt + r] = W[(my_lo + r) + (a.kb + j) * a.ld];
+  // y[k] = current value of panel column c + q * PW + k of my row (rotated view)
+  T y[PW];
+#pragma unroll
+  for (int k = 0; k < PW; ++k) {
+    const int j = q * PW + k;
+    y[k] = (mine && j < ncol) ? W[g + (a.kb + j) * a.ld] : T(0);
   }
-  __syncthreads();
-  unsigned epoch = 0;
+
+  auto publish_header = [&](int cc, unsigned long long bk, int64_t bi) {
+    if (t == 0) {
+      const uint32_t ep = a.seq * 128u + (uint32_t)cc + 1u;
+      uint64_t* h = hdr + ((size_t)(cc & 1) * G + blockIdx.x) * kHdrWords;
+      ll_store(h, (uint32_t)bk, ep);
+      ll_store(h + 1, (uint32_t)(bk >> 32), ep);
+      ll_store(h + 2, bi == INT64_MAX ? 0xffffffffu : (uint32_t)bi, ep);
+    }
+  };
+  // candidate row and row kb + cc: the owners stage their register slices (columns >= cc)
+  auto publish_rows = [&](int cc, int64_t bi) {
+    const int par = cc & 1;
+    const uint32_t ep = a.seq * 128u + (uint32_t)cc + 1u;
+    const int64_t ii = a.kb + cc;
+    if (mine && g == bi) {
+#pragma unroll
+      for (int k = 0; k < PW; ++k) stage[0][q * PW + k] = y[k];
+    }
+    if (mine && g == ii) {
+#pragma unroll
+      for (int k = 0; k < PW; ++k) stage[1][q * PW + k] = y[k];
+    }
+    __syncthreads();
+    for (int j = t; j < ncol; j += nt) {
+      if (bi != INT64_MAX) {
+        const T v = j < cc ? Ls[j * ldt + (int)(bi - my_lo)] : stage[0][j - cc];
+        LLVal<T>::put(rows + ((size_t)par * G + blockIdx.x) * RW + j * VW, v, ep);
+      }
+      if (ii >= my_lo && ii < my_hi) {
+        const T v = j < cc ? Ls[j * ldt + (int)(ii - my_lo)] : stage[1][j - cc];
+        LLVal<T>::put(diag + (size_t)par * RW + j * VW, v, ep);
+      }
+    }
+  };
+
+  {
+    unsigned long long bk = lead ? piv_key(fabs((double)y[0])) : 0ull;
+    int64_t bi = lead ? g : INT64_MAX;
+    cta_argmax_key(bk, bi, wk[0], wi[0]);
+    publish_header(0, bk, bi);
+    publish_rows(0, bi);
+  }
   for (int c = 0; c < ncol; ++c) {
     const int64_t i = a.kb + c;
     const int par = c & 1;
-    // ---- phase A: local candidate of column c over my rows >= i
-    const int r0 = (int)max((int64_t)0, i - my_lo);
-    double bv = -1.0;
-    int64_t bi = INT64_MAX;
-    for (int r = r0 + threadIdx.x; r < nr; r += blockDim.x) {
-      const double v = fabs((double)tile[c * ldt + r]);
-      if (piv_better(v, my_lo + r, bv, bi)) {
-        bv = v;
-        bi = my_lo + r;
+    const uint32_t ep = a.seq * 128u + (uint32_t)c + 1u;
+    const long long t_c = clock64();
+    // ---- poll the G headers, reduce (ties -> lowest row)
+    unsigned long long gk = 0ull;
+    int64_t gi = INT64_MAX;
+    for (int b = t; b < (int)G; b += nt) {
+      const uint64_t* h = hdr + ((size_t)par * G + b) * kHdrWords;
+      uint64_t x0, x1, x2;
+      do {
+        x0 = ll_load(h);
+        x1 = ll_load(h + 1);
+        x2 = ll_load(h + 2);
+      } while (!(ll_ok(x0, ep) && ll_ok(x1, ep) && ll_ok(x2, ep)));
+      const unsigned long long k2 = (x0 & 0xffffffffull) | (x1 << 32);
+      const int64_t i2 = (uint32_t)x2 == 0xffffffffu ? INT64_MAX : (int64_t)(uint32_t)x2;
+      if (k2 > gk || (k2 == gk && i2 < gi)) {
+        gk = k2;
+        gi = i2;
       }
     }
-    block_argmax(bv, bi, sv, si);
-    if (threadIdx.x == 0) {
-      a.cand_v[par * G + blockIdx.x] = bv;
-      a.cand_i[par * G + blockIdx.x] = bi;
-      si[0] = bi;
-    }
-    __syncthreads();
-    const int64_t mybest = si[0];
-    if (mybest != INT64_MAX)
-      for (int j = threadIdx.x; j < ncol; j += blockDim.x)
-        cand_row[((size_t)par * G + blockIdx.x) * kPanelMaxW + j] = tile[j * ldt + (int)(mybest - my_lo)];
-    if (i >= my_lo && i < my_hi)
-      for (int j = threadIdx.x; j < ncol; j += blockDim.x)
-        diag_row[par * kPanelMaxW + j] = tile[j * ldt + (int)(i - my_lo)];
-    grid_sync(a.bar, G, epoch);
-    // ---- phase B: global pivot (same in every CTA), pivot row and old row i
-    reduce_candidates(a, par, i, &s_piv);
-    const int64_t p = s_piv;
-    const unsigned owner = (unsigned)((p - a.kb) / per);
-    for (int j = threadIdx.x; j < ncol; j += blockDim.x) {
-      prow[j] = __ldcg(cand_row + ((size_t)par * G + owner) * kPanelMaxW + j);
-      drow[j] = __ldcg(diag_row + par * kPanelMaxW + j);
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.piv[i] = p;  // piv[i] = v (direct.py:67)
-    __syncthreads();
-    if (p != i) {  // full-row swap restricted to the panel (direct.py:68-70)
-      if (i >= my_lo && i < my_hi)
-        for (int j = threadIdx.x; j < ncol; j += blockDim.x) tile[j * ldt + (int)(i - my_lo)] = prow[j];
-      if (p >= my_lo && p < my_hi)
-        for (int j = threadIdx.x; j < ncol; j += blockDim.x) tile[j * ldt + (int)(p - my_lo)] = drow[j];
-    }
-    __syncthreads();
-    const T aii = prow[c];
-    if (aii == T(0)) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) a.zero_cols[i] = 1;  // direct.py:71-74
-    } else {
-      const T recip = div_rn(T(1), aii);
-      const int u0 = (int)max((int64_t)0, i + 1 - my_lo);
-      const int nu = nr - u0;
-      for (int r = u0 + threadIdx.x; r < nr; r += blockDim.x) tile[c * ldt + r] = mul_rn(recip, tile[c * ldt + r]);
-      __syncthreads();
-      const int w = ncol - c - 1;
-      if (nu > 0)
-        for (int idx = threadIdx.x; idx < w * nu; idx += blockDim.x) {
-          const int j = c + 1 + idx / nu, r = u0 + idx % nu;
-          tile[j * ldt + r] = sub_rn(tile[j * ldt + r], mul_rn(tile[c * ldt + r], prow[j]));
+    const long long t_d = clock64();
+    cta_argmax_key(gk, gi, wk[1], wi[1]);
+    const long long t_e = clock64();
+    const int64_t p = gi == INT64_MAX ? i : gi;
+    const int win = gi == INT64_MAX ? -1 : (int)((gi - a.kb) / per);
+    // ---- the winner's row and row i (LL polls), in column order and rotated by c
+    {
+      const uint64_t* pr = rows + ((size_t)par * G + (win < 0 ? 0 : win)) * RW;
+      const uint64_t* dr = diag + (size_t)par * RW;
+      for (int j = t; j < c + kPanelMaxW + 2; j += nt) {
+        if (j < ncol) {
+          uint64_t pw[VW], dw[VW];
+          while (true) {
+            bool ok = true;
+#pragma unroll
+            for (int qq = 0; qq < VW; ++qq) {
+              pw[qq] = win < 0 ? ((uint64_t)ep << 32) : ll_load(pr + j * VW + qq);
+              dw[qq] = ll_load(dr + j * VW + qq);
+              ok = ok && ll_ok(pw[qq], ep) && ll_ok(dw[qq], ep);
+            }
+            if (ok) break;
+          }
+          const T dv = LLVal<T>::get(dw);
+          const T pv = win < 0 ? dv : LLVal<T>::get(pw);
+          drow[j] = dv;
+          prow[j] = pv;
+          if (j >= c) {
+            drs[j - c] = dv;
+            prs[j - c] = pv;
+          }
+        } else if (j >= c) {
+          drs[j - c] = T(0);
+          prs[j - c] = T(0);
         }
+      }
     }
+    if (blockIdx.x == 0 && t == 0) a.piv[i] = p;  // piv[i] = v (direct.py:67)
     __syncthreads();
+    const long long t_f = clock64();
+    const T aii = prow[c];
+    const bool zero = aii == T(0);
+    if (zero && blockIdx.x == 0 && t == 0) a.zero_cols[i] = 1;  // direct.py:71-74
+    // retired columns j < c of rows i and p: one column per thread
+    if (p != i)
+      for (int j = t; j < c; j += nt) {
+        if (i >= my_lo && i < my_hi) Ls[j * ldt + (int)(i - my_lo)] = prow[j];
+        if (p >= my_lo && p < my_hi) Ls[j * ldt + (int)(p - my_lo)] = drow[j];
+      }
+    // ---- swap (direct.py:68-70, restricted to the panel)
+    if (mine && p != i && (g == i || g == p)) {
+#pragma unroll
+      for (int k = 0; k < PW; ++k) y[k] = g == i ? prs[q * PW + k] : drs[q * PW + k];
+    }
+    // ---- reciprocal scale (the lead thread) and the update of column c + 1 first
+    const bool act = mine && g > i && !zero;
+    T l = T(0);
+    if (lead && act) {
+      l = mul_rn(div_rn(T(1), aii), y[0]);
+      y[0] = l;
+      if (PW > 1) y[1] = sub_rn(y[1], mul_rn(l, prs[1]));
+    }
+    l = __shfl_sync(0xffffffffu, l, lead_lane);
+    if (lead) Ls[c * ldt + r] = y[0];  // retire column c
+    unsigned long long bk = 0ull;
+    int64_t bi = INT64_MAX;
+    if (c + 1 < ncol) {
+      // next column's candidate (rows >= i + 1): column c + 1 is y[1] of the lead (PW > 1)
+      const T nx = PW > 1 ? y[1 % PW] : T(0);
+      if (lead && g > i) {
+        bk = piv_key(fabs((double)nx));
+        bi = g;
+      }
+    }
+    if (PW == 1) {  // TPR == 64 is not used; keep the generic path well-defined
+      bk = 0ull;
+      bi = INT64_MAX;
+    }
+    if (c + 1 < ncol) {
+      cta_argmax_key(bk, bi, wk[0], wi[0]);
+      publish_header(c + 1, bk, bi);  // the exchange of column c + 1 starts here
+    }
+    // ---- rest of the rank-1 update of my slice (direct.py:75-79), then rotate by one
+    if (act) {
+#pragma unroll
+      for (int k = 0; k < PW; ++k) {
+        const int j = q * PW + k;
+        if (j >= 2) y[k] = sub_rn(y[k], mul_rn(l, prs[j]));
+      }
+    }
+    {
+      const T carry = __shfl_down_sync(0xffffffffu, y[0], 1);
+#pragma unroll
+      for (int k = 0; k + 1 < PW; ++k) y[k] = y[k + 1];
+      y[PW - 1] = q == TPR - 1 ? T(0) : carry;
+    }
+    if (c + 1 < ncol) publish_rows(c + 1, bi);
+    if (a.trace && t == 0) {
+      const long long t_g = clock64();
+      unsigned long long* tr = a.trace + (size_t)blockIdx.x * 8;
+      tr[2] += t_d - t_c;  // header poll
+      tr[3] += t_e - t_d;  // argmax of the headers
+      tr[4] += t_f - t_e;  // row poll + barrier
+      tr[5] += t_g - t_f;  // swap, scale, next candidate, update, rotate, publish
+    }
   }
-  for (int idx = threadIdx.x; idx < ncol * nr; idx += blockDim.x) {
-    const int j = idx / nr, r = idx % nr;
-    W[(my_lo + r) + (a.kb + j) * a.ld] = tile[j * ldt + r];
+  __syncthreads();
+  for (int idx = t; idx < ncol * nr; idx += nt) {
+    const int j = idx / nr, rr = idx % nr;
+    W[(my_lo + rr) + (a.kb + j) * a.ld] = Ls[j * ldt + rr];
   }
 }
 
@@ -243,7 +499,7 @@ __global__ void __launch_bounds__(kPanelThreads) lu_panel_global_kernel(T* __res
       a.cand_i[blockIdx.x] = bi;
     }
     grid_sync(a.bar, G, epoch);
-    reduce_candidates(a, 0, i, &s_piv);
+    reduce_candidates(a, 0, i, &s_piv, sv, si);
     const int64_t p = s_piv;
     if (blockIdx.x == 0) {
       if (threadIdx.x == 0) a.piv[i] = p;
@@ -469,14 +725,20 @@ __global__ void __launch_bounds__(256)
   const int np = *npairs;
   const int64_t c0 = c_lo + (int64_t)blockIdx.x * cols;
   const int nc = (int)min((int64_t)cols, c_hi - c0);
-  for (int idx = threadIdx.x; idx < np * nc; idx += blockDim.x) {
-    const int q = idx / np, t = idx % np;
-    buf[q * np + t] = W[src[t] + (c0 + q) * ld];
+  // thread <-> pair (rows kb..bf-1 of the plan are contiguous: coalesced), loop over columns
+  for (int t = threadIdx.x; t < np; t += blockDim.x) {
+    const int64_t s_ = src[t];
+    T v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = q < nc ? W[s_ + (c0 + q) * ld] : T(0);  // 8 loads in flight
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < nc) buf[q * np + t] = v[q];
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < np * nc; idx += blockDim.x) {
-    const int q = idx / np, t = idx % np;
-    W[dst[t] + (c0 + q) * ld] = buf[q * np + t];
+  for (int t = threadIdx.x; t < np; t += blockDim.x) {
+    const int64_t d_ = dst[t];
+    for (int q = 0; q < nc; ++q) W[d_ + (c0 + q) * ld] = buf[q * np + t];
   }
 }
 
@@ -504,7 +766,7 @@ int laswp_apply(ds_ctx* ctx, T* W, int64_t ld, int64_t c_lo, int64_t c_hi, const
   if (c_hi <= c_lo) return DS_OK;
   // np <= 2*cnt; size the column group so the staging buffer stays <= 192 KB
   const int64_t npmax = 2 * sp.cnt;
-  const int cols = (int)std::max<int64_t>(1, std::min<int64_t>(8, (192 * 1024) / (npmax * (int64_t)sizeof(T))));
+  const int cols = (int)std::max<int64_t>(1, std::min<int64_t>(8, (192 * 1024) / (npmax * (int64_t)sizeof(T))));  // <= 8 (kernel unroll)
   const size_t smem = (size_t)cols * npmax * sizeof(T);
   static size_t attr[2] = {0, 0};
   size_t& done = attr[sizeof(T) == 8 ? 1 : 0];
@@ -519,6 +781,14 @@ int laswp_apply(ds_ctx* ctx, T* W, int64_t ld, int64_t c_lo, int64_t c_hi, const
   count_launch(ctx);
   DS_CHECK_LAUNCH();
   return DS_OK;
+}
+
+// bytes of the per-launch panel scratch carved in panel_launch (with 256-B alignment slack)
+template <typename T>
+size_t panel_scratch_bytes(int64_t b) {
+  return 256 + 2 * 1024 * 16 + sizeof(T) * (2 * 1024 * kPanelMaxW + 2 * kPanelMaxW) +
+         2 * sizeof(T) * (size_t)std::max<int64_t>(b, 1) + sizeof(uint64_t) * 2 * 1024 * kHdrWords +
+         sizeof(uint64_t) * 2 * 1024 * kPanelMaxW * 2 + sizeof(uint64_t) * 2 * kPanelMaxW * 2 + 16 * 256;
 }
 
 template <typename T>
@@ -540,7 +810,11 @@ int panel_launch(ds_ctx* ctx, T* W, int64_t n, int64_t ld, int64_t kb, int64_t b
   a.diag_row = cv.take<T>(sizeof(T) * 2 * kPanelMaxW);
   a.rowP = cv.take<T>(sizeof(T) * ncol);
   a.rowI = cv.take<T>(sizeof(T) * ncol);
-  DS_CUDA(cudaMemsetAsync(a.bar, 0, 256, ctx->stream));
+  a.ll_hdr = cv.take<uint64_t>(sizeof(uint64_t) * 2 * 1024 * kHdrWords);
+  a.ll_row = cv.take<uint64_t>(sizeof(uint64_t) * 2 * 1024 * kPanelMaxW * 2);
+  a.ll_diag = cv.take<uint64_t>(sizeof(uint64_t) * 2 * kPanelMaxW * 2);
+  a.seq = ++ctx->panel_seq;
+  a.trace = nullptr;
   const size_t smem_cap = std::min<size_t>(ctx->smem_optin, 220 * 1024) - 2048;
   // shared-memory path: rows split over <= num_sms CTAs, >= 16 rows each
   if (ncol <= kPanelMaxW) {
@@ -549,20 +823,59 @@ int panel_launch(ds_ctx* ctx, T* W, int64_t n, int64_t ld, int64_t kb, int64_t b
     g = ceil_div(rows, per);
     const int ldt = (int)(per | 1);
     const size_t smem = (size_t)ncol * ldt * sizeof(T);
-    if (smem <= smem_cap) {
+    const int tpr = per <= kPanelRegThreads / 4 ? 4 : 2;
+    if (smem <= smem_cap && per * tpr <= kPanelRegThreads) {
       a.per = (int)per;
       a.ldt = ldt;
-      static size_t attr_set[2] = {0, 0};
-      size_t& done = attr_set[sizeof(T) == 8 ? 1 : 0];
-      if (smem > done) {
-        DS_CUDA(cudaFuncSetAttribute(lu_panel_smem_kernel<T>,
+      static bool attr_set[2] = {false, false};
+      if (!attr_set[sizeof(T) == 8 ? 1 : 0]) {
+        DS_CUDA(cudaFuncSetAttribute(lu_panel_smem_kernel<T, 2>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
-        done = smem_cap;
+        DS_CUDA(cudaFuncSetAttribute(lu_panel_smem_kernel<T, 4>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
+        attr_set[sizeof(T) == 8 ? 1 : 0] = true;
+      }
+      const int nthr = (int)std::max<int64_t>(ceil_div(per * tpr, 32) * 32, ceil_div(g, 32) * 32);
+      void* kfn = tpr == 4 ? (void*)lu_panel_smem_kernel<T, 4> : (void*)lu_panel_smem_kernel<T, 2>;
+      const char* tr = getenv("DENSOLVE_PANEL_TRACE");  // debug: per-phase timestamps of one panel
+      const bool tracing = tr && atoll(tr) == kb;
+      if (tracing) {
+        DS_CUDA(cudaMalloc((void**)&a.trace, sizeof(unsigned long long) * g * 8));
+        DS_CUDA(cudaMemsetAsync(a.trace, 0, sizeof(unsigned long long) * g * 8, ctx->stream));
       }
       void* args[] = {(void*)&W, (void*)&a};
-      DS_CUDA(cudaLaunchCooperativeKernel((void*)lu_panel_smem_kernel<T>, dim3((unsigned)g),
-                                          dim3(kPanelThreads), args, smem, ctx->stream));
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (tracing) {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, ctx->stream);
+      }
+      // a plain launch: grid <= #SMs at one CTA per SM, so every CTA becomes resident once
+      // any concurrent (look-ahead) GEMM CTAs retire; a cooperative launch costs ~10x
+      // more host time per panel
+      DS_CUDA(cudaLaunchKernel(kfn, dim3((unsigned)g), dim3((unsigned)nthr), args, smem, ctx->stream));
       count_launch(ctx);
+      if (tracing) {
+        cudaEventRecord(e1, ctx->stream);
+        std::vector<unsigned long long> h((size_t)g * 8);
+        DS_CUDA(cudaMemcpyAsync(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        DS_CUDA(cudaStreamSynchronize(ctx->stream));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaFree(a.trace);
+        a.trace = nullptr;
+        double mean[6] = {}, mx[6] = {};
+        for (int64_t b = 0; b < g; ++b)
+          for (int k = 0; k < 6; ++k) {
+            mean[k] += (double)h[b * 8 + k] / g / ncol;
+            mx[k] = std::max(mx[k], (double)h[b * 8 + k] / ncol);
+          }
+        fprintf(stderr, "[panel trace] kb=%lld rows=%lld G=%lld per=%lld: %.2f us/column (events); cycles/column "
+                "mean(max): argmax0 %.0f(%.0f) publish %.0f(%.0f) hdrpoll %.0f(%.0f) argmax1 %.0f(%.0f) "
+                "rowpoll+sync %.0f(%.0f) update %.0f(%.0f)\n", (long long)kb, (long long)rows, (long long)g,
+                (long long)per, 1e3 * ms / ncol, mean[0], mx[0], mean[1], mx[1], mean[2], mx[2], mean[3], mx[3],
+                mean[4], mx[4], mean[5], mx[5]);
+      }
       return DS_OK;
     }
   }
@@ -572,6 +885,7 @@ int panel_launch(ds_ctx* ctx, T* W, int64_t n, int64_t ld, int64_t kb, int64_t b
     DS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m, lu_panel_global_kernel<T>, kPanelThreads, 0));
     if (m < 1) m = 1;
   }
+  DS_CUDA(cudaMemsetAsync(a.bar, 0, 256, ctx->stream));
   int64_t g = std::min<int64_t>(ceil_div(rows, 64), (int64_t)ctx->num_sms);
   g = std::max<int64_t>(1, g);
   int64_t per = ceil_div(rows, g);
@@ -614,8 +928,7 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
                    int8_t* d_zero) {
   void* ws = nullptr;
   const int64_t NB = outer_block(b, w);
-  const size_t scratch_bytes = 256 + 2 * 1024 * 16 + sizeof(T) * (2 * 1024 * kPanelMaxW + 2 * kPanelMaxW) +
-                               2 * sizeof(T) * (size_t)std::max<int64_t>(b, 1) + 16 * 256;
+  const size_t scratch_bytes = panel_scratch_bytes<T>(b);
   DS_TRY(ctx_workspace(ctx, scratch_bytes + 2 * sizeof(int64_t) * 8 * (size_t)NB + 4096, &ws));
   Carver cvs{(char*)ws};
   char* scratch = cvs.take<char>(scratch_bytes);
@@ -679,7 +992,27 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
   };
 
   DS_TRY(factor_outer(0, std::min<int64_t>(NB, w)));
+  // debug timeline (DENSOLVE_LU_TIMELINE=1): an event on the main stream per outer panel
+  // plus host enqueue times; printed at the end
+  const bool timeline = getenv("DENSOLVE_LU_TIMELINE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  std::vector<double> thost;
+  auto host_us = [] {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e6 + ts.tv_nsec * 1e-3;
+  };
+  auto mark = [&] {
+    if (!timeline) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, ctx->stream);
+    tev.push_back(e);
+    thost.push_back(host_us());
+  };
+  mark();
   for (int64_t kb = 0; kb < w; kb += NB) {
+    mark();
     const int64_t bf = std::min<int64_t>(kb + NB, w);
     // swaps of the whole outer panel on the columns outside it.  The L columns
     // [0, kb) are never read again by the factorization, so with look-ahead
@@ -721,6 +1054,27 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
       DS_TRY(outer_update(kb, bf, bf2, w));
       DS_TRY(factor_outer(bf, bf2));
     }
+  }
+  mark();
+  if (timeline && tev.size() > 1) {
+    cudaEventSynchronize(tev.back());
+    const double hend = host_us();
+    std::vector<std::pair<float, int>> d;
+    float tot = 0;
+    for (size_t k = 1; k < tev.size(); ++k) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, tev[k - 1], tev[k]);
+      d.push_back({ms, (int)k - 1});
+      tot += ms;
+    }
+    std::sort(d.begin(), d.end(), [](auto& x, auto& y) { return x.first > y.first; });
+    fprintf(stderr, "[lu timeline] n=%lld steps=%zu device %.2f ms, host enqueue %.2f ms, host total %.2f ms; slowest:",
+            (long long)w, d.size(), tot, thost.back() - thost.front(), hend - thost.front());
+    for (size_t k = 0; k < std::min<size_t>(6, d.size()); ++k)
+      fprintf(stderr, " #%d %.2f ms (enq at %.2f ms)", d[k].second, d[k].first,
+              (thost[d[k].second] - thost.front()) / 1e3);
+    fprintf(stderr, "\n");
+    for (auto e : tev) cudaEventDestroy(e);
   }
   if (lookahead) {
     DS_CUDA(cudaEventRecord(ctx->ev_c, ctx->aux));

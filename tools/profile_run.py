@@ -44,6 +44,14 @@ elif what == "gemm":
     for _ in range(3):
         be.gemm(-1.0, dA, dB, 1.0, dC, out=dC)
     ctx.synchronize()
+elif what == "trsm":
+    m = int(sys.argv[2]) if len(sys.argv) > 2 else 16384
+    L = np.asfortranarray(np.tril(rng.uniform(-1, 1, (64, 64))))
+    B = np.asfortranarray(rng.uniform(-1, 1, (64, m)))
+    dL, dB = be.stage_in(L, B)
+    for _ in range(3):
+        be.trsm_lower_unit(dL, dB)
+    ctx.synchronize()
 elif what == "gmres":
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
     A, b, _ = generate_problem(ProblemSpec("general_nonsymmetric", n, 0))
