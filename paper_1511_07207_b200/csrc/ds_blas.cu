@@ -567,12 +567,14 @@ __global__ void finish_max2_kernel(const double* red, int nblk, double* out) {
 
 // ============================================================================
 // GEMM — FP64 on the DMMA tensor pipe.  out = beta*C + alpha*(A B).
-//   CTA tile 128x64, 4 warps (2x2) of 64x32, BK=16 k-slab, 3-stage cp.async
+//   CTA tile 128x64, 8 warps (4x2) of 32x32, BK=16 k-slab, 3-stage cp.async
 //   pipeline, mma.sync.m8n8k4.row.col.f64 (native DMMA.8x8x4; the only FP64
 //   tensor-core instruction on sm_100a — tcgen05 has no kind::f64).
 // ============================================================================
 namespace gemm64 {
-constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3, THREADS = 128;
+constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3;
+// warp tile WR x 32: 8 warps of 32 x 32 (4 warps per SM sub-partition at 2 CTAs/SM)
+constexpr int WR = 32, MI = WR / 8, WARPS_M = BM / WR, THREADS = WARPS_M * (BN / 32) * 32;
 constexpr int LDA_S = BM + 4;  // smem row (one k) of the A slab, +4 doubles: conflict-free frags
 constexpr int LDB_S = BK + 4;  // smem row (one n) of the B slab
 constexpr int A_STAGE = BK * LDA_S;
@@ -665,18 +667,18 @@ __global__ void __launch_bounds__(gemm64::THREADS, 2)
   double* As = reinterpret_cast<double*>(smem_raw);
   double* Bs = As + STAGES * A_STAGE;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wm = warp & 1, wn = warp >> 1;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
   const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
   const int g = lane >> 2, t = lane & 3;
 
   // MODE 1 (out = C - A B, the LU update): the accumulators start from C (loaded
   // before the main loop, so its latency hides under the cp.async prologue) and
   // the A fragments are negated, making the epilogue store-only.
-  double acc[8][4][2];
+  double acc[MI][4][2];
   if (MODE == 1) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int64_t r = m0 + wm * 64 + i * 8 + g;
+    for (int i = 0; i < MI; ++i) {
+      const int64_t r = m0 + wm * WR + i * 8 + g;
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -687,7 +689,7 @@ __global__ void __launch_bounds__(gemm64::THREADS, 2)
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   }
@@ -711,17 +713,17 @@ __global__ void __launch_bounds__(gemm64::THREADS, 2)
     }
     cp_async_commit();
     const int s = (int)(kt % STAGES);
-    const double* as = As + s * A_STAGE + wm * 64 + g;
+    const double* as = As + s * A_STAGE + wm * WR + g;
     const double* bs = Bs + s * B_STAGE + (wn * 32 + g) * LDB_S + t;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
-      double a[8], b[4];
+      double a[MI], b[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a[i] = MODE == 1 ? -as[(kk + t) * LDA_S + i * 8] : as[(kk + t) * LDA_S + i * 8];
+      for (int i = 0; i < MI; ++i) a[i] = MODE == 1 ? -as[(kk + t) * LDA_S + i * 8] : as[(kk + t) * LDA_S + i * 8];
 #pragma unroll
       for (int j = 0; j < 4; ++j) b[j] = bs[j * 8 * LDB_S + kk];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
@@ -731,8 +733,8 @@ __global__ void __launch_bounds__(gemm64::THREADS, 2)
   // with NumPy's rounding (backends.py:244); C is read in one batch per row group
   // before any store so the loads overlap.
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t r = m0 + wm * 64 + i * 8 + g;
+  for (int i = 0; i < MI; ++i) {
+    const int64_t r = m0 + wm * WR + i * 8 + g;
     if (r >= m) continue;
     double cv[4][2];
     if (MODE == 0) {

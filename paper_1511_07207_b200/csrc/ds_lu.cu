@@ -818,7 +818,12 @@ int panel_launch(ds_ctx* ctx, T* W, int64_t n, int64_t ld, int64_t kb, int64_t b
   const size_t smem_cap = std::min<size_t>(ctx->smem_optin, 220 * 1024) - 2048;
   // shared-memory path: rows split over <= num_sms CTAs, >= 16 rows each
   if (ncol <= kPanelMaxW) {
-    int64_t g = std::min<int64_t>((int64_t)ctx->num_sms, ceil_div(rows, 16));
+    // rows per CTA: at least `target` (fewer CTAs leave SMs to the concurrent look-ahead GEMM)
+    static int64_t target = [] {
+      const char* e = getenv("DENSOLVE_PANEL_ROWS");
+      return e ? std::max<int64_t>(16, atoll(e)) : (int64_t)256;
+    }();
+    int64_t g = std::min<int64_t>((int64_t)ctx->num_sms, ceil_div(rows, target));
     int64_t per = ceil_div(rows, g);
     g = ceil_div(rows, per);
     const int ldt = (int)(per | 1);
@@ -1035,10 +1040,12 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
     } else {
       DS_TRY(laswp_apply<T>(ctx, W, ld, 0, kb, op));
     }
-    DS_TRY(laswp_apply<T>(ctx, W, ld, bf, w, op));
     if (bf >= w) break;
     const int64_t bf2 = std::min<int64_t>(bf + NB, w);
-    DS_TRY(outer_update(kb, bf, bf, bf2));  // look-ahead columns first
+    // the look-ahead columns [bf, bf2) get their swaps and update first: that is the
+    // only work between this panel and the next panel's factorization
+    DS_TRY(laswp_apply<T>(ctx, W, ld, bf, bf2, op));
+    DS_TRY(outer_update(kb, bf, bf, bf2));
     if (lookahead) {
       DS_CUDA(cudaEventRecord(ctx->ev_a, ctx->stream));
       DS_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_a, 0));
@@ -1048,9 +1055,12 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
       ctx->stream = main;
       DS_TRY(rc);
       DS_CUDA(cudaEventRecord(ctx->ev_b, ctx->side));
+      // the rest of the trailing matrix (disjoint columns) overlaps the next panel
+      DS_TRY(laswp_apply<T>(ctx, W, ld, bf2, w, op));
       DS_TRY(outer_update(kb, bf, bf2, w));
       DS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_b, 0));
     } else {
+      DS_TRY(laswp_apply<T>(ctx, W, ld, bf2, w, op));
       DS_TRY(outer_update(kb, bf, bf2, w));
       DS_TRY(factor_outer(bf, bf2));
     }
