@@ -910,8 +910,12 @@ int panel_launch(ds_ctx* ctx, T* W, int64_t n, int64_t ld, int64_t kb, int64_t b
 // outer panel with a K = NB GEMM.  Exact-arithmetic identical to the reference
 // (same pivots), different rounding grouping in the trailing update.
 static int64_t outer_block(int64_t b, int64_t n) {
-  if (b >= 256 || b >= n) return std::min<int64_t>(b, n);
-  return std::min<int64_t>(n, b * std::max<int64_t>(1, 256 / b));
+  static const int64_t nb_target = [] {
+    const char* e = getenv("DENSOLVE_LU_NB");  // tuning knob; default 512
+    return e ? std::max<int64_t>(64, atoll(e)) : (int64_t)512;
+  }();
+  if (b >= nb_target || b >= n) return std::min<int64_t>(b, n);
+  return std::min<int64_t>(n, b * std::max<int64_t>(1, nb_target / b));
 }
 
 // Factor the m x w (m >= w) column-major panel W in place: rows [0, m), columns
