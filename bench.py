@@ -7,8 +7,9 @@ tolerance 1e-300 and max_iterations=ITERS (the reference's own fixed-iteration
 idiom, tests/test_krylov.py:188-191), i.e. symmetry gate + setup + ITERS
 iterations.  ``e2e`` is the same metric through the public API with pinned
 HOST buffers (A, b, x0 uploaded and x downloaded inside every step).
-``components`` adds GMRES(30) n=4096 fp64 (C2, one full cycle per step) and
-blocked LU (b=64) fp64 GFLOP/s.
+``components`` adds GMRES(30) n=4096 fp64 (C2) and GMRES(50) n=65536 fp32 (C5),
+one full cycle per step; blocked LU (b=64) fp64 GFLOP/s at n=16384 (C3) and
+n=32768 (C5 per-GPU size); BiCGSTAB and Cholesky on the C4 matrix.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
@@ -297,14 +298,23 @@ def run_b200(args):
            "h2d_bytes_per_step": int(A_h.nbytes + b_h.nbytes + x0_h.nbytes),
            "d2h_bytes_per_step": int(x_h.nbytes + 8 * (iters + 1)),
            "ms_per_step": e2e_ms / args.steps}
-    del dA, A_h, A_h_t
-    torch.cuda.empty_cache()
+    del A_h, A_h_t
 
     components = {}
     if not args.only_cg:
-        components["gmres"] = bench_gmres(args, torch, stream, be, generate_problem, ProblemSpec,
-                                          gmres_solve, SolverConfig)
-        components["lu"] = bench_lu(args, torch, dev, stream, be, lu_factor_blocked)
+        from paper_1511_07207_b200 import bicgstab_solve, cholesky_factor
+        components["bicgstab"] = bench_bicgstab(args, torch, stream, be, dA, db, dx0, n, bicgstab_solve,
+                                                SolverConfig, hbm_peak)
+        components["cholesky"] = bench_cholesky(args, torch, stream, be, dA, n, cholesky_factor)
+    del dA
+    torch.cuda.empty_cache()
+    if not args.only_cg:
+        components["gmres_c2"] = bench_gmres(args, torch, stream, be, generate_problem, ProblemSpec,
+                                             gmres_solve, SolverConfig)
+        components["gmres_c5"] = bench_gmres_c5(args, torch, dev, stream, be, gmres_solve, SolverConfig,
+                                                hbm_peak)
+        components["lu_c3"] = bench_lu(args, torch, dev, stream, be, lu_factor_blocked, args.lu_n)
+        components["lu_c5"] = bench_lu(args, torch, dev, stream, be, lu_factor_blocked, args.lu_n5)
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -323,31 +333,100 @@ def run_b200(args):
     print(json.dumps(line), flush=True)
 
 
+def _timed(torch, stream, fn, reps):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    out = None
+    for _ in range(reps):
+        out = fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps, out
+
+
 def bench_gmres(args, torch, stream, be, generate_problem, ProblemSpec, gmres_solve, SolverConfig):
+    """C2: GMRES(30) general_nonsymmetric n=4096 fp64 (the harness generator, host-built)."""
     n, m = 4096, 30
     A, b, _ = generate_problem(ProblemSpec(kind="general_nonsymmetric", n=n, seed=0))
     dA, db, dx0 = be.stage_in(A, b, np.zeros_like(b))
     cfg = SolverConfig(tolerance=1e-300, restart_m=m, max_iterations=m)
-    for _ in range(3):
-        gmres_solve(dA, db, dx0, cfg, be)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 10
-    e0.record(stream)
-    for _ in range(reps):
-        x, rep = gmres_solve(dA, db, dx0, cfg, be)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
+    ms, (x, rep) = _timed(torch, stream, lambda: gmres_solve(dA, db, dx0, cfg, be), 10)
     return {"workload": f"C2: GMRES({m}) general_nonsymmetric n={n} fp64, one full cycle per step "
                         "(residual + 30 Arnoldi steps + update + true residual)",
             "value": round(rep.iterations / (ms / 1e3), 1), "unit": "inner iters/s", "ms_per_step": round(ms, 4)}
 
 
-def bench_lu(args, torch, dev, stream, be, lu_factor_blocked):
+def nonsym_fast_device(n, seed, torch, device, dtype):
+    """Synthetic dense diagonally dominant nonsymmetric A = R + 0.6 n I, R ~ U[-1,1] (seeded, on
+    the GPU, in the target dtype; the harness recipe needs ~130 GB of fp64 temporaries at n=65536)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    A = torch.empty((n, n), dtype=dtype, device=device)
+    for c0 in range(0, n, 4096):  # column blocks keep the fp32 temporaries small
+        blk = torch.rand((min(4096, n - c0), n), dtype=dtype, device=device, generator=g)
+        A[c0:c0 + blk.shape[0]] = blk.mul_(2.0).sub_(1.0)
+    A.diagonal().add_(0.6 * n)
+    xt = torch.rand(n, dtype=dtype, device=device, generator=g).mul_(2.0).sub_(1.0)
+    return A, A.t() @ xt  # A is stored transposed (torch row-major) -> column-major A^T; b = A^T x
+
+
+def bench_gmres_c5(args, torch, dev, stream, be, gmres_solve, SolverConfig, hbm_peak):
+    """C5: GMRES(50) n=65536 fp32, one full cycle per step (HBM-capacity sizing, 1 GPU)."""
     from paper_1511_07207_b200.device import DeviceArray
 
-    n = args.lu_n
+    n, m = args.gmres_n, 50
+    ctx = be.ctx
+    At, bt = nonsym_fast_device(n, 3, torch, dev, torch.float32)
+    dA = DeviceArray(ctx, (n, n), np.float32)
+    ctx.lib.ds_memcpy_d2d(ctx.handle, dA.ptr, At.data_ptr(), 4 * n * n)
+    db = DeviceArray(ctx, (n,), np.float32)
+    ctx.lib.ds_memcpy_d2d(ctx.handle, db.ptr, bt.data_ptr(), 4 * n)
+    dx0 = DeviceArray(ctx, (n,), np.float32)
+    ctx.lib.ds_memset(ctx.handle, dx0.ptr, 0, 4 * n)
+    del At, bt
+    torch.cuda.synchronize()
+    cfg = SolverConfig(tolerance=1e-300, restart_m=m, max_iterations=m)
+    ms, (x, rep) = _timed(torch, stream, lambda: gmres_solve(dA, db, dx0, cfg, be), 3)
+    # algorithmic bytes of one cycle: (m + 2) passes over A (m Arnoldi GEMVs + residual + true
+    # residual) + per step k the basis traffic (2k + 7) n + the x update (m + 2) n
+    s = 4.0
+    byts = s * ((m + 2) * n * n + sum((2 * k + 7) * n for k in range(m)) + (m + 2) * n)
+    gbs = byts / (ms / 1e3) / 1e9
+    del dA
+    torch.cuda.empty_cache()
+    return {"workload": f"C5: GMRES({m}) dense diagonally dominant nonsymmetric n={n} fp32 (device-generated), "
+                        "one full cycle per step", "value": round(rep.iterations / (ms / 1e3), 1),
+            "unit": "inner iters/s", "ms_per_step": round(ms, 3), "GBps": round(gbs, 1),
+            "frac_of_hbm_peak": round(gbs / hbm_peak, 4)}
+
+
+def bench_bicgstab(args, torch, stream, be, dA, db, dx0, n, bicgstab_solve, SolverConfig, hbm_peak):
+    """BiCGSTAB on the C4 matrix, fixed 50 iterations per step."""
+    iters = 50
+    cfg = SolverConfig(tolerance=1e-300, max_iterations=iters)
+    ms, (x, rep) = _timed(torch, stream, lambda: bicgstab_solve(dA, db, dx0, cfg, be), 2)
+    its = rep.iterations
+    gbs = 8.0 * (2 * its + 1) * (n * n) / (ms / 1e3) / 1e9
+    return {"workload": f"BiCGSTAB dense SPD n={n} fp64 (C4 matrix), fixed {iters} iterations per step",
+            "value": round(its / (ms / 1e3), 2), "unit": "iters/s", "ms_per_step": round(ms, 3),
+            "iterations": its, "breakdown": rep.breakdown, "GBps_A_stream": round(gbs, 1),
+            "frac_of_hbm_peak": round(gbs / hbm_peak, 4)}
+
+
+def bench_cholesky(args, torch, stream, be, dA, n, cholesky_factor):
+    """Cholesky of the C4 SPD matrix, b=64, device-resident."""
+    ms, _ = _timed(torch, stream, lambda: cholesky_factor(dA, 64, be), 1)
+    tf = n ** 3 / 3.0 / (ms / 1e3) / 1e12
+    return {"workload": f"blocked Cholesky b=64, dense SPD n={n} fp64 (C4 matrix), device-resident",
+            "value": round(tf * 1e3, 1), "unit": "GFLOP/s", "ms": round(ms, 2),
+            "fp64_peak_tflops": FP64_PEAK_TFLOPS, "frac_of_fp64_peak": round(tf / FP64_PEAK_TFLOPS, 4)}
+
+
+def bench_lu(args, torch, dev, stream, be, lu_factor_blocked, n):
+    from paper_1511_07207_b200.device import DeviceArray
+
     ctx = be.ctx
     g = torch.Generator(device=dev)
     g.manual_seed(1)
@@ -358,16 +437,13 @@ def bench_lu(args, torch, dev, stream, be, lu_factor_blocked):
     torch.cuda.synchronize()
     f = lu_factor_blocked(dA, 64, be)  # warm-up
     del f
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    f = lu_factor_blocked(dA, 64, be)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+    ms, f = _timed(torch, stream, lambda: lu_factor_blocked(dA, 64, be), 1)
+    del f, dA
+    torch.cuda.empty_cache()
     flops = 2.0 * n ** 3 / 3.0
     tf = flops / (ms / 1e3) / 1e12
-    return {"workload": f"blocked LU b=64, uniform U[-1,1] n={n} fp64 (pivoting family), device-resident",
+    return {"workload": f"blocked LU b=64, uniform U[-1,1] n={n} fp64 (pivoting family), device-resident "
+                        "(includes the device copy of A, direct.py:61)",
             "value": round(tf * 1e3, 1), "unit": "GFLOP/s", "ms": round(ms, 2),
             "fp64_peak_tflops": FP64_PEAK_TFLOPS, "frac_of_fp64_peak": round(tf / FP64_PEAK_TFLOPS, 4)}
 
@@ -381,6 +457,8 @@ def main():
     ap.add_argument("--n", type=int, default=32768)
     ap.add_argument("--iters", type=int, default=100)
     ap.add_argument("--lu-n", type=int, default=16384)
+    ap.add_argument("--lu-n5", type=int, default=32768)
+    ap.add_argument("--gmres-n", type=int, default=65536)
     ap.add_argument("--only-cg", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
