@@ -46,6 +46,8 @@ extern "C" {
 #define DS_EINVAL 6     /* ValueError (bad config / argument) */
 #define DS_ECUDA 7      /* RuntimeError: CUDA failure */
 #define DS_ENOMEM 8     /* MemoryError: device allocation failed */
+#define DS_EMM 9        /* MatrixMarketError    harness.py:130-135 (ds_mm_read) */
+#define DS_ENOFILE 10   /* FileNotFoundError (ds_mm_read) */
 
 /* ---- dtypes (core.py:14 SUPPORTED_DTYPES) ------------------------------ */
 #define DS_F32 0
@@ -178,6 +180,18 @@ int ds_lu_factor(ds_ctx* ctx, int dtype, int64_t n, void* d_A, int64_t lda, int6
  * factor/solve pair stays on the device (used by the multi-GPU path). */
 int ds_lu_factor_dev(ds_ctx* ctx, int dtype, int64_t n, void* d_A, int64_t lda, int64_t nb,
                      int64_t* d_piv, int32_t* h_singular);
+
+/* ---- input path: Matrix Market ingestion (host side) ------------------ */
+/* Replaces harness.read_matrix_market (harness.py:138-220).  Parses `path`
+ * into the caller's column-major double buffer `h_out` (rows x cols, ld =
+ * rows).  With h_out == NULL or cap < rows*cols only the header and size line
+ * are read and *rows / *cols returned (size query).  DS_EMM: malformed input,
+ * *err_line = the 1-based offending line, message via ds_mm_last_error()
+ * ("line N: ...", the reference's MatrixMarketError text); DS_ENOFILE: the
+ * file does not exist. */
+int ds_mm_read(const char* path, double* h_out, int64_t cap, int64_t* rows, int64_t* cols,
+               int64_t* err_line);
+const char* ds_mm_last_error(void);
 
 /* Blocked Cholesky in place on d_A: replaces direct.cholesky_factor
  * (direct.py:87-120).  On return the lower triangle holds L and the strict

@@ -23,7 +23,8 @@ from . import core
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdensolve_b200.so")
 
-DS_OK, DS_EDIM, DS_EPREC, DS_EDEGRHS, DS_ESINGULAR, DS_ENOTSPD, DS_EINVAL, DS_ECUDA, DS_ENOMEM = range(9)
+(DS_OK, DS_EDIM, DS_EPREC, DS_EDEGRHS, DS_ESINGULAR, DS_ENOTSPD, DS_EINVAL, DS_ECUDA, DS_ENOMEM, DS_EMM,
+ DS_ENOFILE) = range(11)
 DS_F32, DS_F64 = 0, 1
 DS_ORTH_MODIFIED, DS_ORTH_CLASSICAL = 0, 1
 DS_BREAKDOWN_NONE, DS_BREAKDOWN_HAPPY, DS_BREAKDOWN_RHO, DS_BREAKDOWN_OMEGA = 0, 1, 2, 3
@@ -95,6 +96,8 @@ _SIGNATURES = {
                              c_void_p, POINTER(c_int32)]),
     "ds_lu_factor_dev": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_int64,
                                  c_void_p, POINTER(c_int32)]),
+    "ds_mm_read": (c_int, [c_char_p, c_void_p, c_int64, POINTER(c_int64), POINTER(c_int64), POINTER(c_int64)]),
+    "ds_mm_last_error": (c_char_p, []),
     "ds_cholesky_factor": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_int64, POINTER(c_int64)]),
     "ds_cholesky_solve": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
                                   POINTER(c_int64)]),
