@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -378,6 +380,288 @@ __global__ void __launch_bounds__(kT)
   }
 }
 
+// ============================================================================
+// Fused Arnoldi step for small / medium n (latency-bound sizes such as C2, n=4096):
+// ONE kernel per inner step instead of ~7 launches.  Each CTA owns a contiguous
+// block of rows: w = A v_k for its rows (row-split GEMV: no cross-CTA reduction),
+// then every CGS pass is a local partial multi-dot, one grid-wide LL exchange of
+// the (k+1)-vectors of partials (32-bit data + epoch flag words, summed in fixed
+// CTA order by every CTA => identical h everywhere) and a local update; the norm
+// is one more exchange of (scale, ssq) records.  CTA 0 records H / Hraw and runs
+// the Givens / estimate / stop logic of gm_step_finish_kernel.
+// ============================================================================
+constexpr int kArnThreads = 512;
+constexpr int kArnMaxRows = 128;  // rows per CTA (n <= 148 * 128)
+
+struct ArnArgs {
+  int64_t n, lda, ldv, ldh, total_before, cap;
+  int k, passes, per;
+  unsigned seq;
+  double tol;
+  uint64_t* ll;  // [2][grid][64 * 2] exchange words
+  double* est;
+  GmDev* st;
+  unsigned long long* trace;  // optional per-CTA phase cycle accumulators (DENSOLVE_GMRES_TRACE)
+};
+
+__device__ __forceinline__ void arn_store(uint64_t* p, uint32_t data, uint32_t flag) {
+  const uint64_t w = ((uint64_t)flag << 32) | data;
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;\n" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ uint64_t arn_load(const uint64_t* p) {
+  uint64_t w;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+__device__ __forceinline__ void arn_put(uint64_t* p, double v, uint32_t f) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  arn_store(p, (uint32_t)b, f);
+  arn_store(p + 1, (uint32_t)(b >> 32), f);
+}
+// poll one double published with flag f
+__device__ __forceinline__ double arn_get(const uint64_t* p, uint32_t f) {
+  uint64_t a, b;
+  while (true) {
+    a = arn_load(p);
+    b = arn_load(p + 1);
+    if ((uint32_t)(a >> 32) == f && (uint32_t)(b >> 32) == f) break;
+  }
+  return __longlong_as_double((long long)((a & 0xffffffffull) | (b << 32)));
+}
+
+template <typename T, int RCH /* 32-row chunks per CTA: 1, 2 or 4 */>
+__global__ void __launch_bounds__(kArnThreads)
+    arnoldi_step_kernel(const T* __restrict__ A, T* V, T* H, T* Hraw, T* g, T* cs, T* sn, ArnArgs a,
+                        Gate gate) {
+  if (gated(gate)) return;
+  extern __shared__ __align__(16) unsigned char arn_smem[];
+  T* Vb = reinterpret_cast<T*>(arn_smem);  // [kc][nr]: my rows of V[:, 0..k] (staged once)
+  __shared__ double wv[kArnMaxRows];      // w for my rows (fp64 copy of the T values)
+  __shared__ double red[kArnThreads / 32][kArnMaxRows];
+  __shared__ double hs[64], hsave[64], sm[64];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kArnThreads / 32;
+  const unsigned G = gridDim.x;
+  const int64_t r0 = (int64_t)blockIdx.x * a.per;
+  const int nr = (int)max((int64_t)0, min((int64_t)a.per, a.n - r0));
+  const int k = a.k, kc = k + 1;
+  const T* vk = V + (int64_t)k * a.ldv;
+  uint32_t round = 0;
+  long long tt[8];
+  int nt_ = 0;
+  tt[nt_++] = clock64();
+
+  // ---- w = A v_k for my rows: warps split the columns, lanes the rows (RCH chunks
+  // of 32); U columns per warp in flight per step (RCH * U = 16 loads per thread)
+  {
+    constexpr int U = 16 / RCH;
+    double acc[RCH];
+#pragma unroll
+    for (int q = 0; q < RCH; ++q) acc[q] = 0.0;
+    int64_t c = warp;
+    for (; c + (U - 1) * nw < a.n; c += U * nw) {
+      T av[U][RCH];
+      double xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        xv[u] = (double)__ldg(vk + c + u * nw);
+#pragma unroll
+        for (int q = 0; q < RCH; ++q) {
+          const int r = q * 32 + lane;
+          av[u][q] = r < nr ? __ldg(A + (r0 + r) + (c + u * nw) * a.lda) : T(0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < RCH; ++q) acc[q] = fma((double)av[u][q], xv[u], acc[q]);
+    }
+    for (; c < a.n; c += nw) {
+      const double xv = (double)__ldg(vk + c);
+#pragma unroll
+      for (int q = 0; q < RCH; ++q) {
+        const int r = q * 32 + lane;
+        if (r < nr) acc[q] = fma((double)__ldg(A + (r0 + r) + c * a.lda), xv, acc[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < RCH; ++q) red[warp][q * 32 + lane] = acc[q];
+    __syncthreads();
+    for (int r = tid; r < nr; r += blockDim.x) {
+      double s = 0.0;
+      for (int w2 = 0; w2 < nw; ++w2) s += red[w2][r];
+      wv[r] = (double)(T)s;  // the GEMV result in the array dtype
+    }
+    __syncthreads();
+  }
+  tt[nt_++] = clock64();  // after GEMV
+  // stage my rows of the basis (L2-resident) once: coalesced, all loads in flight
+  for (int e0 = 0; e0 < kc * nr; e0 += (int)blockDim.x * 8) {
+    T tv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + tid + u * (int)blockDim.x;
+      tv[u] = e < kc * nr ? V[(r0 + e % nr) + (int64_t)(e / nr) * a.ldv] : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + tid + u * (int)blockDim.x;
+      if (e < kc * nr) Vb[e] = tv[u];
+    }
+  }
+  __syncthreads();
+  tt[nt_++] = clock64();  // after V staging
+  // ---- CGS passes (krylov.py:134-138; pass 2 = re-orthogonalisation)
+  for (int ps = 0; ps < a.passes; ++ps) {
+    // partial h_j over my rows: warp per j, lanes over rows
+    for (int j = warp; j < kc; j += nw) {
+      const T* vj = Vb + j * nr;
+      double s = 0.0;
+      for (int r = lane; r < nr; r += 32) s = fma((double)vj[r], wv[r], s);
+      s = warp_sum(s);
+      if (lane == 0) sm[j] = s;
+    }
+    __syncthreads();
+    // exchange: CTA j reduces component j over the G partials (fixed order), publishes
+    // h_j; every CTA then polls the kc results (two round trips, low contention)
+    const uint32_t ep = a.seq * 4u + round + 1u;
+    uint64_t* buf = a.ll + (size_t)(round & 1) * G * 128;
+    uint64_t* res = a.ll + (size_t)2 * G * 128 + (size_t)(round & 1) * 128;
+    for (int j = tid; j < kc; j += blockDim.x) arn_put(buf + ((size_t)blockIdx.x * 128) + 2 * j, sm[j], ep);
+    ++round;
+    for (int j = (int)blockIdx.x; j < kc; j += (int)G) {
+      if (warp == 0) {
+        uint64_t wd[5][2];
+        while (true) {
+          bool ok = true;
+#pragma unroll
+          for (int u = 0; u < 5; ++u) {
+            const unsigned bb = lane + 32u * u;
+            if (bb < G) {
+              wd[u][0] = arn_load(buf + (size_t)bb * 128 + 2 * j);
+              wd[u][1] = arn_load(buf + (size_t)bb * 128 + 2 * j + 1);
+              ok = ok && (uint32_t)(wd[u][0] >> 32) == ep && (uint32_t)(wd[u][1] >> 32) == ep;
+            }
+          }
+          if (__all_sync(0xffffffffu, ok)) break;
+        }
+        double v = 0.0;
+#pragma unroll
+        for (int u = 0; u < 5; ++u)
+          if (lane + 32u * u < G)
+            v += __longlong_as_double((long long)((wd[u][0] & 0xffffffffull) | (wd[u][1] << 32)));
+        v = warp_sum(v);
+        if (lane == 0) arn_put(res + 2 * j, v, ep);
+      }
+    }
+    if (warp == 0) {
+      for (int j = lane; j < kc; j += 32) hs[j] = arn_get(res + 2 * j, ep);
+    }
+    __syncthreads();
+    if (blockIdx.x == 0) {
+      T* Hcol = H + (int64_t)k * a.ldh;
+      for (int j = tid; j < kc; j += blockDim.x) {
+        if (ps == 0) {
+          hsave[j] = hs[j];
+          Hcol[j] = (T)hs[j];
+        } else {
+          Hcol[j] = (T)(hsave[j] + hs[j]);
+        }
+      }
+    }
+    // w -= sum_j h_j V[:, j] for my rows (sequential axpys, krylov.py:136-138)
+    for (int r = tid; r < nr; r += blockDim.x) {
+      T wi = (T)wv[r];
+      for (int j = 0; j < kc; ++j) wi = add_rn(wi, mul_rn((T)(-hs[j]), Vb[j * nr + r]));
+      wv[r] = (double)wi;
+    }
+    __syncthreads();
+    tt[nt_++] = clock64();  // after each pass
+  }
+  // ---- h_{k+1,k} = ||w|| (scaled, Backend.nrm2) across the grid
+  Ssq q{0.0, 0.0};
+  for (int r = tid; r < nr; r += blockDim.x) q = ssq_add(q, wv[r]);
+  q = block_ssq(q, sm);
+  {
+    const uint32_t ep = a.seq * 4u + round + 1u;
+    uint64_t* buf = a.ll + (size_t)(round & 1) * G * 128;
+    if (tid == 0) {
+      arn_put(buf + (size_t)blockIdx.x * 128, q.scale, ep);
+      arn_put(buf + (size_t)blockIdx.x * 128 + 2, q.ssq, ep);
+    }
+    ++round;
+    uint64_t* res = a.ll + (size_t)2 * G * 128 + (size_t)(round & 1) * 128;
+    ++round;
+    if (blockIdx.x == 0 && warp == 0) {  // CTA 0 merges the G records in fixed order
+      uint64_t wd[5][4];
+      while (true) {
+        bool ok = true;
+#pragma unroll
+        for (int u = 0; u < 5; ++u) {
+          const unsigned bb = lane + 32u * u;
+          if (bb < G) {
+#pragma unroll
+            for (int z = 0; z < 4; ++z) {
+              wd[u][z] = arn_load(buf + (size_t)bb * 128 + z);
+              ok = ok && (uint32_t)(wd[u][z] >> 32) == ep;
+            }
+          }
+        }
+        if (__all_sync(0xffffffffu, ok)) break;
+      }
+      Ssq m{0.0, 0.0};
+#pragma unroll
+      for (int u = 0; u < 5; ++u)
+        if (lane + 32u * u < G)
+          m = ssq_merge(m, Ssq{__longlong_as_double((long long)((wd[u][0] & 0xffffffffull) | (wd[u][1] << 32))),
+                               __longlong_as_double((long long)((wd[u][2] & 0xffffffffull) | (wd[u][3] << 32)))});
+      m = warp_ssq(m);
+      if (lane == 0) {
+        arn_put(res, m.scale, ep);
+        arn_put(res + 2, m.ssq, ep);
+      }
+    }
+    if (tid == 0) {
+      sm[0] = arn_get(res, ep);
+      sm[1] = arn_get(res + 2, ep);
+    }
+    __syncthreads();
+  }
+  tt[nt_++] = clock64();  // after the norm exchange
+  if (a.trace && tid == 0)
+    for (int z = 1; z < nt_ && z < 7; ++z) atomicAdd(a.trace + blockIdx.x * 8 + z, (unsigned long long)(tt[z] - tt[z - 1]));
+  const double hk1 = ssq_norm(sm[0], sm[1]);
+  const bool happy = hk1 == 0.0;
+  {
+    T* vout = V + (int64_t)(k + 1) * a.ldv + r0;
+    const T sc = (T)(1.0 / hk1);
+    for (int r = tid; r < nr; r += blockDim.x) vout[r] = happy ? (T)wv[r] : mul_rn(sc, (T)wv[r]);
+  }
+  if (blockIdx.x == 0 && tid == 0) {  // Givens, estimate, stop (krylov.py:146-163)
+    T* Hk = H + (int64_t)k * a.ldh;
+    T* Hr = Hraw + (int64_t)k * a.ldh;
+    Hk[k + 1] = (T)hk1;
+    for (int j = 0; j <= k + 1; ++j) Hr[j] = Hk[j];
+    for (int j = 0; j < k; ++j) {
+      const T t = add_rn(mul_rn(cs[j], Hk[j]), mul_rn(sn[j], Hk[j + 1]));
+      Hk[j + 1] = add_rn(mul_rn(-sn[j], Hk[j]), mul_rn(cs[j], Hk[j + 1]));
+      Hk[j] = t;
+    }
+    const T denom = sizeof(T) == 8 ? (T)hypot((double)Hk[k], (double)Hk[k + 1])
+                                   : (T)hypotf((float)Hk[k], (float)Hk[k + 1]);
+    cs[k] = div_rn(Hk[k], denom);
+    sn[k] = div_rn(Hk[k + 1], denom);
+    Hk[k] = denom;
+    Hk[k + 1] = T(0);
+    g[k + 1] = mul_rn(-sn[k], g[k]);
+    g[k] = mul_rn(cs[k], g[k]);
+    const double est = fabs((double)g[k + 1]) / a.st->bnorm;
+    a.est[k] = est;
+    const int64_t total = a.total_before + k + 1;
+    if (happy) a.st->happy = 1;
+    if (happy || est <= a.tol || total >= a.cap) a.st->stop_k = k + 1;
+  }
+}
+
 // y = H[:inner,:inner]^-1 g[:inner] (backward_substitution, direct.py:139-152), one thread
 template <typename T>
 __global__ void gm_lsq_kernel(const T* H, int64_t ldh, const T* g, int inner, T* y, GmDev* st) {
@@ -446,7 +730,16 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
   const int64_t ldv = ceil_div(std::max<int64_t>(n, 1), 4) * 4;
   const int64_t ldh = m + 1;
   const int ldp = 64;
+  // fused one-kernel Arnoldi step for n <= 148 * 128 (latency-bound sizes, e.g. C2)
+  const char* fz = getenv("DENSOLVE_GMRES_FUSED");
+  int64_t arn_g = std::min<int64_t>((int64_t)ctx->num_sms, ceil_div(n, 4));
+  int64_t arn_per = ceil_div(ceil_div(n, arn_g), 4) * 4;  // 32-byte aligned row blocks
+  arn_g = ceil_div(n, arn_per);
+  const bool fused = !(fz && fz[0] == '0') && arn_per <= kArnMaxRows;
+  const int arn_rch = (int)std::min<int64_t>(4, ceil_div(arn_per, 32)) == 3 ? 4
+                                                                           : (int)std::min<int64_t>(4, ceil_div(arn_per, 32));
   size_t need = gp.part_bytes + (size_t)ldv * (m + 1) * sizeof(T) + (size_t)n * sizeof(T) +
+                (fused ? ((size_t)2 * arn_g * 128 + 256) * sizeof(uint64_t) + 256 : 0) +
                 (size_t)(ldh * m * 2 + 3 * (m + 2) + 64) * sizeof(T) +
                 ((size_t)mdb * ldp + (size_t)rblocks * 3 + (size_t)vg * 2 + 512) * sizeof(double) +
                 sizeof(GmDev) + 16 * 256;
@@ -469,6 +762,12 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
   double* est = cv.take<double>(64 * sizeof(double));
   double* scal = cv.take<double>(64 * sizeof(double));
   GmDev* st = cv.take<GmDev>(sizeof(GmDev));
+  uint64_t* arn_ll = fused ? cv.take<uint64_t>(((size_t)2 * arn_g * 128 + 256) * sizeof(uint64_t)) : nullptr;
+  unsigned long long* arn_trace = nullptr;
+  if (fused && getenv("DENSOLVE_GMRES_TRACE")) {
+    DS_CUDA(cudaMalloc((void**)&arn_trace, 8 * 8 * arn_g));
+    DS_CUDA(cudaMemsetAsync(arn_trace, 0, 8 * 8 * arn_g, ctx->stream));
+  }
 
   double* hbuf = nullptr;
   DS_TRY(ctx_hostbuf(ctx, 4096, (void**)&hbuf));
@@ -558,6 +857,47 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
         T* vk = V + k * ldv;
         T* w = V + (k + 1) * ldv;
         const int kc = (int)k + 1;
+        if (fused) {
+          const size_t arn_smem = (size_t)kc * arn_per * sizeof(T);
+          static bool arn_attr[2] = {false, false};
+          if (!arn_attr[sizeof(T) == 8]) {
+            const int mx = (int)std::min<size_t>(ctx->smem_optin, 200 * 1024);
+            DS_CUDA(cudaFuncSetAttribute(arnoldi_step_kernel<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            DS_CUDA(cudaFuncSetAttribute(arnoldi_step_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            DS_CUDA(cudaFuncSetAttribute(arnoldi_step_kernel<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            arn_attr[sizeof(T) == 8] = true;
+          }
+          ArnArgs aa;
+          aa.n = n;
+          aa.lda = lda;
+          aa.ldv = ldv;
+          aa.ldh = ldh;
+          aa.total_before = total_it;
+          aa.cap = cap;
+          aa.k = (int)k;
+          aa.passes = orth == DS_ORTH_CLASSICAL ? 1 : 2;
+          aa.per = (int)arn_per;
+          aa.seq = ++ctx->panel_seq;
+          aa.tol = tol;
+          aa.ll = arn_ll;
+          aa.est = est;
+          aa.st = st;
+          aa.trace = arn_trace;
+          if (arn_rch == 1)
+            arnoldi_step_kernel<T, 1><<<(unsigned)arn_g, kArnThreads, arn_smem, ctx->stream>>>(A, V, H, Hraw, g, cs, sn,
+                                                                                       aa, gt);
+          else if (arn_rch == 2)
+            arnoldi_step_kernel<T, 2><<<(unsigned)arn_g, kArnThreads, arn_smem, ctx->stream>>>(A, V, H, Hraw, g, cs, sn,
+                                                                                       aa, gt);
+          else
+            arnoldi_step_kernel<T, 4><<<(unsigned)arn_g, kArnThreads, arn_smem, ctx->stream>>>(A, V, H, Hraw, g, cs, sn,
+                                                                                       aa, gt);
+          count_launch(ctx);
+          (void)vk;
+          (void)w;
+          (void)kc;
+          continue;
+        }
         DS_TRY(gemv_launch<T>(ctx, gp, A, lda, vk, w, part, EPI_STORE, nullptr, nullptr, nullptr,
                               gt));
         const int passes = orth == DS_ORTH_CLASSICAL ? 1 : 2;
@@ -649,6 +989,21 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
       finish(false, DS_BREAKDOWN_NONE);
       break;
     }
+  }
+  if (arn_trace) {
+    std::vector<unsigned long long> h(8 * arn_g);
+    DS_CUDA(cudaMemcpy(h.data(), arn_trace, 8 * 8 * arn_g, cudaMemcpyDeviceToHost));
+    cudaFree(arn_trace);
+    double mean[8] = {}, mx[8] = {};
+    for (int64_t b = 0; b < arn_g; ++b)
+      for (int z = 1; z < 7; ++z) {
+        mean[z] += (double)h[b * 8 + z] / arn_g / std::max<int64_t>(total_it, 1);
+        mx[z] = std::max(mx[z], (double)h[b * 8 + z] / std::max<int64_t>(total_it, 1));
+      }
+    fprintf(stderr, "[gmres trace] n=%lld G=%lld per=%lld steps=%lld cycles/step mean(max): gemv %.0f(%.0f) "
+            "vstage %.0f(%.0f) pass0 %.0f(%.0f) pass1 %.0f(%.0f) norm %.0f(%.0f)\n", (long long)n, (long long)arn_g,
+            (long long)arn_per, (long long)total_it, mean[1], mx[1], mean[2], mx[2], mean[3], mx[3], mean[4], mx[4],
+            mean[5], mx[5]);
   }
   const int64_t hl = std::min<int64_t>((int64_t)history.size(), hist_cap);
   for (int64_t i = 0; i < hl; ++i) h_hist[i] = history[i];
