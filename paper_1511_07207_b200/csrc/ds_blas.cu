@@ -946,81 +946,54 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// b == 64 (every full LU panel): one thread per right-hand-side column, the
-// column's 64 entries in registers, the strict lower L staged in shared memory
-// and read as 16-byte pairs (broadcast: every thread reads the same element).
-// The j/i loops are fully unrolled (the dependence is only through z[j]), so
-// there is no barrier inside the solve and thousands of independent FMAs per
-// warp hide the FP64 latency.
+// b == 64 (every full LU panel): 8 threads per right-hand-side column, thread
+// `sub` owning rows sub, sub + 8, ..., sub + 56 in registers.  Step j broadcasts
+// z_j from its owner with one shuffle inside the 8-lane group and every thread
+// updates its rows i > j with L[i, j] from shared memory (the 8 lanes of a group
+// read 8 consecutive elements; the 4 groups of a warp read the same ones).  The
+// dependent chain is 63 x (shuffle + FMA) and each thread issues 504 FMAs, so a
+// launch of any width costs ~1-2 us (was one thread per column: 2016 dependent
+// FMAs, ~20 us per launch).
 template <typename T>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
     trsm_lower_unit_cols64(int64_t m, const T* __restrict__ L, int64_t ldl, const T* B, int64_t ldb,
                            T* Z, int64_t ldz) {
-  __shared__ __align__(16) T Ls[64][64];  // Ls[j][i] = L[i, j]
-  extern __shared__ __align__(16) unsigned char trsm_smem[];
-  T* Bs = reinterpret_cast<T*>(trsm_smem);  // [128][65]: the CTA's columns, staged coalesced
-  const int tid = threadIdx.x;
-  const int64_t c0 = (int64_t)blockIdx.x * 128;
-  const int nc = (int)min((int64_t)128, m - c0);
-  // staging: 32 independent loads in flight per thread before the shared stores
+  __shared__ __align__(16) T Ls[64][64];  // Ls[j][i] = L[i, j] (i > j), column j contiguous
+  const int tid = threadIdx.x, lane = tid & 31, sub = lane & 7;
+  const int gbase = lane & ~7;
   {
-    T v[32];
+    T v[16];
 #pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      const int e = tid + u * 128, i = e & 63, j = e >> 6;
+    for (int u = 0; u < 16; ++u) {
+      const int e = tid + u * 256, i = e & 63, j = e >> 6;
       v[u] = i > j ? L[i + (int64_t)j * ldl] : T(0);
     }
 #pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      const int e = tid + u * 128;
+    for (int u = 0; u < 16; ++u) {
+      const int e = tid + u * 256;
       Ls[e >> 6][e & 63] = v[u];
     }
   }
-  for (int base = 0; base < 64 * nc; base += 128 * 32) {  // 64 contiguous rows per column
-    T v[32];
+  __syncthreads();
+  const int64_t col = (int64_t)blockIdx.x * 32 + (tid >> 3);
+  const bool act = col < m;
+  T z[8];
+  const T* bb = B + (act ? col : 0) * ldb;
 #pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      const int e = base + tid + u * 128, i = e & 63, c = e >> 6;
-      v[u] = e < 64 * nc ? B[i + (c0 + c) * ldb] : T(0);
-    }
+  for (int k = 0; k < 8; ++k) z[k] = act ? bb[sub + 8 * k] : T(0);
 #pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      const int e = base + tid + u * 128;
-      if (e < 64 * nc) Bs[(e >> 6) * 65 + (e & 63)] = v[u];
+  for (int j = 0; j < 63; ++j) {
+    const T zj = __shfl_sync(0xffffffffu, z[j >> 3], gbase + (j & 7));
+#pragma unroll
+    for (int k = j >> 3; k < 8; ++k) {
+      const int i = sub + 8 * k;
+      if (i > j) z[k] = fma(-Ls[j][i], zj, z[k]);
     }
   }
-  __syncthreads();
-  if (tid < nc) {
-    T z[64];
+  if (act) {
+    T* zz = Z + col * ldz;
 #pragma unroll
-    for (int i = 0; i < 64; ++i) z[i] = Bs[tid * 65 + i];
-#pragma unroll
-    for (int j = 0; j < 63; ++j) {
-      const T zj = z[j];
-#pragma unroll
-      for (int i2 = (j + 1) / 2; i2 < 32; ++i2) {
-        const int i = 2 * i2;
-        T l0, l1;
-        if (sizeof(T) == 8) {
-          const double2 v = *reinterpret_cast<const double2*>(&Ls[j][i]);
-          l0 = (T)v.x;
-          l1 = (T)v.y;
-        } else {
-          const float2 v = *reinterpret_cast<const float2*>(&Ls[j][i]);
-          l0 = (T)v.x;
-          l1 = (T)v.y;
-        }
-        if (i > j) z[i] = fma(-l0, zj, z[i]);
-        z[i + 1] = fma(-l1, zj, z[i + 1]);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 64; ++i) Bs[tid * 65 + i] = z[i];
-  }
-  __syncthreads();
-  for (int e = tid; e < 64 * nc; e += blockDim.x) {
-    const int i = e & 63, c = e >> 6;
-    Z[i + (c0 + c) * ldz] = Bs[c * 65 + i];
+    for (int k = 0; k < 8; ++k) zz[sub + 8 * k] = z[k];
   }
 }
 
@@ -1062,15 +1035,7 @@ int trsm_lower_unit_launch(ds_ctx* ctx, int64_t b, int64_t m, const T* L, int64_
                            int64_t ldb, T* Z, int64_t ldz) {
   if (b == 0 || m == 0) return DS_OK;
   if (b == 64) {
-    const size_t smem = (size_t)128 * 65 * sizeof(T);
-    static bool attr[2] = {false, false};
-    if (!attr[sizeof(T) == 8]) {
-      DS_CUDA(cudaFuncSetAttribute(trsm_lower_unit_cols64<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-      attr[sizeof(T) == 8] = true;
-    }
-    trsm_lower_unit_cols64<T><<<(unsigned)ceil_div(m, 128), 128, smem, ctx->stream>>>(m, L, ldl, B, ldb,
-                                                                                     Z, ldz);
+    trsm_lower_unit_cols64<T><<<(unsigned)ceil_div(m, 32), 256, 0, ctx->stream>>>(m, L, ldl, B, ldb, Z, ldz);
   } else if (b < 64) {
     trsm_lower_unit_tile<T><<<(unsigned)ceil_div(m, 32), 256, 0, ctx->stream>>>(
         (int)b, m, L, ldl, B, ldb, Z, ldz);
