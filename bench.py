@@ -142,7 +142,9 @@ def run_reference(args):
         return
     from oracle import densolve_oracle as O
 
-    n, iters = args.n, args.iters
+    n = args.n
+    # bounded sample: ~0.35 s per CPU iteration at n=32768, keep the whole run near 3 minutes
+    iters = max(10, min(args.iters, int(180.0 / ((args.steps + 1) * 0.35))))
     cores = os.cpu_count() or 1
     A, b = spd_fast_host(n, 0)
     x0 = np.zeros(n)
@@ -159,8 +161,8 @@ def run_reference(args):
             "unit": f"CG iters/s (n={n} fp64)", "n_gpus": ws, "steps": args.steps,
             "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C4 CG dense SPD n={n} fp64, fixed {iters} iterations per step",
-                       "n": n, "iters_per_step": iters},
+            "config": {"workload": f"C4 CG dense SPD n={n} fp64, fixed iterations per step (bounded CPU sample)",
+                       "n": n, "iters_per_step": iters, "b200_arm_iters_per_step": args.iters},
             "cpu_baseline": {"value": val, "unit": f"CG iters/s (n={n} fp64)", "cores": cores, "kind": "port",
                              "sample": f"oracle.cg (NumPy/OpenBLAS restatement of krylov.cg_solve incl. "
                                        f"symmetry gate), n={n}, {iters} iterations per step"},
@@ -318,7 +320,7 @@ def run_b200(args):
 
     cpu = None
     if not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(n, iters)
+        cpu = cpu_baseline_sample(n, min(iters, 50))  # ~15-20 s of host work
 
     line = {"metric": BASELINE_METRIC, "value": round(value, 3), "unit": f"CG iters/s (n={n} fp64)",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
