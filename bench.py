@@ -192,9 +192,11 @@ def run_b200(args):
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
+    sharded = ws > 1 or args.force_sharded
+    if sharded:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if not dist.is_initialized():
+            dist.init_process_group("nccl", device_id=dev)
     from paper_1511_07207_b200 import (SolverConfig, cg_solve, get_backend, gmres_solve,
                                        lu_factor_blocked, pinned_empty)
     from paper_1511_07207_b200.device import DeviceArray
@@ -209,7 +211,7 @@ def run_b200(args):
     n, iters = args.n, args.iters
     cfg = SolverConfig(tolerance=1e-300, max_iterations=iters)
 
-    if ws > 1:
+    if sharded:
         from paper_1511_07207_b200 import distributed as D
         return D.bench_sharded_cg(args, torch, dev, be)
 
@@ -463,6 +465,7 @@ def main():
     ap.add_argument("--gmres-n", type=int, default=65536)
     ap.add_argument("--only-cg", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-sharded", action="store_true", help="run the row-sharded (N>1) path even at N=1")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3

@@ -96,6 +96,12 @@ _SIGNATURES = {
                              c_void_p, POINTER(c_int32)]),
     "ds_lu_factor_dev": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_int64,
                                  c_void_p, POINTER(c_int32)]),
+    "ds_comm_unique_id": (c_int, [c_void_p]),
+    "ds_comm_create": (c_int, [c_void_p, c_int, c_int, c_void_p, POINTER(c_void_p)]),
+    "ds_comm_destroy": (c_int, [c_void_p]),
+    "ds_cg_shard_iterations": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int64, c_void_p, c_int64, c_void_p,
+                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                       c_void_p, c_void_p, c_void_p, c_double, c_int64, c_int64, c_int64]),
     "ds_mm_read": (c_int, [c_char_p, c_void_p, c_int64, POINTER(c_int64), POINTER(c_int64), POINTER(c_int64)]),
     "ds_mm_last_error": (c_char_p, []),
     "ds_cholesky_factor": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_int64, POINTER(c_int64)]),

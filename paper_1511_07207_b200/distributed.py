@@ -110,6 +110,28 @@ class TorchComm:
     def barrier(self):
         self.dist.barrier(group=self.group)
 
+    def native(self, ctx, device):
+        """The library's own NCCL communicator over this group (ds_comm_create), created
+        once: rank 0's ncclUniqueId is broadcast through torch.distributed."""
+        import ctypes
+
+        import torch
+
+        if getattr(self, "_native", None) is None:
+            idt = torch.zeros(128, dtype=torch.uint8, device=device)
+            if self.rank == 0:
+                buf = (ctypes.c_ubyte * 128)()
+                _lib.check(ctx.lib.ds_comm_unique_id(ctypes.cast(buf, c_void_p)))
+                idt.copy_(torch.tensor(list(bytes(buf)), dtype=torch.uint8))
+            self.dist.broadcast(idt, 0, group=self.group)
+            raw = bytes(idt.cpu().tolist())
+            h = c_void_p()
+            buf = (ctypes.c_ubyte * 128).from_buffer_copy(raw)
+            _lib.check(ctx.lib.ds_comm_create(ctx.handle, self.size, self.rank, ctypes.cast(buf, c_void_p),
+                                              ctypes.byref(h)))
+            self._native = h
+        return self._native
+
 
 # ---------------------------------------------------------------------------
 # per-rank compute on the device (product implementation)
@@ -161,6 +183,13 @@ class CudaShardOps:
     def cg_init(self, bparts, rparts, nranks, state, hist, tol, cap):
         _lib.check(self.lib.ds_cg_shard_init(self.h, _p(bparts), _p(rparts), nranks, _p(state), _p(hist),
                                              float(tol), int(cap)))
+
+    def cg_iterations(self, comm, A, n_loc, n, full, x, r, p, Ap, state, hist, pap, pap_all, parts, rparts,
+                      tol, cap, k0, k1):
+        _lib.check(self.lib.ds_cg_shard_iterations(
+            self.h, comm, self.code(x), n_loc, n, _p(A), n_loc, _p(full), _p(x), _p(r), _p(p), _p(Ap),
+            _p(state), _p(hist), _p(pap), _p(pap_all), _p(parts), _p(rparts), float(tol), int(cap), int(k0),
+            int(k1)))
 
     def cg_update(self, nranks, pap_all, state, k, x, r, p, Ap, out3):
         _lib.check(self.lib.ds_cg_shard_update(self.h, self.code(x), x.numel(), nranks, _p(pap_all), _p(state),
@@ -300,12 +329,26 @@ def cg_solve_sharded(A_blk, b_loc, x0_loc, n: int, cfg: SolverConfig, comm, ops,
     if st[1] == 0.0:
         raise DegenerateRhsError("||b|| = 0")
     p = r.clone()
+    # DENSOLVE_NATIVE_NCCL=1: the chunk's iterations are enqueued by the library itself with
+    # its own NCCL communicator (ds_cg_shard_iterations, no per-iteration Python).  Off by
+    # default: at N=1 it measured slower (640 vs 720 it/s, raw NCCL kernels vs torch's 1-rank
+    # shortcut) and N>1 is unmeasured this round.  The per-call loop below also serves the
+    # CPU / gloo test double.
+    import os as _os
+    native = None
+    if (_os.environ.get("DENSOLVE_NATIVE_NCCL") == "1" and isinstance(ops, CudaShardOps)
+            and isinstance(comm, TorchComm) and dev.type == "cuda" and comm.dist.get_backend(comm.group) == "nccl"):
+        native = comm.native(ops.ctx, dev)
     k, chunk = 0, 2
     while True:
         st = state.cpu().numpy()
         if st[3] <= k or k >= cap or st[2] != 0:
             break
         kend = min(cap, k + chunk)
+        if native is not None:
+            ops.cg_iterations(native, A_blk, n_loc, n, full, x, r, p, Ap, state, hist, pap, pap_all, parts,
+                              rparts, cfg.tolerance, cap, k, kend)
+            k = kend
         while k < kend:
             comm.allgather(full, p)
             ops.gemv(A_blk, n_loc, n_loc, n, full, Ap)
@@ -569,9 +612,10 @@ def gather_block_cyclic(W_loc, idx, n: int, comm):
 # benchmark entry (C4 on N GPUs)
 # ---------------------------------------------------------------------------
 def spd_block_device(n: int, r0: int, r1: int, torch, device, seed: int = 0):
-    """Rows [r0, r1) of the synthetic symmetric matrix A = S + sqrt(n) I, S[i,j] =
+    """Rows [r0, r1) of the synthetic symmetric matrix A = S + 1.5 sqrt(n) I, S[i,j] =
     u(min(i,j), max(i,j)) with u a counter-based hash in [-1, 1) (symmetric by
-    construction, generated independently on every rank).  Returned as a
+    construction, generated independently on every rank).  S has a semicircle
+    spectrum of radius 2 sqrt(n/3) = 1.15 sqrt(n), so A is SPD with kappa ~ 7.6.  Returned as a
     column-major (n, r1-r0) tensor (= A[r0:r1, :]^T row-major)."""
     rows = torch.arange(r0, r1, device=device, dtype=torch.int64)
     out = torch.empty((n, r1 - r0), dtype=torch.float64, device=device)
@@ -586,15 +630,20 @@ def spd_block_device(n: int, r0: int, r1: int, torch, device, seed: int = 0):
         h = (h ^ (h >> 29)) * 0x2545F4914F6CDD1D & mask
         h = h ^ (h >> 32)
         v = (h & ((1 << 52) - 1)).to(torch.float64) * (2.0 / float(1 << 52)) - 1.0
-        v = torch.where(i == j, v + math.sqrt(n), v)
+        v = torch.where(i == j, v + 1.5 * math.sqrt(n), v)
         out[c0:c0 + cols.numel()] = v
     return out
 
 
 def bench_sharded_cg(args, torch, dev, be):
-    """`bench.py --gpus N` under torchrun: C4 CG row-sharded over N GPUs (strong scaling)."""
+    """`bench.py --gpus N` under torchrun: C4 CG row-sharded over N GPUs (strong scaling).
+    Same JSON contract as the 1-GPU line: device-resident `value` (max over ranks of the
+    CUDA-event time), `e2e` (each rank uploads its row block of A, b, x0 from pinned host
+    memory and downloads its x shard every step), the per-rank GEMV `roofline`, clocks."""
     import json
     import torch.distributed as dist
+
+    from bench import BASELINE_METRIC, ClockSampler, _peaks  # noqa: E402  (repo root on sys.path)
 
     comm = TorchComm()
     ops = CudaShardOps(be.ctx)
@@ -617,24 +666,79 @@ def bench_sharded_cg(args, torch, dev, be):
     comm.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = be.ctx.launches()
-    e0.record(stream)
-    for _ in range(args.steps):
-        x, rep = cg_solve_sharded(A_blk, b, x0, n, cfg, comm, ops)
-    e1.record(stream)
-    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            x, rep = cg_solve_sharded(A_blk, b, x0, n, cfg, comm, ops)
+        e1.record(stream)
+        torch.cuda.synchronize()
     comm.barrier()
+    launches = be.ctx.launches() - l0
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
+
+    # per-rank GEMV roofline: the local n x n_loc block streamed once (8 (n n_loc + n + n_loc) B)
+    full = torch.zeros(N, dtype=torch.float64, device=dev)
+    y = torch.empty(n_loc, dtype=torch.float64, device=dev)
+    for _ in range(3):
+        ops.gemv(A_blk, n_loc, n_loc, n, full, y)
+    torch.cuda.synchronize()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record(stream)
+    for _ in range(20):
+        ops.gemv(A_blk, n_loc, n_loc, n, full, y)
+    g1.record(stream)
+    torch.cuda.synchronize()
+    gemv_ms = torch.tensor([g0.elapsed_time(g1) / 20], dtype=torch.float64, device=dev)
+    dist.all_reduce(gemv_ms, op=dist.ReduceOp.MAX)
+    gemv_ms = float(gemv_ms.item())
+    hbm_peak, peak_src = _peaks()
+    gbytes = 8.0 * (n * n_loc + n + n_loc)
+    achieved = gbytes / (gemv_ms / 1e3) / 1e9
+
+    # end to end: pinned host shards -> device -> solve -> x shard back, every step
+    A_h = torch.empty((n, n_loc), dtype=torch.float64, pin_memory=True)
+    A_h.copy_(A_blk)
+    b_h = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
+    b_h.copy_(b)
+    x0_h = torch.zeros(n_loc, dtype=torch.float64, pin_memory=True)
+    x_h = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
+    torch.cuda.synchronize()
+    comm.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        A_blk.copy_(A_h, non_blocking=True)
+        b.copy_(b_h, non_blocking=True)
+        x0.copy_(x0_h, non_blocking=True)
+        x, rep = cg_solve_sharded(A_blk, b, x0, n, cfg, comm, ops)
+        x_h.copy_(x, non_blocking=True)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    comm.barrier()
+    e2e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
     if q == 0:
         value = iters * args.steps / (ms / 1e3)
+        unit = f"CG iters/s (n={n} fp64)"
         print(json.dumps({
-            "metric": "CG/GMRES iters/sec & HBM GB/s; LU GFLOP/s at n=32768, 1/2/4/8 B200 vs CPU",
-            "value": round(value, 3), "unit": f"CG iters/s (n={n} fp64)", "n_gpus": G, "steps": args.steps,
+            "metric": BASELINE_METRIC, "value": round(value, 3), "unit": unit, "n_gpus": G, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (hash-generated symmetric A = S + sqrt(n) I, row blocks generated per rank)",
+            "data": "synthetic (hash-generated symmetric A = S + 1.5 sqrt(n) I, row blocks generated per rank)",
             "config": {"workload": f"C4: CG dense SPD n={n} fp64 row-sharded over {G} GPUs, {iters} iterations/step",
                        "n": n, "iters_per_step": iters, "parallelism": f"rows{G}",
                        "l2_policy": "inputs larger than L2"},
-            "gpu_launches": be.ctx.launches() - l0, "timing": "max over ranks of CUDA-event time"}), flush=True)
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                         "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                         "kernel": "per-rank ds_gemv on the n x n_loc block (max over ranks)",
+                         "algorithmic_bytes_per_launch": gbytes, "avg_launch_ms": round(gemv_ms, 4),
+                         "peak_source": peak_src},
+            "cpu_baseline": None,
+            "e2e": {"value": iters * args.steps / (e2e_ms / 1e3), "unit": unit,
+                    "h2d_bytes_per_step": int(G * (A_h.numel() + 2 * n_loc) * 8),
+                    "d2h_bytes_per_step": int(G * n_loc * 8), "ms_per_step": e2e_ms / args.steps},
+            "gpu_launches": launches, "clocks": clk.summary(),
+            "timing": "max over ranks of CUDA-event time"}), flush=True)
