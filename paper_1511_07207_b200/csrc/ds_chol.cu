@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "ds_common.cuh"
 #include "ds_kernels.cuh"
@@ -157,14 +158,32 @@ static int transpose_launch(ds_ctx* ctx, int64_t rows, int64_t cols, const T* in
 
 template <typename T>
 int chol_factor_impl(ds_ctx* ctx, int64_t n, T* W, int64_t ld, int64_t b, long long* d_err) {
-  const int64_t NB = (b >= 256 || b >= n) ? std::min<int64_t>(b, n)
-                                          : std::min<int64_t>(n, b * std::max<int64_t>(1, 256 / b));
-  // scratch for the transposed L block (B operand of the SYRK): NB x n
+  static const int64_t nb_target = [] {
+    const char* e = getenv("DENSOLVE_CHOL_NB");  // tuning knob
+    return e ? std::max<int64_t>(64, atoll(e)) : (int64_t)512;
+  }();
+  const int64_t NB = (b >= nb_target || b >= n) ? std::min<int64_t>(b, n)
+                                                : std::min<int64_t>(n, b * std::max<int64_t>(1, nb_target / b));
+  // scratch for the transposed L blocks (B operands of the SYRKs): NB x n for the main
+  // stream, NB x NB... x n for the look-ahead panel on the side stream
   void* ws = nullptr;
-  DS_TRY(ctx_workspace(ctx, (size_t)NB * (size_t)n * sizeof(T) + 4096, &ws));
-  T* Bt = (T*)ws;
-  for (int64_t kb = 0; kb < n; kb += NB) {
-    const int64_t bf = std::min<int64_t>(kb + NB, n);
+  DS_TRY(ctx_workspace(ctx, 2 * (size_t)NB * (size_t)n * sizeof(T) + 8192, &ws));
+  T* Bt_main = (T*)ws;
+  T* Bt_side = Bt_main + (size_t)NB * (size_t)n + 64;
+  const bool lookahead = n > NB && n >= 2048 && !(getenv("DENSOLVE_CHOL_LOOKAHEAD") &&
+                                                   getenv("DENSOLVE_CHOL_LOOKAHEAD")[0] == '0');
+  if (lookahead && !ctx->side) {
+    int lo = 0, hi = 0;
+    DS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    DS_CUDA(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, hi));
+    DS_CUDA(cudaStreamCreateWithPriority(&ctx->aux, cudaStreamNonBlocking, lo));
+    DS_CUDA(cudaEventCreateWithFlags(&ctx->ev_a, cudaEventDisableTiming));
+    DS_CUDA(cudaEventCreateWithFlags(&ctx->ev_b, cudaEventDisableTiming));
+    DS_CUDA(cudaEventCreateWithFlags(&ctx->ev_c, cudaEventDisableTiming));
+  }
+  // factor the outer panel [kb, bf): the reference's b-panels (direct.py:103-115), each
+  // followed by the update of the rest of the outer panel
+  auto factor_outer = [&](int64_t kb, int64_t bf, T* Bt) -> int {
     for (int64_t ib = kb; ib < bf; ib += b) {
       const int64_t ibf = std::min<int64_t>(ib + b, bf);
       // a b-panel wider than kCholW is factored in kCholW-wide slices with a K-slice
@@ -190,11 +209,36 @@ int chol_factor_impl(ds_ctx* ctx, int64_t n, T* W, int64_t ld, int64_t b, long l
         }
       }
     }
-    if (bf < n) {  // trailing SYRK (direct.py:117-119), lower tiles only
-      const int64_t K = bf - kb, m = n - bf;
-      DS_TRY(transpose_launch<T>(ctx, m, K, W + bf + kb * ld, ld, Bt, K));
-      DS_TRY(gemm_sub_lower_launch<T>(ctx, m, m, K, W + bf + kb * ld, ld, Bt, K, W + bf + bf * ld, ld));
+    return DS_OK;
+  };
+  DS_TRY(factor_outer(0, std::min<int64_t>(NB, n), Bt_main));
+  for (int64_t kb = 0; kb < n; kb += NB) {
+    const int64_t bf = std::min<int64_t>(kb + NB, n);
+    if (bf >= n) break;
+    const int64_t bf2 = std::min<int64_t>(bf + NB, n);
+    const int64_t K = bf - kb, m = n - bf;
+    // trailing SYRK (direct.py:117-119), lower tiles only: the next outer panel's
+    // columns [bf, bf2) first, then (overlapping that panel's factorization on the
+    // side stream) the rest of the trailing matrix
+    DS_TRY(transpose_launch<T>(ctx, m, K, W + bf + kb * ld, ld, Bt_main, K));
+    DS_TRY(gemm_sub_lower_launch<T>(ctx, m, bf2 - bf, K, W + bf + kb * ld, ld, Bt_main, K, W + bf + bf * ld, ld));
+    if (lookahead) {
+      DS_CUDA(cudaEventRecord(ctx->ev_a, ctx->stream));
+      DS_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_a, 0));
+      cudaStream_t main = ctx->stream;
+      ctx->stream = ctx->side;
+      const int rc = factor_outer(bf, bf2, Bt_side);
+      ctx->stream = main;
+      DS_TRY(rc);
+      DS_CUDA(cudaEventRecord(ctx->ev_b, ctx->side));
     }
+    if (bf2 < n)
+      DS_TRY(gemm_sub_lower_launch<T>(ctx, n - bf2, n - bf2, K, W + bf2 + kb * ld, ld, Bt_main + (bf2 - bf) * K,
+                                      K, W + bf2 + bf2 * ld, ld));
+    if (lookahead)
+      DS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_b, 0));
+    else
+      DS_TRY(factor_outer(bf, bf2, Bt_main));
   }
   dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 64)), (unsigned)n);
   tril_kernel<T><<<g, 256, 0, ctx->stream>>>(n, W, ld);
