@@ -210,3 +210,55 @@ def test_relative_residual_device(backend, rng):
     x, b = rng.standard_normal(8), rng.standard_normal(8)
     assert relative_residual(A, x, b) == pytest.approx(O.relative_residual(A, x, b), rel=1e-13)
     assert relative_residual(np.asfortranarray(np.eye(2)), np.zeros(2), np.array([3.0, 4.0])) == 1.0
+
+
+# ---- larger / ragged shapes through the register-row panel kernel (several CTA
+# layouts: 256-row CTAs, the 4-threads-per-row tail, ragged last panels).  The pivot
+# oracle at these sizes is LAPACK getrf (scipy), which SURVEY.md §8c validated to give
+# the reference's pivots on these families.
+@pytest.mark.parametrize("n,b", [(3001, 64), (4096, 64), (2500, 48), (1300, 100)])
+def test_lu_large_ragged_pivots_vs_lapack(backend, n, b):
+    sl = pytest.importorskip("scipy.linalg")
+    A = np.asfortranarray(np.random.default_rng([n, b]).uniform(-1.0, 1.0, (n, n)))
+    f = lu_factor_blocked(A, b, backend)
+    lu_ref, piv_ref = sl.lu_factor(A)
+    np.testing.assert_array_equal(f.pivots, piv_ref)
+    # same pivots; factors agree to summation-order noise relative to the factor scale
+    # (LAPACK's recursive blocking groups the trailing updates differently again)
+    d = np.max(np.abs(f.packed - lu_ref)) / np.max(np.abs(lu_ref))
+    assert d <= 1e-12 * n, d
+    xt = np.random.default_rng(1).uniform(-1, 1, n)
+    x = lu_solve(f, A @ xt)
+    assert np.linalg.norm(x - xt) <= 1e-8 * np.linalg.norm(xt)
+
+
+def test_lu_large_singular_column(backend):
+    # an exactly zero column in the middle of a large matrix: singular flag, the
+    # reference's semantics (skip scale / rank-1 update, keep going), pivots = LAPACK's
+    sl = pytest.importorskip("scipy.linalg")
+    n = 2000
+    A = np.asfortranarray(np.random.default_rng(5).uniform(-1.0, 1.0, (n, n)))
+    A[:, 1234] = 0.0
+    f = lu_factor_blocked(A, 64, backend)
+    assert f.singular
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        _, piv_ref = sl.lu_factor(A, check_finite=False)
+    np.testing.assert_array_equal(f.pivots[:1234], piv_ref[:1234])
+    with pytest.raises(Exception):
+        lu_solve(f, np.ones(n))
+
+
+def test_lu_f32_large(backend):
+    sl = pytest.importorskip("scipy.linalg")
+    n = 2048
+    A = np.asfortranarray(np.random.default_rng(11).uniform(-1.0, 1.0, (n, n)).astype(np.float32))
+    f = lu_factor_blocked(A, 64, backend)
+    assert f.packed.dtype == np.float32
+    _, piv_ref = sl.lu_factor(A.astype(np.float64))
+    # fp32 rounding may legitimately flip a near-tie; nearly all pivots agree
+    assert np.mean(f.pivots == piv_ref) > 0.99
+    xt = np.random.default_rng(2).uniform(-1, 1, n).astype(np.float32)
+    x = lu_solve(f, A @ xt)
+    assert np.linalg.norm(x - xt) <= 1e-2 * np.linalg.norm(xt)
