@@ -312,6 +312,7 @@ __global__ void __launch_bounds__(kPanelRegThreads, 1) lu_panel_smem_kernel(T* _
       for (int k = 0; k < PW; ++k) stage[1][q * PW + k] = y[k];
     }
     __syncthreads();
+    if (G == 1) return;  // a single CTA reads its candidate straight from shared memory
     for (int j = t; j < ncol; j += nt) {
       if (bi != INT64_MAX) {
         const T v = j < cc ? Ls[j * ldt + (int)(bi - my_lo)] : stage[0][j - cc];
@@ -324,12 +325,16 @@ __global__ void __launch_bounds__(kPanelRegThreads, 1) lu_panel_smem_kernel(T* _
     }
   };
 
+  unsigned long long cand_k;  // this CTA's candidate of the current column
+  int64_t cand_i;
   {
     unsigned long long bk = lead ? piv_key(fabs((double)y[0])) : 0ull;
     int64_t bi = lead ? g : INT64_MAX;
     cta_argmax_key(bk, bi, wk[0], wi[0]);
-    publish_header(0, bk, bi);
+    if (G > 1) publish_header(0, bk, bi);
     publish_rows(0, bi);
+    cand_k = bk;
+    cand_i = bi;
   }
   for (int c = 0; c < ncol; ++c) {
     const int64_t i = a.kb + c;
@@ -339,7 +344,7 @@ __global__ void __launch_bounds__(kPanelRegThreads, 1) lu_panel_smem_kernel(T* _
     // ---- poll the G headers, reduce (ties -> lowest row)
     unsigned long long gk = 0ull;
     int64_t gi = INT64_MAX;
-    for (int b = t; b < (int)G; b += nt) {
+    for (int b = t; G > 1 && b < (int)G; b += nt) {
       const uint64_t* h = hdr + ((size_t)par * G + b) * kHdrWords;
       uint64_t x0, x1, x2;
       do {
@@ -355,7 +360,12 @@ __global__ void __launch_bounds__(kPanelRegThreads, 1) lu_panel_smem_kernel(T* _
       }
     }
     const long long t_d = clock64();
-    cta_argmax_key(gk, gi, wk[1], wi[1]);
+    if (G > 1) {
+      cta_argmax_key(gk, gi, wk[1], wi[1]);
+    } else {  // one CTA: its own candidate is the pivot
+      gk = cand_k;
+      gi = cand_i;
+    }
     const long long t_e = clock64();
     const int64_t p = gi == INT64_MAX ? i : gi;
     const int win = gi == INT64_MAX ? -1 : (int)((gi - a.kb) / per);
@@ -364,7 +374,17 @@ __global__ void __launch_bounds__(kPanelRegThreads, 1) lu_panel_smem_kernel(T* _
       const uint64_t* pr = rows + ((size_t)par * G + (win < 0 ? 0 : win)) * RW;
       const uint64_t* dr = diag + (size_t)par * RW;
       for (int j = t; j < c + kPanelMaxW + 2; j += nt) {
-        if (j < ncol) {
+        if (j < ncol && G == 1) {  // single CTA: rows from shared memory (published by publish_rows)
+          const int64_t pi_ = gi == INT64_MAX ? i : gi;
+          const T pv = j < c ? Ls[j * ldt + (int)(pi_ - my_lo)] : stage[0][j - c];
+          const T dv = j < c ? Ls[j * ldt + (int)(i - my_lo)] : stage[1][j - c];
+          drow[j] = dv;
+          prow[j] = gi == INT64_MAX ? dv : pv;
+          if (j >= c) {
+            drs[j - c] = dv;
+            prs[j - c] = prow[j];
+          }
+        } else if (j < ncol) {
           uint64_t pw[VW], dw[VW];
           while (true) {
             bool ok = true;
@@ -433,7 +453,9 @@ __global__ void __launch_bounds__(kPanelRegThreads, 1) lu_panel_smem_kernel(T* _
     }
     if (c + 1 < ncol) {
       cta_argmax_key(bk, bi, wk[0], wi[0]);
-      publish_header(c + 1, bk, bi);  // the exchange of column c + 1 starts here
+      if (G > 1) publish_header(c + 1, bk, bi);  // the exchange of column c + 1 starts here
+      cand_k = bk;
+      cand_i = bi;
     }
     // ---- rest of the rank-1 update of my slice (direct.py:75-79), then rotate by one
     if (act) {
@@ -1087,6 +1109,12 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
     for (size_t k = 0; k < std::min<size_t>(6, d.size()); ++k)
       fprintf(stderr, " #%d %.2f ms (enq at %.2f ms)", d[k].second, d[k].first,
               (thost[d[k].second] - thost.front()) / 1e3);
+    fprintf(stderr, "\n[lu timeline] per outer panel (ms):");
+    for (size_t k = 1; k < tev.size(); ++k) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, tev[k - 1], tev[k]);
+      fprintf(stderr, " %.2f", ms);
+    }
     fprintf(stderr, "\n");
     for (auto e : tev) cudaEventDestroy(e);
   }
