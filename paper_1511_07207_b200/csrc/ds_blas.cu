@@ -157,7 +157,17 @@ __global__ void __launch_bounds__(kRedThreads)
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double s = 0.0;
   if (i < m) {
-    for (int64_t c = 0; c < nchunks; ++c) s += part[c * m + i];
+    // the chunk partials are summed in chunk order; loads are batched 8 at a time so the
+    // L2 round trips overlap instead of serialising behind the dependent adds
+    int64_t c = 0;
+    for (; c + 8 <= nchunks; c += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = part[(c + u) * m + i];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; c < nchunks; ++c) s += part[c * m + i];
   }
   const T yi = (T)s;
   if (EPI == EPI_STORE) {

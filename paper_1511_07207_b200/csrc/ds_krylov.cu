@@ -9,9 +9,11 @@
 // (Gate{stop_it, k}) so the host enqueues iterations speculatively in growing
 // chunks and synchronises only once per chunk — never once per dot product as
 // the reference's Python loop does.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -319,7 +321,15 @@ __global__ void __launch_bounds__(kT)
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     T wi = w[i];
-    for (int j = 0; j < kc; ++j) wi = add_rn(wi, mul_rn((T)(-hs[j]), V[i + (int64_t)j * ldv]));
+    int j = 0;
+    for (; j + 8 <= kc; j += 8) {
+      T vv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) vv[u] = V[i + (int64_t)(j + u) * ldv];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) wi = add_rn(wi, mul_rn((T)(-hs[j + u]), vv[u]));
+    }
+    for (; j < kc; ++j) wi = add_rn(wi, mul_rn((T)(-hs[j]), V[i + (int64_t)j * ldv]));
     w[i] = wi;
     q = ssq_add(q, (double)wi);
   }
@@ -662,6 +672,135 @@ __global__ void __launch_bounds__(kArnThreads)
   }
 }
 
+// ============================================================================
+// Cluster orthogonalisation (small / medium n): after w = A v_k (the streamed
+// GEMV on every SM), ONE thread-block cluster of up to 16 CTAs runs the CGS
+// passes, the norm, the normalisation and the Givens step.  Each CTA owns a
+// contiguous row block; the three reductions per step go through distributed
+// shared memory (partials in each CTA's smem, cluster barrier, every CTA reads the
+// CL partials of each component in rank order => identical h everywhere) instead
+// of L2 round trips.  CTA rank 0 records H / Hraw and runs the Givens logic.
+// ============================================================================
+constexpr int kOrthThreads = 512;
+
+template <typename T>
+__global__ void __launch_bounds__(kOrthThreads, 1)
+    arnoldi_orth_cluster_kernel(int64_t n, T* V, int64_t ldv, int k, int passes, T* H, T* Hraw, int64_t ldh, T* g,
+                                T* cs, T* sn, double* est_out, GmDev* st, double tol, int64_t total_before,
+                                int64_t cap, Gate gate) {
+  namespace cgr = cooperative_groups;
+  if (gated(gate)) return;
+  cgr::cluster_group cluster = cgr::this_cluster();
+  const unsigned CL = cluster.num_blocks();
+  const unsigned rank = cluster.block_rank();
+  extern __shared__ __align__(16) unsigned char orth_smem[];
+  double* wv = reinterpret_cast<double*>(orth_smem);  // my rows of w (fp64 copy of T values)
+  __shared__ double part[3][64];                      // my partials, buffer per exchange
+  __shared__ double hs[64], hsave[64], sm[64];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kOrthThreads / 32;
+  const int64_t per = ceil_div(ceil_div(n, (int64_t)CL), 4) * 4;
+  const int64_t r0 = (int64_t)rank * per;
+  const int nr = (int)max((int64_t)0, min(per, n - r0));
+  const int kc = k + 1;
+  T* w = V + (int64_t)(k + 1) * ldv;  // A v_k, written by the GEMV
+  for (int r = tid; r < nr; r += blockDim.x) wv[r] = (double)w[r0 + r];
+  __syncthreads();
+  for (int ps = 0; ps < passes; ++ps) {
+    // partial h_j over my rows: warp per j, lanes over rows (V from L2)
+    for (int j = warp; j < kc; j += nw) {
+      const T* vj = V + (int64_t)j * ldv + r0;
+      double s = 0.0;
+#pragma unroll 8
+      for (int r = lane; r < nr; r += 32) s = fma((double)vj[r], wv[r], s);
+      s = warp_sum(s);
+      if (lane == 0) part[ps][j] = s;
+    }
+    cluster.sync();
+    for (int j = tid; j < kc; j += blockDim.x) {  // rank-ordered sum over the cluster (DSMEM)
+      double s = 0.0;
+      for (unsigned b = 0; b < CL; ++b) s += cluster.map_shared_rank(&part[ps][0], b)[j];
+      hs[j] = s;
+    }
+    __syncthreads();
+    if (rank == 0) {
+      T* Hcol = H + (int64_t)k * ldh;
+      for (int j = tid; j < kc; j += blockDim.x) {
+        if (ps == 0) {
+          hsave[j] = hs[j];
+          Hcol[j] = (T)hs[j];
+        } else {
+          Hcol[j] = (T)(hsave[j] + hs[j]);
+        }
+      }
+    }
+    // w -= sum_j h_j V[:, j] for my rows (sequential axpys, krylov.py:136-138)
+    for (int r = tid; r < nr; r += blockDim.x) {
+      T wi = (T)wv[r];
+      const T* vr = V + r0 + r;
+      int j = 0;
+      for (; j + 8 <= kc; j += 8) {  // 8 basis loads in flight, then the ordered axpys
+        T vv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) vv[u] = vr[(int64_t)(j + u) * ldv];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) wi = add_rn(wi, mul_rn((T)(-hs[j + u]), vv[u]));
+      }
+      for (; j < kc; ++j) wi = add_rn(wi, mul_rn((T)(-hs[j]), vr[(int64_t)j * ldv]));
+      wv[r] = (double)wi;
+    }
+    __syncthreads();
+  }
+  // h_{k+1,k} = ||w|| (scaled): (scale, ssq) per CTA, merged in rank order
+  Ssq q{0.0, 0.0};
+  for (int r = tid; r < nr; r += blockDim.x) q = ssq_add(q, wv[r]);
+  q = block_ssq(q, sm);
+  if (tid == 0) {
+    part[2][0] = q.scale;
+    part[2][1] = q.ssq;
+  }
+  cluster.sync();
+  if (tid == 0) {
+    Ssq m{0.0, 0.0};
+    for (unsigned b = 0; b < CL; ++b) {
+      const double* rp = cluster.map_shared_rank(&part[2][0], b);
+      m = ssq_merge(m, Ssq{rp[0], rp[1]});
+    }
+    sm[0] = ssq_norm(m.scale, m.ssq);
+  }
+  // no CTA may exit (or reuse part[]) while others still read its shared memory
+  cluster.sync();
+  const double hk1 = sm[0];
+  const bool happy = hk1 == 0.0;
+  {
+    const T sc = (T)(1.0 / hk1);  // scal(1.0/hk1, w) (krylov.py:143-144)
+    for (int r = tid; r < nr; r += blockDim.x) w[r0 + r] = happy ? (T)wv[r] : mul_rn(sc, (T)wv[r]);
+  }
+  if (rank == 0 && tid == 0) {  // Givens, estimate, stop (krylov.py:146-163)
+    T* Hk = H + (int64_t)k * ldh;
+    T* Hr = Hraw + (int64_t)k * ldh;
+    Hk[k + 1] = (T)hk1;
+    for (int j = 0; j <= k + 1; ++j) Hr[j] = Hk[j];
+    for (int j = 0; j < k; ++j) {
+      const T t = add_rn(mul_rn(cs[j], Hk[j]), mul_rn(sn[j], Hk[j + 1]));
+      Hk[j + 1] = add_rn(mul_rn(-sn[j], Hk[j]), mul_rn(cs[j], Hk[j + 1]));
+      Hk[j] = t;
+    }
+    const T denom = sizeof(T) == 8 ? (T)hypot((double)Hk[k], (double)Hk[k + 1])
+                                   : (T)hypotf((float)Hk[k], (float)Hk[k + 1]);
+    cs[k] = div_rn(Hk[k], denom);
+    sn[k] = div_rn(Hk[k + 1], denom);
+    Hk[k] = denom;
+    Hk[k + 1] = T(0);
+    g[k + 1] = mul_rn(-sn[k], g[k]);
+    g[k] = mul_rn(cs[k], g[k]);
+    const double est = fabs((double)g[k + 1]) / st->bnorm;
+    est_out[k] = est;
+    const int64_t total = total_before + k + 1;
+    if (happy) st->happy = 1;
+    if (happy || est <= tol || total >= cap) st->stop_k = k + 1;
+  }
+}
+
 // y = H[:inner,:inner]^-1 g[:inner] (backward_substitution, direct.py:139-152), one thread
 template <typename T>
 __global__ void gm_lsq_kernel(const T* H, int64_t ldh, const T* g, int inner, T* y, GmDev* st) {
@@ -736,6 +875,48 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
   int64_t arn_per = ceil_div(ceil_div(n, arn_g), 4) * 4;  // 32-byte aligned row blocks
   arn_g = ceil_div(n, arn_per);
   const bool fused = !(fz && fz[0] == '0') && arn_per <= kArnMaxRows;
+  // cluster orthogonalisation (DENSOLVE_GMRES_ORTH=cluster|grid): the largest cluster
+  // (16 non-portable, else 8) that the device can co-schedule; rows per CTA <= 4096
+  int orth_cl = 0;
+  size_t orth_smem = 0;
+  {
+    const char* oe = getenv("DENSOLVE_GMRES_ORTH");
+    const bool want = !(oe && strcmp(oe, "grid") == 0) && n <= 16 * 4096;
+    if (want) {
+      static int best[2] = {-1, -1};
+      int& bc = best[sizeof(T) == 8];
+      if (bc < 0) {
+        bc = 0;
+        DS_CUDA(cudaFuncSetAttribute(arnoldi_orth_cluster_kernel<T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        DS_CUDA(cudaFuncSetAttribute(arnoldi_orth_cluster_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     4096 * (int)sizeof(double)));
+        for (int c : {16, 8}) {
+          cudaLaunchConfig_t lc = {};
+          lc.gridDim = dim3((unsigned)c);
+          lc.blockDim = dim3(kOrthThreads);
+          lc.dynamicSmemBytes = 4096 * sizeof(double);
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeClusterDimension;
+          at[0].val.clusterDim.x = (unsigned)c;
+          at[0].val.clusterDim.y = 1;
+          at[0].val.clusterDim.z = 1;
+          lc.attrs = at;
+          lc.numAttrs = 1;
+          int nclusters = 0;
+          if (cudaOccupancyMaxActiveClusters(&nclusters, (void*)arnoldi_orth_cluster_kernel<T>, &lc) == cudaSuccess &&
+              nclusters >= 1) {
+            bc = c;
+            break;
+          }
+          cudaGetLastError();
+        }
+      }
+      if (bc > 0 && ceil_div(ceil_div(n, (int64_t)bc), 4) * 4 <= 4096) {
+        orth_cl = bc;
+        orth_smem = (size_t)ceil_div(ceil_div(n, (int64_t)bc), 4) * 4 * sizeof(double);
+      }
+    }
+  }
   const int arn_rch = (int)std::min<int64_t>(4, ceil_div(arn_per, 32)) == 3 ? 4
                                                                            : (int)std::min<int64_t>(4, ceil_div(arn_per, 32));
   size_t need = gp.part_bytes + (size_t)ldv * (m + 1) * sizeof(T) + (size_t)n * sizeof(T) +
@@ -841,7 +1022,9 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
     DS_CHECK_LAUNCH();
 
     // inner Arnoldi steps, enqueued in chunks behind the device gate
-    int64_t k = 0, chunk = 4;
+    // all m steps are enqueued at once (gated kernels after a stop are near-free): one
+    // host synchronisation per cycle instead of one per chunk
+    int64_t k = 0, chunk = m;
     int64_t stop_k = m;
     while (true) {
       if (k > 0) {
@@ -857,6 +1040,26 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
         T* vk = V + k * ldv;
         T* w = V + (k + 1) * ldv;
         const int kc = (int)k + 1;
+        if (orth_cl > 0) {  // streamed GEMV on every SM + one-cluster orthogonalisation
+          DS_TRY(gemv_launch<T>(ctx, gp, A, lda, vk, w, part, EPI_STORE, nullptr, nullptr, nullptr, gt));
+          cudaLaunchConfig_t lc = {};
+          lc.gridDim = dim3((unsigned)orth_cl);
+          lc.blockDim = dim3(kOrthThreads);
+          lc.dynamicSmemBytes = orth_smem;
+          lc.stream = ctx->stream;
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeClusterDimension;
+          at[0].val.clusterDim.x = (unsigned)orth_cl;
+          at[0].val.clusterDim.y = 1;
+          at[0].val.clusterDim.z = 1;
+          lc.attrs = at;
+          lc.numAttrs = 1;
+          const int passes = orth == DS_ORTH_CLASSICAL ? 1 : 2;
+          DS_CUDA(cudaLaunchKernelEx(&lc, arnoldi_orth_cluster_kernel<T>, n, V, ldv, (int)k, passes, H, Hraw, ldh, g,
+                                     cs, sn, est, st, tol, total_it, cap, gt));
+          count_launch(ctx);
+          continue;
+        }
         if (fused) {
           const size_t arn_smem = (size_t)kc * arn_per * sizeof(T);
           static bool arn_attr[2] = {false, false};
