@@ -203,30 +203,8 @@ __device__ __forceinline__ Ssq block_ssq(Ssq v, double* smem /* >= 64 doubles */
 }
 
 // ---------------------------------------------------------------------------
-// software grid barrier for cooperative launches (all CTAs co-resident).
-// bar[0] = arrival counter, bar[1] = generation.
+// software grid barrier for cooperative launches (all CTAs co-resident)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned int* vgen = bar + 1;
-    unsigned int gen = *vgen;
-    __threadfence();
-    unsigned int arrived = atomicAdd(bar, 1u);
-    if (arrived == nblocks - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*vgen == gen) {
-        __nanosleep(32);
-      }
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 // Monotonic grid barrier: the counter is zeroed before the launch; barrier #e
 // completes when the counter reaches e * nblocks.  Thread 0 of each CTA releases
 // the CTA's prior writes (fence + relaxed add) and acquires everyone else's.

@@ -65,11 +65,6 @@ struct PanelArgs {
   unsigned long long* trace;  // optional [grid][ncol][4] %globaltimer stamps (DENSOLVE_PANEL_TRACE)
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 
 constexpr int kPanelMaxW = 64;
 
@@ -169,35 +164,6 @@ struct LLVal<float> {
   __device__ static void put(uint64_t* p, float v, uint32_t f) { ll_store(p, __float_as_uint(v), f); }
   __device__ static float get(const uint64_t* w) { return __uint_as_float((uint32_t)w[0]); }
 };
-
-// First-max argmax over the CTA with one barrier: warp shuffle tree, one record per
-// warp in shared memory (double-buffered by the caller's slot so back-to-back calls
-// need no trailing barrier), then every thread reduces the warp records in the same
-// order => the identical result in all threads.
-__device__ __forceinline__ void cta_argmax(double& bv, int64_t& bi, double* wv, int64_t* wi) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-    const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (piv_better(ov, oi, bv, bi)) {
-      bv = ov;
-      bi = oi;
-    }
-  }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) {
-    wv[wid] = bv;
-    wi[wid] = bi;
-  }
-  __syncthreads();
-  bv = wv[0];
-  bi = wi[0];
-  for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
-    if (piv_better(wv[w], wi[w], bv, bi)) {
-      bv = wv[w];
-      bi = wi[w];
-    }
-}
 
 // First-max argmax over the CTA: keys are the IEEE bits of |v| (monotone for
 // v >= 0, NaN canonicalised above +inf so it wins like np.argmax), reduced with
