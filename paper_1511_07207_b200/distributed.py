@@ -507,7 +507,8 @@ def gmres_solve_sharded(A_blk, b_loc, x0_loc, n: int, cfg: SolverConfig, comm, o
 # 1-D block-cyclic LU  (direct.lu_factor_blocked, direct.py:50-84)
 # ---------------------------------------------------------------------------
 def outer_block(b: int, n: int) -> int:
-    """Same internal outer block as the single-GPU factorization (ds_lu.cu)."""
+    """Column-block width of the 1-D block-cyclic layout: 256 (b * floor(256/b)); narrower
+    than the single-GPU outer block (512) so 8 ranks still own 16 blocks each at n=32768."""
     if b >= 256 or b >= n:
         return min(b, n)
     return min(n, b * max(1, 256 // b))
@@ -516,7 +517,12 @@ def outer_block(b: int, n: int) -> int:
 def lu_factor_block_cyclic(W_loc, n: int, b: int, comm, ops, nb_outer: int | None = None):
     """Factor the block-cyclic matrix in place.  W_loc: (n_loc_cols, n) tensor =
     column-major n x n_loc_cols holding this rank's column blocks (block k at
-    local position (k // G) * NB).  Returns (pivots int64 tensor (n,), singular)."""
+    local position (k // G) * NB).  Returns (pivots int64 tensor (n,), singular).
+
+    Look-ahead: after receiving panel k, the owner of block k+1 first applies the
+    swaps and the update of step k to that block and factors it, and only then
+    updates its other blocks -- so panel k+1 is ready (and broadcast) while the
+    other ranks are still running their step-k trailing GEMMs."""
     import torch
 
     G, q = comm.size, comm.rank
@@ -527,19 +533,49 @@ def lu_factor_block_cyclic(W_loc, n: int, b: int, comm, ops, nb_outer: int | Non
     zero = torch.zeros(n, dtype=torch.int8, device=dev)
     mine = local_blocks(nblocks, q, G)
     lcol = {k: i * NB for i, k in enumerate(mine)}   # local column offset of block k
+
+    def factor_own(k):
+        """Owner of block k: factor its (already updated) panel; return (panel, pv, zf)."""
+        kb, bf = k * NB, min((k + 1) * NB, n)
+        w = bf - kb
+        c0 = lcol[k]
+        pv = torch.empty(w, dtype=torch.int64, device=dev)
+        zf = torch.zeros(w, dtype=torch.int8, device=dev)
+        ops.lu_panel(offset_view(W_loc, kb, c0), n, n - kb, w, b, pv, zf)  # pivots relative to row kb
+        pv += kb
+        panel = W_loc[c0:c0 + w, kb:].clone()  # column-major (n-kb) x w
+        return panel, pv, zf
+
+    def update_blocks(k, L00, blocks_):
+        """TRSM of the U block row + trailing GEMM of step k on the given local blocks
+        (contiguous ascending run)."""
+        if not blocks_:
+            return
+        kb, bf = k * NB, min((k + 1) * NB, n)
+        w = bf - kb
+        c0 = lcol[blocks_[0]]
+        cw = sum(min(NB, n - kk * NB) for kk in blocks_)
+        for ib in range(0, w, b):
+            ibf = min(ib + b, w)
+            ops.trsm_lower_unit(ibf - ib, cw, offset_view(L00, ib, ib), n - kb, offset_view(W_loc, kb + ib, c0), n)
+            if ibf < w:
+                ops.gemm_sub(w - ibf, cw, ibf - ib, offset_view(L00, ibf, ib), n - kb,
+                             offset_view(W_loc, kb + ib, c0), n, offset_view(W_loc, kb + ibf, c0), n)
+        if bf < n:
+            ops.gemm_sub(n - bf, cw, w, offset_view(L00, w, 0), n - kb, offset_view(W_loc, kb, c0), n,
+                         offset_view(W_loc, bf, c0), n)
+
+    ready = factor_own(0) if block_owner(0, G) == q else None
     for k in range(nblocks):
         kb, bf = k * NB, min((k + 1) * NB, n)
         w = bf - kb
         owner = block_owner(k, G)
-        panel = torch.empty((w, n - kb), dtype=W_loc.dtype, device=dev)  # column-major (n-kb) x w
-        pv = torch.empty(w, dtype=torch.int64, device=dev)
-        zf = torch.zeros(w, dtype=torch.int8, device=dev)
         if q == owner:
-            c0 = lcol[k]
-            Pview = offset_view(W_loc, kb, c0)
-            ops.lu_panel(Pview, n, n - kb, w, b, pv, zf)       # pivots relative to row kb
-            pv += kb
-            panel.copy_(W_loc[c0:c0 + w, kb:])
+            panel, pv, zf = ready
+        else:
+            panel = torch.empty((w, n - kb), dtype=W_loc.dtype, device=dev)
+            pv = torch.empty(w, dtype=torch.int64, device=dev)
+            zf = torch.zeros(w, dtype=torch.int8, device=dev)
         comm.broadcast(panel, owner)
         comm.broadcast(pv, owner)
         comm.broadcast(zf, owner)
@@ -549,26 +585,13 @@ def lu_factor_block_cyclic(W_loc, n: int, b: int, comm, ops, nb_outer: int | Non
         for kk in mine:
             if kk == k:
                 continue
-            c0 = lcol[kk]
-            cw = min(NB, n - kk * NB)
-            ops.laswp(offset_view(W_loc, 0, c0), n, cw, kb, bf, piv)
-        # TRSM + trailing GEMM on local blocks to the right
+            ops.laswp(offset_view(W_loc, 0, lcol[kk]), n, min(NB, n - kk * NB), kb, bf, piv)
         right = [kk for kk in mine if kk > k]
-        if not right:
-            continue
-        c0 = lcol[right[0]]
-        cw = sum(min(NB, n - kk * NB) for kk in right)
-        # local right blocks are contiguous in W_loc (ascending k)
-        U = offset_view(W_loc, kb, c0)
-        L00 = panel  # rows kb..bf of the panel = first w rows (ld = n - kb)
-        for ib in range(0, w, b):
-            ibf = min(ib + b, w)
-            ops.trsm_lower_unit(ibf - ib, cw, offset_view(L00, ib, ib), n - kb, offset_view(W_loc, kb + ib, c0), n)
-            if ibf < w:
-                ops.gemm_sub(w - ibf, cw, ibf - ib, offset_view(L00, ibf, ib), n - kb,
-                             offset_view(W_loc, kb + ib, c0), n, offset_view(W_loc, kb + ibf, c0), n)
-        if bf < n:
-            ops.gemm_sub(n - bf, cw, w, offset_view(L00, w, 0), n - kb, U, n, offset_view(W_loc, bf, c0), n)
+        if k + 1 < nblocks and block_owner(k + 1, G) == q:
+            update_blocks(k, panel, [k + 1])  # look-ahead block first
+            ready = factor_own(k + 1)
+            right = [kk for kk in right if kk != k + 1]
+        update_blocks(k, panel, right)
     return piv, bool(zero.any().item())
 
 
@@ -720,6 +743,7 @@ def bench_sharded_cg(args, torch, dev, be):
     e2e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
     dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
+    lu = bench_block_cyclic_lu(args, torch, dev, comm, ops) if not getattr(args, "only_cg", False) else None
     if q == 0:
         value = iters * args.steps / (ms / 1e3)
         unit = f"CG iters/s (n={n} fp64)"
@@ -741,4 +765,50 @@ def bench_sharded_cg(args, torch, dev, be):
                     "h2d_bytes_per_step": int(G * (A_h.numel() + 2 * n_loc) * 8),
                     "d2h_bytes_per_step": int(G * n_loc * 8), "ms_per_step": e2e_ms / args.steps},
             "gpu_launches": launches, "clocks": clk.summary(),
+            "components": {"lu_block_cyclic": lu} if lu else {},
             "timing": "max over ranks of CUDA-event time"}), flush=True)
+
+
+def bench_block_cyclic_lu(args, torch, dev, comm, ops):
+    """1-D block-cyclic LU (b=64, NB-wide column blocks dealt round-robin) of a uniform
+    U[-1,1] n x n matrix (every column block seeded by its index, so the matrix does not
+    depend on N); GFLOP/s of 2n^3/3, max over ranks of the CUDA-event time."""
+    import torch.distributed as dist
+
+    n, b = args.lu_n5, 64
+    G, q = comm.size, comm.rank
+    NB = outer_block(b, n)
+    blocks = local_blocks(-(-n // NB), q, G)
+    ncols = sum(min(NB, n - k * NB) for k in blocks)
+
+    def make():
+        W = torch.empty((ncols, n), dtype=torch.float64, device=dev)
+        c0 = 0
+        for k in blocks:
+            w = min(NB, n - k * NB)
+            g = torch.Generator(device=dev)
+            g.manual_seed(1000 + k)
+            W[c0:c0 + w] = torch.rand((w, n), dtype=torch.float64, device=dev, generator=g).mul_(2.0).sub_(1.0)
+            c0 += w
+        return W
+
+    W = make()
+    lu_factor_block_cyclic(W, n, b, comm, ops)  # warm-up
+    W = make()
+    torch.cuda.synchronize()
+    comm.barrier()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    piv, sing = lu_factor_block_cyclic(W, n, b, comm, ops)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    tf = 2.0 * n ** 3 / 3.0 / (ms / 1e3) / 1e12
+    del W
+    torch.cuda.empty_cache()
+    return {"workload": f"1-D block-cyclic LU b=64 (NB={NB} column blocks) uniform U[-1,1] n={n} fp64 over {G} GPUs",
+            "value": round(tf * 1e3, 1), "unit": "GFLOP/s", "ms": round(ms, 2), "singular": sing,
+            "fp64_peak_tflops_per_gpu": 37.1, "frac_of_aggregate_fp64_peak": round(tf / (37.1 * G), 4)}
