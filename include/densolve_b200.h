@@ -181,6 +181,15 @@ int ds_lu_factor(ds_ctx* ctx, int dtype, int64_t n, void* d_A, int64_t lda, int6
 int ds_lu_factor_dev(ds_ctx* ctx, int dtype, int64_t n, void* d_A, int64_t lda, int64_t nb,
                      int64_t* d_piv, int32_t* h_singular);
 
+/* Asynchronous staging (pipelining solves): column-major host (ld_host) -> device
+ * (ld_dev) copy on the context's copy stream; *event_out is an opaque event that
+ * ds_wait_event makes the context stream wait on (destroy with ds_event_destroy).
+ * The destination must not be in use by pending work. */
+int ds_upload_async(ds_ctx* ctx, int dtype, const void* h_src, int64_t rows, int64_t cols, int64_t ld_host,
+                    void* d_dst, int64_t ld_dev, void** event_out);
+int ds_wait_event(ds_ctx* ctx, void* event);
+int ds_event_destroy(void* event);
+
 /* ---- multi-GPU: NCCL inside the library (row-sharded Krylov) - */
 /* A communicator over the ranks of a row-sharded solve.  Rank 0 creates the
  * id with ds_comm_unique_id, the caller distributes the DS_COMM_ID_BYTES bytes

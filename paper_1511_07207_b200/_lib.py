@@ -96,6 +96,10 @@ _SIGNATURES = {
                              c_void_p, POINTER(c_int32)]),
     "ds_lu_factor_dev": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_int64,
                                  c_void_p, POINTER(c_int32)]),
+    "ds_upload_async": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64,
+                                POINTER(c_void_p)]),
+    "ds_wait_event": (c_int, [c_void_p, c_void_p]),
+    "ds_event_destroy": (c_int, [c_void_p]),
     "ds_comm_unique_id": (c_int, [c_void_p]),
     "ds_comm_create": (c_int, [c_void_p, c_int, c_int, c_void_p, POINTER(c_void_p)]),
     "ds_comm_destroy": (c_int, [c_void_p]),

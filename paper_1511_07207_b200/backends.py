@@ -113,6 +113,18 @@ class B200Backend(Backend):
         out = tuple(to_device(a, self.ctx) for a in arrays)
         return out if len(out) != 1 else out[0]
 
+    def stage_in_async(self, *arrays, out=None):
+        """Asynchronous stage_in: copies on the context's copy stream (pinned host arrays
+        overlap a running solve); a solver consuming the handles waits for the copies.
+        ``out`` reuses existing DeviceArrays (e.g. double buffers) instead of allocating."""
+        if out is None:
+            out = tuple(DeviceArray(self.ctx, np.asarray(a).shape, np.asarray(a).dtype) for a in arrays)
+        elif isinstance(out, DeviceArray):
+            out = (out,)
+        for d, a in zip(out, arrays):
+            d.upload_async(a)
+        return out if len(out) != 1 else out[0]
+
     def stage_out(self, *arrays):
         out = tuple(a.to_host() if is_device(a) else a for a in arrays)
         return out if len(out) != 1 else out[0]

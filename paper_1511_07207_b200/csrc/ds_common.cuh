@@ -264,6 +264,7 @@ struct ds_ctx {
   // LU look-ahead: a high-priority side stream for the next panel's factorization
   cudaStream_t side = nullptr;
   cudaStream_t aux = nullptr;  // low-priority stream for the swaps of already-factored L columns
+  cudaStream_t copy = nullptr;  // asynchronous host->device staging (ds_upload_async)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
   unsigned panel_seq = 0;  // LU panel launches (epochs of the LL exchange words)
 };

@@ -143,6 +143,7 @@ int ds_ctx_destroy(ds_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->copy) cudaStreamDestroy(ctx->copy);
   if (ctx->hbuf) cudaFreeHost(ctx->hbuf);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->side) cudaStreamDestroy(ctx->side);
@@ -248,6 +249,40 @@ int ds_memset(ds_ctx* ctx, void* dst, int value, size_t bytes) {
   DS_TRY(ctx_begin(ctx));
   if (bytes == 0) return DS_OK;
   DS_CUDA(cudaMemsetAsync(dst, value, bytes, ctx->stream));
+  return DS_OK;
+}
+
+// Asynchronous staging on the context's copy stream (created on first use): the upload
+// of the next solve's operands overlaps the current solve.  The caller guarantees the
+// destination is not in use by pending work; ds_wait_event orders a later solve after it.
+int ds_upload_async(ds_ctx* ctx, int dtype, const void* src, int64_t rows, int64_t cols, int64_t ld_host,
+                    void* dst, int64_t ld_dev, void** event_out) {
+  DS_TRY(ctx_begin(ctx));
+  *event_out = nullptr;
+  if (rows < 0 || cols < 0 || ld_dev < (rows > 0 ? rows : 1) || ld_host < (rows > 0 ? rows : 1)) {
+    set_error("upload_async: bad shape %lld x %lld", (long long)rows, (long long)cols);
+    return DS_EDIM;
+  }
+  if (!ctx->copy) DS_CUDA(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+  const size_t es = dtype_size(dtype);
+  if (rows > 0 && cols > 0)
+    DS_CUDA(cudaMemcpy2DAsync(dst, ld_dev * es, src, ld_host * es, rows * es, cols, cudaMemcpyHostToDevice,
+                              ctx->copy));
+  cudaEvent_t ev;
+  DS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  DS_CUDA(cudaEventRecord(ev, ctx->copy));
+  *event_out = (void*)ev;
+  return DS_OK;
+}
+
+int ds_wait_event(ds_ctx* ctx, void* event) {
+  DS_TRY(ctx_begin(ctx));
+  if (event) DS_CUDA(cudaStreamWaitEvent(ctx->stream, (cudaEvent_t)event, 0));
+  return DS_OK;
+}
+
+int ds_event_destroy(void* event) {
+  if (event) cudaEventDestroy((cudaEvent_t)event);
   return DS_OK;
 }
 

@@ -30,7 +30,7 @@ def _padded_ld(rows: int) -> int:
 class DeviceArray:
     """A 1-d vector or 2-d column-major matrix in device memory."""
 
-    __slots__ = ("ctx", "shape", "dtype", "ld", "ptr", "_fin", "__weakref__")
+    __slots__ = ("ctx", "shape", "dtype", "ld", "ptr", "_fin", "_pending", "_src", "__weakref__")
 
     def __init__(self, ctx: _lib.Context, shape, dtype, ld: int | None = None):
         self.ctx = ctx
@@ -48,6 +48,8 @@ class DeviceArray:
         p = c_void_p()
         _lib.check(ctx.lib.ds_malloc(ctx.handle, max(nbytes, 16), ctypes.byref(p)))
         self.ptr = p.value
+        self._pending = None  # event of an in-flight asynchronous upload (upload_async)
+        self._src = None      # the host array it reads (kept alive until consumed)
         self._fin = weakref.finalize(self, ctx.lib.ds_free, ctx.handle, c_void_p(self.ptr))
 
     # -- numpy-like metadata used by the validators -------------------------------------
@@ -89,6 +91,7 @@ class DeviceArray:
         a = np.asarray(a)
         if a.shape != self.shape or a.dtype != self.dtype:
             raise core.DimensionError(f"upload of {a.shape}/{a.dtype} into {self.shape}/{self.dtype}")
+        self.settle()
         lib, h = self.ctx.lib, self.ctx.handle
         if self.ndim == 1:
             a = np.ascontiguousarray(a)
@@ -105,7 +108,32 @@ class DeviceArray:
         _lib.check(lib.ds_upload_matrix(h, self.dcode, a.ctypes.data_as(c_void_p), rows, cols,
                                         max(ld_host, 1), order, c_void_p(self.ptr), self.ld))
 
+    def upload_async(self, a):
+        """Stage a host array (F-order or 1-d; pinned for a true async copy) on the context's
+        copy stream; the next solver call on this array waits for it (pipelined solves)."""
+        a = np.asarray(a)
+        if a.shape != self.shape or a.dtype != self.dtype:
+            raise core.DimensionError(f"upload of {a.shape}/{a.dtype} into {self.shape}/{self.dtype}")
+        if self.ndim == 2 and not a.flags.f_contiguous:
+            raise ValueError("upload_async needs an F-order (column-major) host matrix")
+        self.settle()
+        rows, cols = (self.shape[0], 1) if self.ndim == 1 else self.shape
+        ev = c_void_p()
+        _lib.check(self.ctx.lib.ds_upload_async(self.ctx.handle, self.dcode, a.ctypes.data_as(c_void_p), rows, cols,
+                                                max(rows, 1), c_void_p(self.ptr), self.ld if self.ndim == 2
+                                                else max(rows, 1), ctypes.byref(ev)))
+        self._pending, self._src = ev, a
+        return self
+
+    def settle(self):
+        """Order the context stream after a pending asynchronous upload into this array."""
+        if self._pending is not None:
+            _lib.check(self.ctx.lib.ds_wait_event(self.ctx.handle, self._pending))
+            self.ctx.lib.ds_event_destroy(self._pending)
+            self._pending, self._src = None, None
+
     def to_host(self, out: np.ndarray | None = None) -> np.ndarray:
+        self.settle()
         lib, h = self.ctx.lib, self.ctx.handle
         if self.ndim == 1:
             if out is None:
@@ -121,6 +149,7 @@ class DeviceArray:
         return out
 
     def copy(self) -> "DeviceArray":
+        self.settle()
         out = DeviceArray(self.ctx, self.shape, self.dtype, ld=self.ld)
         _lib.check(self.ctx.lib.ds_memcpy_d2d(self.ctx.handle, c_void_p(out.ptr), c_void_p(self.ptr),
                                               self.nbytes))
@@ -136,6 +165,7 @@ def to_device(a, ctx: _lib.Context | None = None) -> DeviceArray:
     if isinstance(a, DeviceArray):
         if a.ctx is not ctx:
             raise ValueError("operand lives on another device context")
+        a.settle()
         return a
     return DeviceArray.from_host(a, ctx)
 

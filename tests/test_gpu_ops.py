@@ -201,3 +201,31 @@ def test_device_resident_chain(backend, rng):
     dy = backend.gemv(dA, dx)  # stays on device
     assert hasattr(dy, "ptr")
     np.testing.assert_allclose(backend.stage_out(dy), A @ x, rtol=1e-12, atol=1e-12)
+
+
+def test_stage_in_async_pipelined_solves(backend):
+    # two device buffer sets, the next upload in flight while the current solve runs
+    from paper_1511_07207_b200 import SolverConfig, cg_solve, pinned_empty
+    from paper_1511_07207_b200.device import DeviceArray
+    from paper_1511_07207_b200.harness import ProblemSpec, generate_problem
+    outs = []
+    probs = [generate_problem(ProblemSpec(kind="spd", n=300, seed=s)) for s in range(4)]
+    pinned = []
+    for A, b, _ in probs:
+        Ap = pinned_empty(A.shape, A.dtype)
+        Ap[...] = A
+        bp = pinned_empty(b.shape, b.dtype)
+        bp[...] = b
+        pinned.append((Ap, bp, np.zeros_like(b)))
+    ctx = backend.ctx
+    bufs = [(DeviceArray(ctx, (300, 300), np.float64), DeviceArray(ctx, (300,), np.float64),
+             DeviceArray(ctx, (300,), np.float64)) for _ in range(2)]
+    backend.stage_in_async(*pinned[0], out=bufs[0])
+    for s in range(4):
+        if s + 1 < 4:
+            backend.stage_in_async(*pinned[s + 1], out=bufs[(s + 1) % 2])
+        x, rep = cg_solve(*bufs[s % 2], SolverConfig(tolerance=1e-10), backend)
+        outs.append(x.to_host())
+    for (A, b, _), x in zip(probs, outs):
+        xs, _ = cg_solve(A, b, np.zeros_like(b), SolverConfig(tolerance=1e-10), backend)
+        np.testing.assert_array_equal(x, xs)
