@@ -656,159 +656,3 @@ def spd_block_device(n: int, r0: int, r1: int, torch, device, seed: int = 0):
         v = torch.where(i == j, v + 1.5 * math.sqrt(n), v)
         out[c0:c0 + cols.numel()] = v
     return out
-
-
-def bench_sharded_cg(args, torch, dev, be):
-    """`bench.py --gpus N` under torchrun: C4 CG row-sharded over N GPUs (strong scaling).
-    Same JSON contract as the 1-GPU line: device-resident `value` (max over ranks of the
-    CUDA-event time), `e2e` (each rank uploads its row block of A, b, x0 from pinned host
-    memory and downloads its x shard every step), the per-rank GEMV `roofline`, clocks."""
-    import json
-    import torch.distributed as dist
-
-    from bench import BASELINE_METRIC, ClockSampler, _peaks  # noqa: E402  (repo root on sys.path)
-
-    comm = TorchComm()
-    ops = CudaShardOps(be.ctx)
-    ops.bind_current_stream()
-    stream = torch.cuda.current_stream()
-    n, iters = args.n, args.iters
-    G, q = comm.size, comm.rank
-    n_loc, N = row_partition(n, G)
-    r0, r1 = q * n_loc, min(n, (q + 1) * n_loc)
-    A_blk = torch.zeros((n, n_loc), dtype=torch.float64, device=dev)
-    if r1 > r0:
-        A_blk[:, : r1 - r0] = spd_block_device(n, r0, r1, torch, dev)
-    b = torch.zeros(n_loc, dtype=torch.float64, device=dev)
-    b[: r1 - r0] = 1.0
-    x0 = torch.zeros(n_loc, dtype=torch.float64, device=dev)
-    cfg = SolverConfig(tolerance=1e-300, max_iterations=iters)
-    for _ in range(args.warmup):
-        cg_solve_sharded(A_blk, b, x0, n, cfg, comm, ops)
-    torch.cuda.synchronize()
-    comm.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    l0 = be.ctx.launches()
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            x, rep = cg_solve_sharded(A_blk, b, x0, n, cfg, comm, ops)
-        e1.record(stream)
-        torch.cuda.synchronize()
-    comm.barrier()
-    launches = be.ctx.launches() - l0
-    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
-
-    # per-rank GEMV roofline: the local n x n_loc block streamed once (8 (n n_loc + n + n_loc) B)
-    full = torch.zeros(N, dtype=torch.float64, device=dev)
-    y = torch.empty(n_loc, dtype=torch.float64, device=dev)
-    for _ in range(3):
-        ops.gemv(A_blk, n_loc, n_loc, n, full, y)
-    torch.cuda.synchronize()
-    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    g0.record(stream)
-    for _ in range(20):
-        ops.gemv(A_blk, n_loc, n_loc, n, full, y)
-    g1.record(stream)
-    torch.cuda.synchronize()
-    gemv_ms = torch.tensor([g0.elapsed_time(g1) / 20], dtype=torch.float64, device=dev)
-    dist.all_reduce(gemv_ms, op=dist.ReduceOp.MAX)
-    gemv_ms = float(gemv_ms.item())
-    hbm_peak, peak_src = _peaks()
-    gbytes = 8.0 * (n * n_loc + n + n_loc)
-    achieved = gbytes / (gemv_ms / 1e3) / 1e9
-
-    # end to end: pinned host shards -> device -> solve -> x shard back, every step
-    A_h = torch.empty((n, n_loc), dtype=torch.float64, pin_memory=True)
-    A_h.copy_(A_blk)
-    b_h = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
-    b_h.copy_(b)
-    x0_h = torch.zeros(n_loc, dtype=torch.float64, pin_memory=True)
-    x_h = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
-    torch.cuda.synchronize()
-    comm.barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    for _ in range(args.steps):
-        A_blk.copy_(A_h, non_blocking=True)
-        b.copy_(b_h, non_blocking=True)
-        x0.copy_(x0_h, non_blocking=True)
-        x, rep = cg_solve_sharded(A_blk, b, x0, n, cfg, comm, ops)
-        x_h.copy_(x, non_blocking=True)
-    f1.record(stream)
-    torch.cuda.synchronize()
-    comm.barrier()
-    e2e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
-    dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_ms = float(e2e_ms.item())
-    lu = bench_block_cyclic_lu(args, torch, dev, comm, ops) if not getattr(args, "only_cg", False) else None
-    if q == 0:
-        value = iters * args.steps / (ms / 1e3)
-        unit = f"CG iters/s (n={n} fp64)"
-        print(json.dumps({
-            "metric": BASELINE_METRIC, "value": round(value, 3), "unit": unit, "n_gpus": G, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (hash-generated symmetric A = S + 1.5 sqrt(n) I, row blocks generated per rank)",
-            "config": {"workload": f"C4: CG dense SPD n={n} fp64 row-sharded over {G} GPUs, {iters} iterations/step",
-                       "n": n, "iters_per_step": iters, "parallelism": f"rows{G}",
-                       "l2_policy": "inputs larger than L2"},
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                         "frac": round(achieved / hbm_peak, 4), "traffic": None,
-                         "kernel": "per-rank ds_gemv on the n x n_loc block (max over ranks)",
-                         "algorithmic_bytes_per_launch": gbytes, "avg_launch_ms": round(gemv_ms, 4),
-                         "peak_source": peak_src},
-            "cpu_baseline": None,
-            "e2e": {"value": iters * args.steps / (e2e_ms / 1e3), "unit": unit,
-                    "h2d_bytes_per_step": int(G * (A_h.numel() + 2 * n_loc) * 8),
-                    "d2h_bytes_per_step": int(G * n_loc * 8), "ms_per_step": e2e_ms / args.steps},
-            "gpu_launches": launches, "clocks": clk.summary(),
-            "components": {"lu_block_cyclic": lu} if lu else {},
-            "timing": "max over ranks of CUDA-event time"}), flush=True)
-
-
-def bench_block_cyclic_lu(args, torch, dev, comm, ops):
-    """1-D block-cyclic LU (b=64, NB-wide column blocks dealt round-robin) of a uniform
-    U[-1,1] n x n matrix (every column block seeded by its index, so the matrix does not
-    depend on N); GFLOP/s of 2n^3/3, max over ranks of the CUDA-event time."""
-    import torch.distributed as dist
-
-    n, b = args.lu_n5, 64
-    G, q = comm.size, comm.rank
-    NB = outer_block(b, n)
-    blocks = local_blocks(-(-n // NB), q, G)
-    ncols = sum(min(NB, n - k * NB) for k in blocks)
-
-    def make():
-        W = torch.empty((ncols, n), dtype=torch.float64, device=dev)
-        c0 = 0
-        for k in blocks:
-            w = min(NB, n - k * NB)
-            g = torch.Generator(device=dev)
-            g.manual_seed(1000 + k)
-            W[c0:c0 + w] = torch.rand((w, n), dtype=torch.float64, device=dev, generator=g).mul_(2.0).sub_(1.0)
-            c0 += w
-        return W
-
-    W = make()
-    lu_factor_block_cyclic(W, n, b, comm, ops)  # warm-up
-    W = make()
-    torch.cuda.synchronize()
-    comm.barrier()
-    stream = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    piv, sing = lu_factor_block_cyclic(W, n, b, comm, ops)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
-    tf = 2.0 * n ** 3 / 3.0 / (ms / 1e3) / 1e12
-    del W
-    torch.cuda.empty_cache()
-    return {"workload": f"1-D block-cyclic LU b=64 (NB={NB} column blocks) uniform U[-1,1] n={n} fp64 over {G} GPUs",
-            "value": round(tf * 1e3, 1), "unit": "GFLOP/s", "ms": round(ms, 2), "singular": sing,
-            "fp64_peak_tflops_per_gpu": 37.1, "frac_of_aggregate_fp64_peak": round(tf / (37.1 * G), 4)}
