@@ -348,7 +348,7 @@ def run_b200(args):
 
     cpu = None
     if not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(n, min(iters, 50))  # ~15-20 s of host work
+        cpu = cpu_baseline_sample(n, min(iters, 30))  # ~15-25 s of host work
 
     line = {"metric": BASELINE_METRIC, "value": round(value, 3), "unit": f"CG iters/s (n={n} fp64)",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
