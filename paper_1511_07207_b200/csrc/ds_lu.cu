@@ -62,6 +62,7 @@ struct PanelArgs {
   uint64_t* ll_row;    // smem kernel: [2][grid][kPanelMaxW * words/value] LL candidate rows
   uint64_t* ll_diag;   // smem kernel: [2][kPanelMaxW * words/value] LL row i
   unsigned seq;        // per-context panel launch counter (LL epochs)
+  int backoff;         // poller kernel: __nanosleep between failed LL polls (0 = spin)
   unsigned long long* trace;  // optional [grid][ncol][4] %globaltimer stamps (DENSOLVE_PANEL_TRACE)
 };
 
@@ -381,6 +382,7 @@ __global__ void __launch_bounds__(kPanelRegThreads, 1) lu_panel_smem_kernel(T* _
     const long long t_f = clock64();
     const T aii = prow[c];
     const bool zero = aii == T(0);
+    long long t_f1 = 0, t_f2 = 0, t_f3 = 0;
     if (zero && blockIdx.x == 0 && t == 0) a.zero_cols[i] = 1;  // direct.py:71-74
     // retired columns j < c of rows i and p: one column per thread
     if (p != i)
@@ -403,6 +405,7 @@ __global__ void __launch_bounds__(kPanelRegThreads, 1) lu_panel_smem_kernel(T* _
     }
     l = __shfl_sync(0xffffffffu, l, lead_lane);
     if (lead) Ls[c * ldt + r] = y[0];  // retire column c
+    if (a.trace) t_f1 = clock64();
     unsigned long long bk = 0ull;
     int64_t bi = INT64_MAX;
     if (c + 1 < ncol) {
@@ -423,6 +426,7 @@ __global__ void __launch_bounds__(kPanelRegThreads, 1) lu_panel_smem_kernel(T* _
       cand_k = bk;
       cand_i = bi;
     }
+    if (a.trace) t_f2 = clock64();
     // ---- rest of the rank-1 update of my slice (direct.py:75-79), then rotate by one
     if (act) {
 #pragma unroll
@@ -437,6 +441,7 @@ __global__ void __launch_bounds__(kPanelRegThreads, 1) lu_panel_smem_kernel(T* _
       for (int k = 0; k + 1 < PW; ++k) y[k] = y[k + 1];
       y[PW - 1] = q == TPR - 1 ? T(0) : carry;
     }
+    if (a.trace) t_f3 = clock64();
     if (c + 1 < ncol) publish_rows(c + 1, bi);
     if (a.trace && t == 0) {
       const long long t_g = clock64();
@@ -444,11 +449,376 @@ __global__ void __launch_bounds__(kPanelRegThreads, 1) lu_panel_smem_kernel(T* _
       tr[2] += t_d - t_c;  // header poll
       tr[3] += t_e - t_d;  // argmax of the headers
       tr[4] += t_f - t_e;  // row poll + barrier
-      tr[5] += t_g - t_f;  // swap, scale, next candidate, update, rotate, publish
+      tr[0] += t_f1 - t_f;  // swap, scale
+      tr[1] += t_f2 - t_f1;  // next column's CTA argmax + header publish
+      tr[5] += t_f3 - t_f2;  // rank-1 update, rotate
+      tr[6] += t_g - t_f3;   // publish rows
     }
   }
   __syncthreads();
   for (int idx = t; idx < ncol * nr; idx += nt) {
+    const int j = idx / nr, rr = idx % nr;
+    W[(my_lo + rr) + (a.kb + j) * a.ld] = Ls[j * ldt + rr];
+  }
+}
+
+// Poller-warp panel (default for <= 224 rows per CTA): warp 0 of every CTA is a
+// dedicated exchange warp with no rows; warps 1..7 hold one row per thread (the
+// whole 64-column row rotated in registers).  Per column the row warps meet
+// ONCE (the CTA argmax of the next column's candidate); right after it the
+// candidate's owner publishes the header (signed value + row) and the candidate
+// row and row i+1 as LL words, BEFORE the rank-1 update of the column: the rows
+// go out with that update still pending, and the poller applies it to the two
+// received rows (same mul/sub, same order: bitwise what the owner would have
+// computed).  So the G-wide exchange latency overlaps the update.  The poller
+// polls the headers, reduces them with warp REDUX, computes the reciprocal of
+// the pivot while the row poll is in flight, fills CTA-shared, column-parity
+// double-buffered row copies and hands them to the row warps through an
+// mbarrier.  Same arithmetic and pivots as lu_panel_smem_kernel (bitwise the
+// reference, direct.py:59-79).
+__device__ __forceinline__ void warp_argmax_key(unsigned long long& key, int64_t& idx) {
+  const unsigned hi = (unsigned)(key >> 32);
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned lo = hi == mhi ? (unsigned)key : 0u;
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, lo);
+  const bool top = hi == mhi && (unsigned)key == mlo;
+  const unsigned widx = __reduce_min_sync(0xffffffffu, top ? (unsigned)min(idx, (int64_t)0xffffffff) : 0xffffffffu);
+  key = ((unsigned long long)mhi << 32) | mlo;
+  idx = widx == 0xffffffffu ? INT64_MAX : (int64_t)widx;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @!P1 bra WAIT_%=;\n}\n" ::"r"(
+          (unsigned)__cvta_generic_to_shared(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+constexpr int kPanelWarpThreads = 256;              // 1 poller warp + 7 row warps
+constexpr int kPanelWarpRows = kPanelWarpThreads - 32;
+constexpr int kRot = kPanelMaxW + 2;                // rotated row copies, zero padded
+
+template <typename T>
+__global__ void __launch_bounds__(kPanelWarpThreads, 1) lu_panel_warp_kernel(T* __restrict__ W, PanelArgs a) {
+  constexpr int PW = kPanelMaxW;
+  constexpr int VW = LLVal<T>::W;
+  constexpr int NW = kPanelWarpThreads / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Ls = reinterpret_cast<T*>(smem_raw);  // [ncol][ldt]: retired columns
+  __shared__ unsigned long long wk[2][NW];
+  __shared__ int64_t wi[2][NW];
+  __shared__ __align__(16) T pabs[2][kPanelMaxW];  // [column parity]: pivot row, column order
+  __shared__ __align__(16) T dabs[2][kPanelMaxW];  // row i before the swap, column order
+  __shared__ __align__(16) T prot[2][kRot];        // prot[k] = pivot row[c + k], zero padded
+  __shared__ __align__(16) T drot[2][kRot];        // drot[k] = row i[c + k]
+  __shared__ __align__(16) T wstage[NW][2][2 * kPanelMaxW];  // per row warp: rows being published
+  __shared__ int64_t s_piv[2];
+  __shared__ T s_rcp[2];
+  __shared__ __align__(8) uint64_t s_bar;  // poller -> row warps, one phase per column
+  const unsigned G = gridDim.x;
+  const int per = a.per, ldt = a.ldt;
+  const int64_t my_lo = a.kb + (int64_t)blockIdx.x * per;
+  const int64_t my_hi = min(a.n, my_lo + per);
+  const int nr = (int)(my_hi - my_lo);
+  const int ncol = (int)(a.bf - a.kb);
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const bool poller = wid == 0;
+  const int r = t - 32;  // my row (row warps)
+  const bool mine = r >= 0 && r < nr;
+  const int64_t g = my_lo + r;
+  uint64_t* hdr = a.ll_hdr;    // [2][G][kHdrWords]
+  uint64_t* rows = a.ll_row;   // [2][G][kPanelMaxW * VW]
+  uint64_t* diag = a.ll_diag;  // [2][kPanelMaxW * VW]
+  const int RW = kPanelMaxW * VW;
+  if (t == 0) mbar_init(&s_bar, 1);
+
+  __syncthreads();  // mbarrier initialised
+  if (poller) {
+    // ======== exchange warp
+    {
+      unsigned long long ck = 0ull;
+      int64_t ci = INT64_MAX;
+      cta_argmax_key(ck, ci, wk[0], wi[0]);
+    }
+    bool prev_zero = false;  // column c - 1 had a zero pivot (its update was skipped)
+    for (int c = 0; c < ncol; ++c) {
+      const int64_t i = a.kb + c;
+      const int par = c & 1;
+      const uint32_t ep = a.seq * 128u + (uint32_t)c + 1u;
+      const long long t_c = a.trace ? clock64() : 0;
+      // ---- pivot: poll the G headers, reduce (first max, ties -> lowest row)
+      unsigned long long gk = 0ull;
+      int64_t gi = INT64_MAX;
+      double gv = 0.0;
+      {
+        // up to kHdrPerLane headers per lane, all loads in flight at once; re-poll the
+        // ones not yet published
+        constexpr int kHdrPerLane = 5;  // G <= 160
+        uint64_t x[kHdrPerLane][3];
+        unsigned pending = 0;
+#pragma unroll
+        for (int s2 = 0; s2 < kHdrPerLane; ++s2)
+          if (lane + 32 * s2 < (int)G) pending |= 1u << s2;
+        while (pending) {
+#pragma unroll
+          for (int s2 = 0; s2 < kHdrPerLane; ++s2)
+            if (pending >> s2 & 1u) {
+              const uint64_t* h = hdr + ((size_t)par * G + lane + 32 * s2) * kHdrWords;
+              x[s2][0] = ll_load(h);
+              x[s2][1] = ll_load(h + 1);
+              x[s2][2] = ll_load(h + 2);
+            }
+#pragma unroll
+          for (int s2 = 0; s2 < kHdrPerLane; ++s2)
+            if ((pending >> s2 & 1u) && ll_ok(x[s2][0], ep) && ll_ok(x[s2][1], ep) && ll_ok(x[s2][2], ep))
+              pending &= ~(1u << s2);
+          if (pending && a.backoff) __nanosleep(a.backoff);
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < kHdrPerLane; ++s2)
+          if (lane + 32 * s2 < (int)G) {
+            const double v = __longlong_as_double((long long)((x[s2][0] & 0xffffffffull) | (x[s2][1] << 32)));
+            const int64_t i2 = (uint32_t)x[s2][2] == 0xffffffffu ? INT64_MAX : (int64_t)(uint32_t)x[s2][2];
+            const unsigned long long k2 = i2 == INT64_MAX ? 0ull : piv_key(fabs(v));
+            if (k2 > gk || (k2 == gk && i2 < gi)) {
+              gk = k2;
+              gi = i2;
+              gv = v;
+            }
+          }
+      }
+      const unsigned long long mk = gk;
+      const int64_t mi = gi;
+      warp_argmax_key(gk, gi);
+      const unsigned src = __ballot_sync(0xffffffffu, mk == gk && mi == gi);
+      gv = __shfl_sync(0xffffffffu, gv, src ? __ffs(src) - 1 : 0);
+      const long long t_d = a.trace ? clock64() : 0;
+      const int64_t p = gi == INT64_MAX ? i : gi;
+      const int win = gi == INT64_MAX ? -1 : (int)((gi - a.kb) / per);
+      // ---- the winner's row and row i; column c - 1's pending update applied here
+      const uint64_t* prow_ll = rows + ((size_t)par * G + (win < 0 ? 0 : win)) * RW;
+      const uint64_t* drow_ll = diag + (size_t)par * RW;
+      T rcp = div_rn(T(1), (T)gv);  // overlaps the row poll
+      const T* pprev = pabs[par ^ 1];  // column c - 1's pivot row
+      T pv[2], dv[2];  // columns lane and lane + 32
+      {
+        uint64_t pw[2][VW], dw[2][VW];
+        unsigned pending = (lane < ncol ? 1u : 0u) | (lane + 32 < ncol ? 2u : 0u);
+        while (pending) {
+#pragma unroll
+          for (int s2 = 0; s2 < 2; ++s2)
+            if (pending >> s2 & 1u) {
+              const int j = lane + 32 * s2;
+#pragma unroll
+              for (int qq = 0; qq < VW; ++qq) {
+                pw[s2][qq] = win < 0 ? ((uint64_t)ep << 32) : ll_load(prow_ll + j * VW + qq);
+                dw[s2][qq] = ll_load(drow_ll + j * VW + qq);
+              }
+            }
+#pragma unroll
+          for (int s2 = 0; s2 < 2; ++s2)
+            if (pending >> s2 & 1u) {
+              bool ok = true;
+#pragma unroll
+              for (int qq = 0; qq < VW; ++qq) ok = ok && ll_ok(pw[s2][qq], ep) && ll_ok(dw[s2][qq], ep);
+              if (ok) pending &= ~(1u << s2);
+            }
+          if (pending && a.backoff) __nanosleep(a.backoff);
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) {
+          dv[s2] = LLVal<T>::get(dw[s2]);
+          pv[s2] = win < 0 ? dv[s2] : LLVal<T>::get(pw[s2]);
+        }
+      }
+      if (c > 0 && !prev_zero) {
+        // the owners published before column c - 1's update: v -= l * u for columns > c,
+        // l = the row's own column c - 1 (its multiplier), u = column c - 1's pivot row
+        const int jl = c - 1;
+        const T lp = __shfl_sync(0xffffffffu, jl < 32 ? pv[0] : pv[1], jl & 31);
+        const T ld_ = __shfl_sync(0xffffffffu, jl < 32 ? dv[0] : dv[1], jl & 31);
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) {
+          const int j = lane + 32 * s2;
+          if (j > c && j < ncol) {
+            const T up = pprev[j];
+            dv[s2] = sub_rn(dv[s2], mul_rn(ld_, up));
+            pv[s2] = win < 0 ? dv[s2] : sub_rn(pv[s2], mul_rn(lp, up));
+          }
+        }
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2) {
+        const int j = lane + 32 * s2;
+        if (j < ncol) {
+          pabs[par][j] = pv[s2];
+          dabs[par][j] = dv[s2];
+          if (j >= c) {
+            prot[par][j - c] = pv[s2];
+            drot[par][j - c] = dv[s2];
+          }
+        }
+      }
+      for (int k = ncol - c + lane; k < kRot; k += 32) {  // zero pad past the panel
+        prot[par][k] = T(0);
+        drot[par][k] = T(0);
+      }
+      __syncwarp();
+      const T aii = prot[par][0];
+      if (gi == INT64_MAX) rcp = div_rn(T(1), aii);
+      prev_zero = aii == T(0);
+      if (lane == 0) {
+        s_piv[par] = p;
+        s_rcp[par] = rcp;
+        if (blockIdx.x == 0) {
+          a.piv[i] = p;                         // piv[i] = v (direct.py:67)
+          if (prev_zero) a.zero_cols[i] = 1;    // direct.py:71-74
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_bar);
+      if (a.trace && t == 0) {
+        unsigned long long* tr = a.trace + (size_t)blockIdx.x * 8;
+        tr[2] += t_d - t_c;         // header poll + reduce
+        tr[4] += clock64() - t_d;   // row poll + handoff
+      }
+      if (c + 1 < ncol) {
+        unsigned long long ck = 0ull;
+        int64_t ci = INT64_MAX;
+        cta_argmax_key(ck, ci, wk[(c + 1) & 1], wi[(c + 1) & 1]);
+      }
+    }
+  } else {
+    // ======== row warps
+    T y[PW];  // y[k] = current value of panel column c + k of my row
+#pragma unroll
+    for (int k = 0; k < PW; ++k) y[k] = (mine && k < ncol) ? W[g + (a.kb + k) * a.ld] : T(0);
+    // column cc's CTA candidate ci and row kb + cc go out as LL words.  y[0] holds
+    // column `base` (cc == base: current rows; cc == base + 1: the candidate's
+    // column cc is current, columns > cc still miss column base's update).
+    auto publish = [&](int cc, int base, int64_t ci) {
+      const int par = cc & 1;
+      const uint32_t ep = a.seq * 128u + (uint32_t)cc + 1u;
+      const int64_t ii = a.kb + cc;
+      const bool has_c = ci != INT64_MAX;
+      const bool has_d = ii >= my_lo && ii < my_hi;
+      const int cw = has_c ? 1 + ((int)(ci - my_lo) >> 5) : -1;
+      const int dw = has_d ? 1 + ((int)(ii - my_lo) >> 5) : -1;
+      if (has_c ? (mine && g == ci) : t == 32) {
+        uint64_t* h = hdr + ((size_t)par * G + blockIdx.x) * kHdrWords;
+        const T hv = cc == base ? y[0] : y[1];
+        const unsigned long long b = (unsigned long long)__double_as_longlong(has_c ? (double)hv : 0.0);
+        ll_store(h, (uint32_t)b, ep);
+        ll_store(h + 1, (uint32_t)(b >> 32), ep);
+        ll_store(h + 2, has_c ? (uint32_t)ci : 0xffffffffu, ep);
+      }
+      if (wid == cw || wid == dw) {
+        if (mine && (g == ci || g == ii)) {  // y[k] -> slot base + k (slots < cc are not read)
+          T* st = wstage[wid][g == ci ? 0 : 1] + base;
+#pragma unroll
+          for (int k = 0; k < PW; ++k) st[k] = y[k];
+          if (g == ci && g == ii) {
+            T* st2 = wstage[wid][1] + base;
+#pragma unroll
+            for (int k = 0; k < PW; ++k) st2[k] = y[k];
+          }
+        }
+        __syncwarp();
+        for (int j = lane; j < ncol; j += 32) {
+          if (wid == cw) {
+            const T v = j < cc ? Ls[j * ldt + (int)(ci - my_lo)] : wstage[wid][0][j];
+            LLVal<T>::put(rows + ((size_t)par * G + blockIdx.x) * RW + j * VW, v, ep);
+          }
+          if (wid == dw) {
+            const T v = j < cc ? Ls[j * ldt + (int)(ii - my_lo)] : wstage[wid][1][j];
+            LLVal<T>::put(diag + (size_t)par * RW + j * VW, v, ep);
+          }
+        }
+        __syncwarp();
+      }
+    };
+
+    {
+      unsigned long long ck = mine ? piv_key(fabs((double)y[0])) : 0ull;
+      int64_t ci = mine ? g : INT64_MAX;
+      cta_argmax_key(ck, ci, wk[0], wi[0]);
+      publish(0, 0, ci);
+    }
+    for (int c = 0; c < ncol; ++c) {
+      const int64_t i = a.kb + c;
+      const int par = c & 1;
+      const long long t_c = a.trace ? clock64() : 0;
+      mbar_wait(&s_bar, (unsigned)par);
+      const long long t_e2 = a.trace ? clock64() : 0;
+      const T* pa = pabs[par];
+      const T* da = dabs[par];
+      const T* pr = prot[par];
+      const T* dr = drot[par];
+      const int64_t p = s_piv[par];
+      const T aii = pr[0];
+      const bool zero = aii == T(0);
+      // ---- swap (direct.py:68-70, restricted to the panel): retired columns by the
+      // owning warps, the register rows by their threads
+      if (p != i) {
+        if (i >= my_lo && i < my_hi && wid == 1 + ((int)(i - my_lo) >> 5))
+          for (int j = lane; j < c; j += 32) Ls[j * ldt + (int)(i - my_lo)] = pa[j];
+        if (p >= my_lo && p < my_hi && wid == 1 + ((int)(p - my_lo) >> 5))
+          for (int j = lane; j < c; j += 32) Ls[j * ldt + (int)(p - my_lo)] = da[j];
+        if (mine && (g == i || g == p)) {
+          const T* src = g == i ? pr : dr;
+#pragma unroll
+          for (int k = 0; k < PW; ++k) y[k] = src[k];
+        }
+      }
+      // ---- reciprocal scale and the update of column c + 1 first
+      const bool act = mine && g > i && !zero;
+      T l = T(0);
+      if (act) {
+        l = mul_rn(s_rcp[par], y[0]);
+        y[0] = l;
+        y[1] = sub_rn(y[1], mul_rn(l, pr[1]));
+      }
+      if (mine) Ls[c * ldt + r] = y[0];  // retire column c
+      const long long t_f = a.trace ? clock64() : 0;
+      // ---- next column's CTA candidate (rows >= i + 1): the one CTA-wide barrier,
+      // then its header and rows go out before the rest of the update
+      int64_t ci = INT64_MAX;
+      if (c + 1 < ncol) {
+        unsigned long long ck = (mine && g > i) ? piv_key(fabs((double)y[1])) : 0ull;
+        ci = (mine && g > i) ? g : INT64_MAX;
+        cta_argmax_key(ck, ci, wk[(c + 1) & 1], wi[(c + 1) & 1]);
+        publish(c + 1, c, ci);
+      }
+      const long long t_g = a.trace ? clock64() : 0;
+      // ---- rest of the rank-1 update (direct.py:75-79), then rotate by one
+      if (act) {
+#pragma unroll
+        for (int k = 2; k < PW; ++k) y[k] = sub_rn(y[k], mul_rn(l, pr[k]));
+      }
+#pragma unroll
+      for (int k = 0; k + 1 < PW; ++k) y[k] = y[k + 1];
+      y[PW - 1] = T(0);
+      if (a.trace && t == 32) {
+        const long long t_h = clock64();
+        unsigned long long* tr = a.trace + (size_t)blockIdx.x * 8;
+        tr[3] += t_e2 - t_c;  // wait for the handoff
+        tr[0] += t_f - t_e2;  // swap, scale
+        tr[1] += t_g - t_f;   // next column's CTA argmax + publish
+        tr[5] += t_h - t_g;   // update, rotate
+      }
+    }
+  }
+  __syncthreads();
+  for (int idx = t; idx < ncol * nr; idx += blockDim.x) {
     const int j = idx / nr, rr = idx % nr;
     W[(my_lo + rr) + (a.kb + j) * a.ld] = Ls[j * ldt + rr];
   }
@@ -803,6 +1173,11 @@ int panel_launch(ds_ctx* ctx, T* W, int64_t n, int64_t ld, int64_t kb, int64_t b
   a.ll_diag = cv.take<uint64_t>(sizeof(uint64_t) * 2 * kPanelMaxW * 2);
   a.seq = ++ctx->panel_seq;
   a.trace = nullptr;
+  static const int backoff = [] {
+    const char* e = getenv("DENSOLVE_PANEL_BACKOFF");
+    return e ? atoi(e) : 0;
+  }();
+  a.backoff = backoff;
   const size_t smem_cap = std::min<size_t>(ctx->smem_optin, 220 * 1024) - 2048;
   // shared-memory path: rows split over <= num_sms CTAs, >= 16 rows each
   if (ncol <= kPanelMaxW) {
@@ -811,12 +1186,26 @@ int panel_launch(ds_ctx* ctx, T* W, int64_t n, int64_t ld, int64_t kb, int64_t b
       const char* e = getenv("DENSOLVE_PANEL_ROWS");
       return e ? std::max<int64_t>(16, atoll(e)) : (int64_t)256;
     }();
-    int64_t g = std::min<int64_t>((int64_t)ctx->num_sms, ceil_div(rows, target));
+    // kernel choice (measured per column, n = 16384): the poller-warp kernel wins for
+    // 2..40 CTAs of <= 224 rows (2.9 vs 3.3 us at G = 10); the CTA-synchronous
+    // register-row kernel for one CTA (shared memory only) and for the tall panels.
+    // DENSOLVE_PANEL_KERNEL = 1 / 2 forces one of them.
+    static const int force = [] {
+      const char* e = getenv("DENSOLVE_PANEL_KERNEL");
+      return e ? atoi(e) : 0;
+    }();
+    static const int64_t kWarpMaxG = [] {  // tuning knob
+      const char* e = getenv("DENSOLVE_PANEL_WARP_MAXG");
+      return e ? (int64_t)atoll(e) : (int64_t)40;
+    }();
+    const int64_t gw = ceil_div(rows, (int64_t)kPanelWarpRows);
+    const bool warp_k = force == 1 ? gw <= (int64_t)ctx->num_sms : force == 2 ? false : (gw >= 2 && gw <= kWarpMaxG);
+    int64_t g = warp_k ? gw : std::min<int64_t>((int64_t)ctx->num_sms, ceil_div(rows, target));
     int64_t per = ceil_div(rows, g);
     g = ceil_div(rows, per);
     const int ldt = (int)(per | 1);
     const size_t smem = (size_t)ncol * ldt * sizeof(T);
-    const int tpr = per <= kPanelRegThreads / 4 ? 4 : 2;
+    const int tpr = warp_k ? 1 : per <= kPanelRegThreads / 4 ? 4 : 2;
     if (smem <= smem_cap && per * tpr <= kPanelRegThreads) {
       a.per = (int)per;
       a.ldt = ldt;
@@ -826,10 +1215,16 @@ int panel_launch(ds_ctx* ctx, T* W, int64_t n, int64_t ld, int64_t kb, int64_t b
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
         DS_CUDA(cudaFuncSetAttribute(lu_panel_smem_kernel<T, 4>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
+        // <= 256 rows x 64 columns of retired values (131.6 KB) beside ~26 KB of static buffers
+        DS_CUDA(cudaFuncSetAttribute(lu_panel_warp_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)std::min<size_t>(smem_cap, 160 * 1024)));
         attr_set[sizeof(T) == 8 ? 1 : 0] = true;
       }
-      const int nthr = (int)std::max<int64_t>(ceil_div(per * tpr, 32) * 32, ceil_div(g, 32) * 32);
-      void* kfn = tpr == 4 ? (void*)lu_panel_smem_kernel<T, 4> : (void*)lu_panel_smem_kernel<T, 2>;
+      const int nthr = warp_k ? (int)(32 + ceil_div(per, 32) * 32)
+                             : (int)std::max<int64_t>(ceil_div(per * tpr, 32) * 32, ceil_div(g, 32) * 32);
+      void* kfn = warp_k     ? (void*)lu_panel_warp_kernel<T>
+                  : tpr == 4 ? (void*)lu_panel_smem_kernel<T, 4>
+                             : (void*)lu_panel_smem_kernel<T, 2>;
       const char* tr = getenv("DENSOLVE_PANEL_TRACE");  // debug: per-phase timestamps of one panel
       const bool tracing = tr && atoll(tr) == kb;
       if (tracing) {
@@ -857,17 +1252,20 @@ int panel_launch(ds_ctx* ctx, T* W, int64_t n, int64_t ld, int64_t kb, int64_t b
         cudaEventElapsedTime(&ms, e0, e1);
         cudaFree(a.trace);
         a.trace = nullptr;
-        double mean[6] = {}, mx[6] = {};
+        double mean[7] = {}, mx[7] = {};
         for (int64_t b = 0; b < g; ++b)
-          for (int k = 0; k < 6; ++k) {
+          for (int k = 0; k < 7; ++k) {
             mean[k] += (double)h[b * 8 + k] / g / ncol;
             mx[k] = std::max(mx[k], (double)h[b * 8 + k] / ncol);
           }
         fprintf(stderr, "[panel trace] kb=%lld rows=%lld G=%lld per=%lld: %.2f us/column (events); cycles/column "
-                "mean(max): argmax0 %.0f(%.0f) publish %.0f(%.0f) hdrpoll %.0f(%.0f) argmax1 %.0f(%.0f) "
-                "rowpoll+sync %.0f(%.0f) update %.0f(%.0f)\n", (long long)kb, (long long)rows, (long long)g,
-                (long long)per, 1e3 * ms / ncol, mean[0], mx[0], mean[1], mx[1], mean[2], mx[2], mean[3], mx[3],
-                mean[4], mx[4], mean[5], mx[5]);
+                "mean(max) [poller kernel: 0 swap+scale, 1 next argmax+publish, 2 poller hdr poll, 3 row-warp wait, "
+                "4 poller row poll, 5 update; cta kernel: 0 swap+scale, 1 next argmax, 2 hdr poll, 3 hdr argmax, 4 row "
+                "poll+sync, 5 update, 6 publish rows]: %.0f(%.0f) %.0f(%.0f) %.0f(%.0f) %.0f(%.0f) %.0f(%.0f) %.0f(%.0f) "
+                "%.0f(%.0f) [tpr %d, %d threads]\n",
+                (long long)kb, (long long)rows, (long long)g, (long long)per, 1e3 * ms / ncol, mean[0], mx[0],
+                mean[1], mx[1], mean[2], mx[2], mean[3], mx[3], mean[4], mx[4], mean[5], mx[5], mean[6], mx[6],
+                tpr, nthr);
       }
       return DS_OK;
     }
