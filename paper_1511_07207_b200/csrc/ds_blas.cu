@@ -243,6 +243,7 @@ int gemv_launch(ds_ctx* ctx, const GemvPlan& p, const T* A, int64_t lda, const T
     count_launch(ctx);
     DS_CHECK_LAUNCH();
   }
+  if (epi == EPI_PARTIAL) return DS_OK;
   const int64_t nch = n == 0 ? 1 : p.nchunks;
   switch (epi) {
     case EPI_STORE:
@@ -264,6 +265,8 @@ int gemv_launch(ds_ctx* ctx, const GemvPlan& p, const T* A, int64_t lda, const T
     case EPI_DOT2:
       gemv_reduce_kernel<T, EPI_DOT2>
           <<<rblocks, kRedThreads, 0, ctx->stream>>>(part, m, nch, y, v, red, stop);
+      break;
+    default:
       break;
   }
   count_launch(ctx);

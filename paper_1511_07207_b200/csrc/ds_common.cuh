@@ -135,6 +135,10 @@ __device__ __forceinline__ double block_nanmax(double v, double* smem) {
 // Restates the intent of Backend.nrm2 (backends.py:114-122: m*sqrt(dot(x/m,x/m)))
 // in a single pass: partial pairs are combined to the global max scale m.
 // ---------------------------------------------------------------------------
+// max propagating NaN (np.max semantics)
+__device__ __forceinline__ double nan_max(double a, double b) {
+  return (a != a) ? a : (b != b) ? b : fmax(a, b);
+}
 struct Ssq {
   double scale;  // max |x| seen (NaN-propagating)
   double ssq;    // sum (x/scale)^2

@@ -18,6 +18,8 @@ enum GemvEpi : int {
   EPI_AXPY_INTO = 3,  // y = y + (A x)   (GMRES x += V y, krylov.py:167)
   EPI_DOT2 = 4,       // y = A x ; block partials of dot(v, y) -> red[blk], dot(y, y) -> red[nblk + blk]
                       //   (BiCGSTAB t's and t't, krylov.py:230-231)
+  EPI_PARTIAL = 5,    // stage 1 only: the chunk partials stay in `part` for a consumer
+                      //   kernel that sums them itself (GMRES cluster orthogonalisation)
 };
 
 // Device-side loop gate: solver kernels of iteration k return immediately once

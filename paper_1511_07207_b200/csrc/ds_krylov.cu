@@ -682,29 +682,62 @@ __global__ void __launch_bounds__(kArnThreads)
 // of L2 round trips.  CTA rank 0 records H / Hraw and runs the Givens logic.
 // ============================================================================
 constexpr int kOrthThreads = 512;
+constexpr unsigned kOrthMaxCluster = 16;  // the launch uses 16 or 8
 
 template <typename T>
 __global__ void __launch_bounds__(kOrthThreads, 1)
     arnoldi_orth_cluster_kernel(int64_t n, T* V, int64_t ldv, int k, int passes, T* H, T* Hraw, int64_t ldh, T* g,
                                 T* cs, T* sn, double* est_out, GmDev* st, double tol, int64_t total_before,
-                                int64_t cap, Gate gate) {
+                                int64_t cap, Gate gate, const double* __restrict__ gpart, int64_t nchunks,
+                                unsigned long long* trace) {
   namespace cgr = cooperative_groups;
   if (gated(gate)) return;
   cgr::cluster_group cluster = cgr::this_cluster();
   const unsigned CL = cluster.num_blocks();
   const unsigned rank = cluster.block_rank();
+  // debug (DENSOLVE_ORTH_TRACE): %globaltimer at the phase boundaries, ranks 0 and CL - 1
+  auto stamp = [&](int idx) {
+    if (trace && threadIdx.x == 0 && (rank == 0 || rank == CL - 1)) {
+      unsigned long long tm;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tm));
+      trace[((size_t)k * 2 + (rank == 0 ? 0 : 1)) * 16 + idx] = tm;
+    }
+  };
+  stamp(0);
   extern __shared__ __align__(16) unsigned char orth_smem[];
   double* wv = reinterpret_cast<double*>(orth_smem);  // my rows of w (fp64 copy of T values)
-  __shared__ double part[3][64];                      // my partials, buffer per exchange
+  __shared__ double part[2][64];                      // my CGS partials, buffer per pass
+  __shared__ double inbox[2][kOrthMaxCluster];        // norm partials pushed by every CTA
   __shared__ double hs[64], hsave[64], sm[64];
+  __shared__ T hcol[64], css[64], sns[64];            // rank 0: H[:, k] and the rotations so far
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kOrthThreads / 32;
   const int64_t per = ceil_div(ceil_div(n, (int64_t)CL), 4) * 4;
   const int64_t r0 = (int64_t)rank * per;
   const int nr = (int)max((int64_t)0, min(per, n - r0));
   const int kc = k + 1;
-  T* w = V + (int64_t)(k + 1) * ldv;  // A v_k, written by the GEMV
-  for (int r = tid; r < nr; r += blockDim.x) wv[r] = (double)w[r0 + r];
+  T* w = V + (int64_t)(k + 1) * ldv;
+  // w = A v_k: the GEMV's chunk partials summed here, in chunk order (gemv_reduce_kernel's
+  // order, so w is bitwise the EPI_STORE result), up to 32 loads in flight
+  for (int r = tid; r < nr; r += blockDim.x) {
+    const double* pr = gpart + r0 + r;
+    double s = 0.0;
+    for (int64_t c0 = 0; c0 < nchunks; c0 += 32) {
+      double v[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) v[u] = c0 + u < nchunks ? pr[(c0 + u) * n] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 32; ++u)
+        if (c0 + u < nchunks) s += v[u];
+    }
+    wv[r] = (double)(T)s;
+  }
+  if (rank == 0)
+    for (int j = tid; j < k; j += blockDim.x) {
+      css[j] = cs[j];
+      sns[j] = sn[j];
+    }
   __syncthreads();
+  stamp(1);
   for (int ps = 0; ps < passes; ++ps) {
     // partial h_j over my rows: warp per j, lanes over rows (V from L2)
     for (int j = warp; j < kc; j += nw) {
@@ -715,21 +748,29 @@ __global__ void __launch_bounds__(kOrthThreads, 1)
       s = warp_sum(s);
       if (lane == 0) part[ps][j] = s;
     }
+    stamp(2 + 4 * ps);
     cluster.sync();
+    stamp(3 + 4 * ps);
     for (int j = tid; j < kc; j += blockDim.x) {  // rank-ordered sum over the cluster (DSMEM)
+      double v[kOrthMaxCluster];  // every remote load in flight before the ordered sum
+#pragma unroll
+      for (unsigned b = 0; b < kOrthMaxCluster; ++b)
+        v[b] = b < CL ? cluster.map_shared_rank(&part[ps][0], b)[j] : 0.0;
       double s = 0.0;
-      for (unsigned b = 0; b < CL; ++b) s += cluster.map_shared_rank(&part[ps][0], b)[j];
+#pragma unroll
+      for (unsigned b = 0; b < kOrthMaxCluster; ++b)
+        if (b < CL) s += v[b];
       hs[j] = s;
     }
     __syncthreads();
+    stamp(4 + 4 * ps);
     if (rank == 0) {
-      T* Hcol = H + (int64_t)k * ldh;
       for (int j = tid; j < kc; j += blockDim.x) {
         if (ps == 0) {
           hsave[j] = hs[j];
-          Hcol[j] = (T)hs[j];
+          hcol[j] = (T)hs[j];
         } else {
-          Hcol[j] = (T)(hsave[j] + hs[j]);
+          hcol[j] = (T)(hsave[j] + hs[j]);
         }
       }
     }
@@ -737,68 +778,96 @@ __global__ void __launch_bounds__(kOrthThreads, 1)
     for (int r = tid; r < nr; r += blockDim.x) {
       T wi = (T)wv[r];
       const T* vr = V + r0 + r;
-      int j = 0;
-      for (; j + 8 <= kc; j += 8) {  // 8 basis loads in flight, then the ordered axpys
-        T vv[8];
+      for (int j0 = 0; j0 < kc; j0 += 32) {  // up to 32 basis loads in flight, then the ordered axpys
+        T vv[32];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) vv[u] = vr[(int64_t)(j + u) * ldv];
+        for (int u = 0; u < 32; ++u) vv[u] = j0 + u < kc ? vr[(int64_t)(j0 + u) * ldv] : T(0);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) wi = add_rn(wi, mul_rn((T)(-hs[j + u]), vv[u]));
+        for (int u = 0; u < 32; ++u)
+          if (j0 + u < kc) wi = add_rn(wi, mul_rn((T)(-hs[j0 + u]), vv[u]));
       }
-      for (; j < kc; ++j) wi = add_rn(wi, mul_rn((T)(-hs[j]), vr[(int64_t)j * ldv]));
       wv[r] = (double)wi;
     }
     __syncthreads();
+    stamp(5 + 4 * ps);
   }
-  // h_{k+1,k} = ||w|| (scaled): (scale, ssq) per CTA, merged in rank order
-  Ssq q{0.0, 0.0};
-  for (int r = tid; r < nr; r += blockDim.x) q = ssq_add(q, wv[r]);
-  q = block_ssq(q, sm);
-  if (tid == 0) {
-    part[2][0] = q.scale;
-    part[2][1] = q.ssq;
+  // h_{k+1,k} = nrm2(w), the reference's two-pass form (backends.py:114-122):
+  // m = max|w| (exact, order-free), then m * sqrt(sum (w/m)^2).  Both cluster
+  // exchanges PUSH each CTA's partial into every CTA's inbox before the barrier,
+  // so afterwards only local shared memory is read (no exit guard needed).
+  double mx = 0.0;
+  for (int r = tid; r < nr; r += blockDim.x) mx = nan_max(mx, fabs(wv[r]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = nan_max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) sm[warp] = mx;
+  __syncthreads();
+  if (tid < (int)CL) {
+    double cm = 0.0;
+    for (int w2 = 0; w2 < nw; ++w2) cm = nan_max(cm, sm[w2]);
+    cluster.map_shared_rank(&inbox[0][0], (unsigned)tid)[rank] = cm;
   }
   cluster.sync();
-  if (tid == 0) {
-    Ssq m{0.0, 0.0};
-    for (unsigned b = 0; b < CL; ++b) {
-      const double* rp = cluster.map_shared_rank(&part[2][0], b);
-      m = ssq_merge(m, Ssq{rp[0], rp[1]});
+  double m_all = 0.0;
+#pragma unroll
+  for (unsigned b = 0; b < kOrthMaxCluster; ++b)
+    if (b < CL) m_all = nan_max(m_all, inbox[0][b]);
+  double hk1 = m_all;
+  if (m_all != 0.0 && m_all - m_all == 0.0) {  // finite, nonzero
+    double s2 = 0.0;
+    for (int r = tid; r < nr; r += blockDim.x) {
+      const double t = div_rn(wv[r], m_all);
+      s2 = add_rn(s2, mul_rn(t, t));
     }
-    sm[0] = ssq_norm(m.scale, m.ssq);
+    s2 = block_sum(s2, sm);
+    if (tid < (int)CL) cluster.map_shared_rank(&inbox[1][0], (unsigned)tid)[rank] = s2;
+    cluster.sync();
+    double tot = 0.0;
+#pragma unroll
+    for (unsigned b = 0; b < kOrthMaxCluster; ++b)
+      if (b < CL) tot += inbox[1][b];
+    hk1 = mul_rn(m_all, sqrt(tot));
   }
-  // no CTA may exit (or reuse part[]) while others still read its shared memory
-  cluster.sync();
-  const double hk1 = sm[0];
+  stamp(10);
   const bool happy = hk1 == 0.0;
   {
     const T sc = (T)(1.0 / hk1);  // scal(1.0/hk1, w) (krylov.py:143-144)
     for (int r = tid; r < nr; r += blockDim.x) w[r0 + r] = happy ? (T)wv[r] : mul_rn(sc, (T)wv[r]);
   }
+  stamp(11);
   if (rank == 0 && tid == 0) {  // Givens, estimate, stop (krylov.py:146-163)
     T* Hk = H + (int64_t)k * ldh;
     T* Hr = Hraw + (int64_t)k * ldh;
-    Hk[k + 1] = (T)hk1;
-    for (int j = 0; j <= k + 1; ++j) Hr[j] = Hk[j];
+    // the column from shared memory (hsave/hs of the passes), rotations in registers:
+    // the running H[j+1] is carried, so no store -> load round trip per rotation
+    T col_last = (T)hk1;
+    for (int j = 0; j <= k; ++j) Hr[j] = hcol[j];
+    Hr[k + 1] = col_last;
+    T cur = hcol[0];
     for (int j = 0; j < k; ++j) {
-      const T t = add_rn(mul_rn(cs[j], Hk[j]), mul_rn(sn[j], Hk[j + 1]));
-      Hk[j + 1] = add_rn(mul_rn(-sn[j], Hk[j]), mul_rn(cs[j], Hk[j + 1]));
+      const T nxt = hcol[j + 1];
+      const T c = css[j], s_ = sns[j];
+      const T t = add_rn(mul_rn(c, cur), mul_rn(s_, nxt));
+      cur = add_rn(mul_rn(-s_, cur), mul_rn(c, nxt));
       Hk[j] = t;
     }
-    const T denom = sizeof(T) == 8 ? (T)hypot((double)Hk[k], (double)Hk[k + 1])
-                                   : (T)hypotf((float)Hk[k], (float)Hk[k + 1]);
-    cs[k] = div_rn(Hk[k], denom);
-    sn[k] = div_rn(Hk[k + 1], denom);
+    // cur = rotated H[k], col_last = H[k+1]
+    const T denom = sizeof(T) == 8 ? (T)hypot((double)cur, (double)col_last)
+                                   : (T)hypotf((float)cur, (float)col_last);
+    const T ck = div_rn(cur, denom), sk = div_rn(col_last, denom);
+    cs[k] = ck;
+    sn[k] = sk;
     Hk[k] = denom;
     Hk[k + 1] = T(0);
-    g[k + 1] = mul_rn(-sn[k], g[k]);
-    g[k] = mul_rn(cs[k], g[k]);
-    const double est = fabs((double)g[k + 1]) / st->bnorm;
+    const T gk = g[k];
+    g[k + 1] = mul_rn(-sk, gk);
+    g[k] = mul_rn(ck, gk);
+    const double est = fabs((double)mul_rn(-sk, gk)) / st->bnorm;
     est_out[k] = est;
     const int64_t total = total_before + k + 1;
     if (happy) st->happy = 1;
     if (happy || est <= tol || total >= cap) st->stop_k = k + 1;
   }
+  stamp(12);
 }
 
 // y = H[:inner,:inner]^-1 g[:inner] (backward_substitution, direct.py:139-152), one thread
@@ -879,6 +948,7 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
   // (16 non-portable, else 8) that the device can co-schedule; rows per CTA <= 4096
   int orth_cl = 0;
   size_t orth_smem = 0;
+  unsigned long long* orth_trace = nullptr;
   {
     const char* oe = getenv("DENSOLVE_GMRES_ORTH");
     const bool want = !(oe && strcmp(oe, "grid") == 0) && n <= 16 * 4096;
@@ -912,6 +982,10 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
         }
       }
       if (bc > 0 && ceil_div(ceil_div(n, (int64_t)bc), 4) * 4 <= 4096) {
+        if (getenv("DENSOLVE_ORTH_TRACE")) {
+          DS_CUDA(cudaMalloc((void**)&orth_trace, sizeof(unsigned long long) * m * 2 * 16));
+          DS_CUDA(cudaMemset(orth_trace, 0, sizeof(unsigned long long) * m * 2 * 16));
+        }
         orth_cl = bc;
         orth_smem = (size_t)ceil_div(ceil_div(n, (int64_t)bc), 4) * 4 * sizeof(double);
       }
@@ -1041,7 +1115,7 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
         T* w = V + (k + 1) * ldv;
         const int kc = (int)k + 1;
         if (orth_cl > 0) {  // streamed GEMV on every SM + one-cluster orthogonalisation
-          DS_TRY(gemv_launch<T>(ctx, gp, A, lda, vk, w, part, EPI_STORE, nullptr, nullptr, nullptr, gt));
+          DS_TRY(gemv_launch<T>(ctx, gp, A, lda, vk, w, part, EPI_PARTIAL, nullptr, nullptr, nullptr, gt));
           cudaLaunchConfig_t lc = {};
           lc.gridDim = dim3((unsigned)orth_cl);
           lc.blockDim = dim3(kOrthThreads);
@@ -1056,7 +1130,8 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
           lc.numAttrs = 1;
           const int passes = orth == DS_ORTH_CLASSICAL ? 1 : 2;
           DS_CUDA(cudaLaunchKernelEx(&lc, arnoldi_orth_cluster_kernel<T>, n, V, ldv, (int)k, passes, H, Hraw, ldh, g,
-                                     cs, sn, est, st, tol, total_it, cap, gt));
+                                     cs, sn, est, st, tol, total_it, cap, gt, (const double*)part,
+                                     (int64_t)gp.nchunks, orth_trace));
           count_launch(ctx);
           continue;
         }
@@ -1191,6 +1266,25 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
       history.back() = true_res;
       finish(false, DS_BREAKDOWN_NONE);
       break;
+    }
+  }
+  if (orth_trace) {  // last cycle's per-step phase durations (ns), mean over its steps
+    std::vector<unsigned long long> h((size_t)m * 2 * 16);
+    DS_CUDA(cudaMemcpy(h.data(), orth_trace, h.size() * 8, cudaMemcpyDeviceToHost));
+    cudaFree(orth_trace);
+    for (int rk = 0; rk < 2; ++rk) {
+      double d[13] = {};
+      int cnt = 0;
+      for (int64_t kk = 0; kk < m; ++kk) {
+        const unsigned long long* t = h.data() + ((size_t)kk * 2 + rk) * 16;
+        if (t[0] == 0 || t[12] == 0 && rk == 0) continue;
+        ++cnt;
+        for (int z = 1; z <= (rk == 0 ? 12 : 11); ++z) d[z] += (double)(t[z] - t[z - 1]);
+      }
+      fprintf(stderr, "[orth trace] %s, %d steps, ns/step: load %.0f | p0 dot %.0f csync %.0f red %.0f upd %.0f | "
+              "p1 dot %.0f csync %.0f red %.0f upd %.0f | norm+2 csync %.0f | store %.0f | givens %.0f\n",
+              rk == 0 ? "rank 0" : "last rank", cnt, d[1] / cnt, d[2] / cnt, d[3] / cnt, d[4] / cnt, d[5] / cnt,
+              d[6] / cnt, d[7] / cnt, d[8] / cnt, d[9] / cnt, d[10] / cnt, d[11] / cnt, d[12] / cnt);
     }
   }
   if (arn_trace) {
