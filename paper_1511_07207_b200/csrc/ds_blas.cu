@@ -94,7 +94,9 @@ __global__ void __launch_bounds__(kGemvThreads)
     gemv_partial_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t n,
                         const T* __restrict__ x, int64_t chunk, double* __restrict__ part,
                         Gate gate) {
+  pdl_wait();  // x and the stop word come from the previous kernel
   if (gated(gate)) return;
+  pdl_launch_dependents();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* xs = reinterpret_cast<T*>(smem_raw);
   const int64_t c0 = (int64_t)blockIdx.y * chunk;
@@ -274,6 +276,33 @@ int gemv_launch(ds_ctx* ctx, const GemvPlan& p, const T* A, int64_t lda, const T
   return DS_OK;
 }
 
+template <typename T>
+int gemv_partial_pdl_launch(ds_ctx* ctx, const GemvPlan& p, const T* A, int64_t lda, const T* x, double* part,
+                            Gate stop) {
+  constexpr int VEC = sizeof(T) == 8 ? 2 : 4;
+  const bool aligned = (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (lda % VEC == 0);
+  if (p.m == 0 || p.n == 0 || !aligned)
+    return gemv_launch<T>(ctx, p, A, lda, x, nullptr, part, EPI_PARTIAL, nullptr, nullptr, nullptr, stop);
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)p.rowtiles, (unsigned)p.nchunks);
+  lc.blockDim = dim3(kGemvThreads);
+  lc.dynamicSmemBytes = (size_t)p.chunk * sizeof(T);
+  lc.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  const int64_t m = p.m, n = p.n, chunk = p.chunk;
+  DS_CUDA(cudaLaunchKernelEx(&lc, gemv_partial_kernel<T, VEC, 8>, A, lda, m, n, x, chunk, part, stop));
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+template int gemv_partial_pdl_launch<double>(ds_ctx*, const GemvPlan&, const double*, int64_t, const double*, double*,
+                                             Gate);
+template int gemv_partial_pdl_launch<float>(ds_ctx*, const GemvPlan&, const float*, int64_t, const float*, double*,
+                                            Gate);
 template int gemv_launch<double>(ds_ctx*, const GemvPlan&, const double*, int64_t, const double*,
                                  double*, double*, GemvEpi, const double*, double*, int*,
                                  Gate);

@@ -33,6 +33,14 @@ __device__ __forceinline__ bool gated(const Gate& g) {
   return g.stop_it != nullptr && *((volatile const int64_t*)g.stop_it) <= g.k;
 }
 
+// Programmatic dependent launch (PDL): a kernel launched with the programmatic
+// stream-serialization attribute may start while its predecessor still runs; it
+// must wait here before touching the predecessor's results (no-op without PDL).
+// launch_dependents lets the NEXT kernel start launching (it still waits for this
+// grid's completion at its own pdl_wait).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 struct GemvPlan {
   int64_t m, n;
   int rows_per_cta;  // multiple of 32*VEC
@@ -44,6 +52,11 @@ struct GemvPlan {
 
 GemvPlan gemv_plan(ds_ctx* ctx, int64_t m, int64_t n, size_t elem);
 
+// Stage 1 only, launched with the PDL attribute (the GMRES cluster path: the
+// orthogonalisation kernel that follows sums the partials itself).
+template <typename T>
+int gemv_partial_pdl_launch(ds_ctx* ctx, const GemvPlan& p, const T* A, int64_t lda, const T* x, double* part,
+                            Gate stop);
 // Launch stage 1 + 2.  `part` must have plan.part_bytes; `red` (for EPI_DOT /
 // EPI_RESID) receives per-block reduction partials (see reduce_blocks()).
 template <typename T>

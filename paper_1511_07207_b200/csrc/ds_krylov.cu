@@ -691,7 +691,9 @@ __global__ void __launch_bounds__(kOrthThreads, 1)
                                 int64_t cap, Gate gate, const double* __restrict__ gpart, int64_t nchunks,
                                 unsigned long long* trace) {
   namespace cgr = cooperative_groups;
+  pdl_wait();  // the GEMV partials, V and the stop word come from earlier kernels
   if (gated(gate)) return;
+  pdl_launch_dependents();
   cgr::cluster_group cluster = cgr::this_cluster();
   const unsigned CL = cluster.num_blocks();
   const unsigned rank = cluster.block_rank();
@@ -870,25 +872,38 @@ __global__ void __launch_bounds__(kOrthThreads, 1)
   stamp(12);
 }
 
-// y = H[:inner,:inner]^-1 g[:inner] (backward_substitution, direct.py:139-152), one thread
+// y = H[:inner,:inner]^-1 g[:inner] (backward_substitution, direct.py:139-152): the
+// block stages the upper triangle in shared memory, then one thread runs the
+// dependent recurrence out of shared memory (no global round trip per term)
 template <typename T>
 __global__ void gm_lsq_kernel(const T* H, int64_t ldh, const T* g, int inner, T* y, GmDev* st) {
+  __shared__ T Hs[64][65];
+  __shared__ T ys[64];
+  for (int idx = threadIdx.x; idx < inner * inner; idx += blockDim.x) {
+    const int i = idx % inner, j = idx / inner;
+    if (i <= j) Hs[i][j] = H[i + (int64_t)j * ldh];
+  }
+  for (int i = threadIdx.x; i < inner; i += blockDim.x) ys[i] = g[i];
+  __syncthreads();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  for (int i = 0; i < inner; ++i) y[i] = g[i];
   for (int i = inner - 1; i >= 0; --i) {
+    T yi = ys[i];
     if (i + 1 < inner) {
       double s = 0.0;
-      for (int j = i + 1; j < inner; ++j) s = fma((double)H[i + (int64_t)j * ldh], (double)y[j], s);
-      y[i] = sub_rn(y[i], (T)s);
+      for (int j = i + 1; j < inner; ++j) s = fma((double)Hs[i][j], (double)ys[j], s);
+      yi = sub_rn(yi, (T)s);
     }
-    const T d = H[i + (int64_t)i * ldh];
+    ys[i] = yi;
+    const T d = Hs[i][i];
     if (d == T(0)) {
       st->status = DS_ESINGULAR;
       st->bad_row = i;
+      for (int k = 0; k < inner; ++k) y[k] = ys[k];
       return;
     }
-    y[i] = div_rn(y[i], d);
+    ys[i] = div_rn(yi, d);
   }
+  for (int k = 0; k < inner; ++k) y[k] = ys[k];
 }
 
 // cycle start: V[:,0] = scal(1/beta, r); g = beta e1 (krylov.py:116-123)
@@ -948,6 +963,10 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
   // (16 non-portable, else 8) that the device can co-schedule; rows per CTA <= 4096
   int orth_cl = 0;
   size_t orth_smem = 0;
+  static const bool pdl_on = [] {  // programmatic dependent launch in the cluster path
+    const char* e = getenv("DENSOLVE_PDL");
+    return !(e && e[0] == '0');
+  }();
   unsigned long long* orth_trace = nullptr;
   {
     const char* oe = getenv("DENSOLVE_GMRES_ORTH");
@@ -1115,19 +1134,24 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
         T* w = V + (k + 1) * ldv;
         const int kc = (int)k + 1;
         if (orth_cl > 0) {  // streamed GEMV on every SM + one-cluster orthogonalisation
-          DS_TRY(gemv_launch<T>(ctx, gp, A, lda, vk, w, part, EPI_PARTIAL, nullptr, nullptr, nullptr, gt));
+          if (pdl_on)
+            DS_TRY(gemv_partial_pdl_launch<T>(ctx, gp, A, lda, vk, part, gt));
+          else
+            DS_TRY(gemv_launch<T>(ctx, gp, A, lda, vk, w, part, EPI_PARTIAL, nullptr, nullptr, nullptr, gt));
           cudaLaunchConfig_t lc = {};
           lc.gridDim = dim3((unsigned)orth_cl);
           lc.blockDim = dim3(kOrthThreads);
           lc.dynamicSmemBytes = orth_smem;
           lc.stream = ctx->stream;
-          cudaLaunchAttribute at[1];
+          cudaLaunchAttribute at[2];
           at[0].id = cudaLaunchAttributeClusterDimension;
           at[0].val.clusterDim.x = (unsigned)orth_cl;
           at[0].val.clusterDim.y = 1;
           at[0].val.clusterDim.z = 1;
+          at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+          at[1].val.programmaticStreamSerializationAllowed = 1;
           lc.attrs = at;
-          lc.numAttrs = 1;
+          lc.numAttrs = pdl_on ? 2 : 1;
           const int passes = orth == DS_ORTH_CLASSICAL ? 1 : 2;
           DS_CUDA(cudaLaunchKernelEx(&lc, arnoldi_orth_cluster_kernel<T>, n, V, ldv, (int)k, passes, H, Hraw, ldh, g,
                                      cs, sn, est, st, tol, total_it, cap, gt, (const double*)part,
@@ -1211,7 +1235,7 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
     total_it += inner;
 
     // cycle end: y = H^-1 g ; x += V y   (krylov.py:166-167)
-    gm_lsq_kernel<T><<<1, 32, 0, ctx->stream>>>(H, ldh, g, inner, y, st);
+    gm_lsq_kernel<T><<<1, 256, 0, ctx->stream>>>(H, ldh, g, inner, y, st);
     count_launch(ctx);
     {
       const GemvPlan gp2 = gemv_plan(ctx, n, inner, sizeof(T));
@@ -1281,10 +1305,22 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
         ++cnt;
         for (int z = 1; z <= (rk == 0 ? 12 : 11); ++z) d[z] += (double)(t[z] - t[z - 1]);
       }
+      double period = 0.0, outside = 0.0;
+      int np_ = 0;
+      for (int64_t kk = 0; kk + 1 < m; ++kk) {
+        const unsigned long long* t = h.data() + ((size_t)kk * 2) * 16;
+        const unsigned long long* t2 = h.data() + ((size_t)(kk + 1) * 2) * 16;
+        if (t[0] == 0 || t2[0] == 0 || t[12] == 0) continue;
+        period += (double)(t2[0] - t[0]);
+        outside += (double)(t2[0] - t[12]);
+        ++np_;
+      }
       fprintf(stderr, "[orth trace] %s, %d steps, ns/step: load %.0f | p0 dot %.0f csync %.0f red %.0f upd %.0f | "
-              "p1 dot %.0f csync %.0f red %.0f upd %.0f | norm+2 csync %.0f | store %.0f | givens %.0f\n",
+              "p1 dot %.0f csync %.0f red %.0f upd %.0f | norm+2 csync %.0f | store %.0f | givens %.0f || step period "
+              "%.0f, between orth kernels (GEMV + launch gaps) %.0f\n",
               rk == 0 ? "rank 0" : "last rank", cnt, d[1] / cnt, d[2] / cnt, d[3] / cnt, d[4] / cnt, d[5] / cnt,
-              d[6] / cnt, d[7] / cnt, d[8] / cnt, d[9] / cnt, d[10] / cnt, d[11] / cnt, d[12] / cnt);
+              d[6] / cnt, d[7] / cnt, d[8] / cnt, d[9] / cnt, d[10] / cnt, d[11] / cnt, d[12] / cnt,
+              np_ ? period / np_ : 0.0, np_ ? outside / np_ : 0.0);
     }
   }
   if (arn_trace) {
