@@ -1076,16 +1076,24 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
   };
 
   int64_t residual_evals = 0;
+  // the previous cycle's true residual (same x, same kernels) is this cycle's r and beta:
+  // reused instead of recomputed (still tallied as the reference's evaluation)
+  bool have_r = false;
+  double next_beta = 0.0;
   while (true) {
     // r = b - A x ; beta = nrm2(r)   (krylov.py:104-106)
     ++residual_evals;
-    int rb = 0;
-    DS_TRY(gemv_launch<T>(ctx, gp, A, lda, x, r, part, EPI_RESID, b, red_a, &rb));
-    finish_resid_kernel<<<1, 256, 0, ctx->stream>>>(red_a, rb, scal + 2);
-    count_launch(ctx);
-    DS_CUDA(cudaMemcpyAsync(hbuf, scal + 2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    DS_CUDA(cudaStreamSynchronize(ctx->stream));
-    const double beta = hbuf[0];
+    double beta = next_beta;
+    if (!have_r) {
+      int rb = 0;
+      DS_TRY(gemv_launch<T>(ctx, gp, A, lda, x, r, part, EPI_RESID, b, red_a, &rb));
+      finish_resid_kernel<<<1, 256, 0, ctx->stream>>>(red_a, rb, scal + 2);
+      count_launch(ctx);
+      DS_CUDA(cudaMemcpyAsync(hbuf, scal + 2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      DS_CUDA(cudaStreamSynchronize(ctx->stream));
+      beta = hbuf[0];
+    }
+    have_r = false;
     const double relres = beta / bnorm;
     if (total_it == 0) history.push_back(relres);
     if (relres <= tol) {
@@ -1119,12 +1127,16 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
     // host synchronisation per cycle instead of one per chunk
     int64_t k = 0, chunk = m;
     int64_t stop_k = m;
+    // one readback per chunk: the device state and the estimates together (pinned)
+    GmDev* h_st = reinterpret_cast<GmDev*>(hbuf + 64);
+    double* h_est = hbuf + 128;
+    static_assert(sizeof(GmDev) <= 64 * sizeof(double), "GmDev staging slot");
     while (true) {
       if (k > 0) {
-        DS_CUDA(cudaMemcpyAsync(hbuf, &st->stop_k, sizeof(int64_t), cudaMemcpyDeviceToHost,
-                                ctx->stream));
+        DS_CUDA(cudaMemcpyAsync(h_st, st, sizeof(GmDev), cudaMemcpyDeviceToHost, ctx->stream));
+        DS_CUDA(cudaMemcpyAsync(h_est, est, (size_t)m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         DS_CUDA(cudaStreamSynchronize(ctx->stream));
-        stop_k = *reinterpret_cast<int64_t*>(hbuf);
+        stop_k = h_st->stop_k;
         if (stop_k <= k || k >= m) break;
       }
       const int64_t kend = std::min<int64_t>(m, k + chunk);
@@ -1218,20 +1230,10 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
       DS_CHECK_LAUNCH();
       chunk = std::min<int64_t>(chunk * 2, 32);
     }
-    GmDev hst;
-    DS_CUDA(cudaMemcpyAsync(&hst, st, sizeof(GmDev), cudaMemcpyDeviceToHost, ctx->stream));
-    DS_CUDA(cudaStreamSynchronize(ctx->stream));
+    GmDev hst = *h_st;  // read by the chunk loop's final readback
     const int inner = (int)std::min<int64_t>(hst.stop_k, m);
     const bool happy = hst.happy != 0;
-    {
-      std::vector<double> e(inner);
-      if (inner > 0) {
-        DS_CUDA(cudaMemcpyAsync(e.data(), est, inner * sizeof(double), cudaMemcpyDeviceToHost,
-                                ctx->stream));
-        DS_CUDA(cudaStreamSynchronize(ctx->stream));
-      }
-      for (int i = 0; i < inner; ++i) history.push_back(e[i]);
-    }
+    for (int i = 0; i < inner; ++i) history.push_back(h_est[i]);
     total_it += inner;
 
     // cycle end: y = H^-1 g ; x += V y   (krylov.py:166-167)
@@ -1246,12 +1248,18 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
       DS_TRY(gemv_launch<T>(ctx, gp2, V, ldv, y, x, part, EPI_AXPY_INTO, nullptr, nullptr,
                             nullptr));
     }
-    DS_CUDA(cudaMemcpyAsync(&hst, st, sizeof(GmDev), cudaMemcpyDeviceToHost, ctx->stream));
-    DS_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (hst.status == DS_ESINGULAR) {
-      set_error("zero diagonal at row %lld", (long long)hst.bad_row);
-      info->error_index = hst.bad_row;
-      return DS_ESINGULAR;
+    auto singular_check = [&]() -> int {
+      if (h_st->status == DS_ESINGULAR) {
+        set_error("zero diagonal at row %lld", (long long)h_st->bad_row);
+        info->error_index = h_st->bad_row;
+        return DS_ESINGULAR;
+      }
+      return DS_OK;
+    };
+    if (sink) {  // the sink sees V / H only for a nonsingular cycle
+      DS_CUDA(cudaMemcpyAsync(h_st, st, sizeof(GmDev), cudaMemcpyDeviceToHost, ctx->stream));
+      DS_CUDA(cudaStreamSynchronize(ctx->stream));
+      DS_TRY(singular_check());
     }
     if (sink) {  // krylov.py:168-169
       hV.resize((size_t)n * (m + 1));
@@ -1271,8 +1279,12 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
       count_launch(ctx);
       DS_CUDA(cudaMemcpyAsync(hbuf, scal + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost,
                               ctx->stream));
+      DS_CUDA(cudaMemcpyAsync(h_st, st, sizeof(GmDev), cudaMemcpyDeviceToHost, ctx->stream));
       DS_CUDA(cudaStreamSynchronize(ctx->stream));
+      DS_TRY(singular_check());  // the least-squares solve's zero-diagonal flag (krylov.py:166)
     }
+    have_r = true;
+    next_beta = hbuf[0];
     const double true_res = sqrt(hbuf[1]) / bnorm_plain;
     if (happy || history.back() <= tol || true_res <= tol) {  // krylov.py:172-175
       history.back() = true_res;
