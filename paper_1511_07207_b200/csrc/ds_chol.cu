@@ -37,85 +37,103 @@ __device__ __forceinline__ float sqrt_rn(float x) { return __fsqrt_rn(x); }
 
 // Factor the nbw x nbw diagonal block W[ib:ib+nbw, ib:ib+nbw] (lower part) with
 // the reference's column loop (direct.py:104-115).  err: first failing index.
+// One thread per block row, the row rotated in registers (x[k] = column i + k at
+// step i, so every step is the same straight-line code): thread i takes the
+// square root, every row below scales its column-i entry and publishes it, then
+// updates its remaining entries with the published column (W[r, j] -= W[r, i] *
+// W[j, i], the reference's order per element).  Two barriers per column.
 template <typename T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kCholW)
     chol_diag_kernel(T* __restrict__ W, int64_t ld, int64_t ib, int nbw, long long* err) {
-  __shared__ T D[kCholW][kCholW + 1];  // D[r][c]
-  __shared__ T s_rinv;
+  __shared__ T colv[2][kCholW + 1];  // step parity: column i of the scaled block, colv[.][j] = W[j, i]
+  __shared__ T s_rinv[2];
   __shared__ int s_fail;
   if (*((volatile long long*)err) >= 0) return;
-  const int tid = threadIdx.x;
-  for (int e = tid; e < nbw * nbw; e += blockDim.x) {
-    const int r = e % nbw, c = e / nbw;
-    if (r >= c) D[r][c] = W[(ib + r) + (ib + c) * ld];
-  }
-  if (tid == 0) s_fail = 0;
+  const int r = threadIdx.x;
+  const bool mine = r < nbw;
+  T x[kCholW];
+#pragma unroll
+  for (int k = 0; k < kCholW; ++k) x[k] = (mine && k <= r) ? W[(ib + r) + (ib + k) * ld] : T(0);
+  if (r == 0) s_fail = 0;
   __syncthreads();
   for (int i = 0; i < nbw; ++i) {
-    if (tid == 0) {
-      const T aii = D[i][i];
+    const int par = i & 1;
+    if (r == i) {
+      const T aii = x[0];
       if (!(aii > T(0)) || !isfinite((double)aii)) {  // direct.py:106-107
         s_fail = 1;
         *err = (long long)(ib + i);
       } else {
-        const T d = sqrt_rn(aii);      // W[i, i] = np.sqrt(aii)
-        D[i][i] = d;
-        s_rinv = div_rn(T(1), d);      // 1.0 / W[i, i] in the array dtype
+        const T d = sqrt_rn(aii);  // W[i, i] = np.sqrt(aii)
+        x[0] = d;
+        s_rinv[par] = div_rn(T(1), d);  // 1.0 / W[i, i] in the array dtype
       }
     }
     __syncthreads();
     if (s_fail) return;
-    const T rinv = s_rinv;
-    for (int r = i + 1 + tid; r < nbw; r += blockDim.x) D[r][i] = mul_rn(rinv, D[r][i]);  // scal
-    __syncthreads();
-    // ger restricted to the panel: W[r, j] += -1 * (W[r, i] * W[j, i]), i < j <= r
-    const int w = nbw - i - 1;
-    for (int e = tid; e < w * w; e += blockDim.x) {
-      const int r = i + 1 + e % w, j = i + 1 + e / w;
-      if (j <= r) D[r][j] = sub_rn(D[r][j], mul_rn(D[r][i], D[j][i]));
+    if (mine && r > i) {
+      x[0] = mul_rn(s_rinv[par], x[0]);  // scal
+      colv[par][r] = x[0];
     }
+    if (mine && r >= i) W[(ib + r) + (ib + i) * ld] = x[0];  // column i of row r is final (lower part only)
     __syncthreads();
-  }
-  for (int e = tid; e < nbw * nbw; e += blockDim.x) {
-    const int r = e % nbw, c = e / nbw;
-    if (r >= c) W[(ib + r) + (ib + c) * ld] = D[r][c];
+    // ger restricted to the panel: x[k] (column j = i + k, i < j <= r) -= W[r, i] * W[j, i]
+    if (mine && r > i) {
+      const T l = x[0];
+#pragma unroll
+      for (int k = 1; k < kCholW; ++k) {
+        const int j = i + k;
+        x[k - 1] = (j <= r) ? sub_rn(x[k], mul_rn(l, colv[par][j < kCholW ? j : kCholW])) : x[k];
+      }
+      x[kCholW - 1] = T(0);
+    }
   }
 }
 
 // Rows r in [r0, n): the same column sequence on W[r, ib:ib+nbw] given the
-// factored diagonal block (direct.py:110-115 restricted to row r).
+// factored diagonal block (direct.py:110-115 restricted to row r).  One thread per
+// row, the row rotated in registers (x[k] = column i + k at step i): the update of
+// step i and the shift by one are one fused pass, so the loop body is short
+// straight-line code (the fully unrolled triangular form was ~13k instructions and
+// thrashed the instruction cache).  The last 32 steps only touch x[0..31].
 template <typename T>
 __global__ void __launch_bounds__(128)
     chol_rows_kernel(T* __restrict__ W, int64_t ld, int64_t n, int64_t ib, int nbw, int64_t r0,
                      const long long* err) {
-  __shared__ T Lc[kCholW][kCholW];  // Lc[i][j] = L[ib + j, ib + i] (column i contiguous)
+  __shared__ __align__(16) T Lr[kCholW][kCholW];  // Lr[i][k] = L[ib + i + k, ib + i] (0 past the block)
   __shared__ T rinv[kCholW];
   if (*((volatile const long long*)err) >= 0) return;
-  for (int e = threadIdx.x; e < nbw * nbw; e += blockDim.x) {
-    const int j = e % nbw, i = e / nbw;
-    Lc[i][j] = j >= i ? W[(ib + j) + (ib + i) * ld] : T(0);
+  for (int e = threadIdx.x; e < kCholW * kCholW; e += blockDim.x) {
+    const int k = e % kCholW, i = e / kCholW;
+    Lr[i][k] = (i < nbw && i + k < nbw) ? W[(ib + i + k) + (ib + i) * ld] : T(0);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < nbw; i += blockDim.x) rinv[i] = div_rn(T(1), Lc[i][i]);
+  for (int i = threadIdx.x; i < nbw; i += blockDim.x) rinv[i] = div_rn(T(1), Lr[i][0]);
   __syncthreads();
   const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   T x[kCholW];
 #pragma unroll
-  for (int i = 0; i < kCholW; ++i) x[i] = i < nbw ? W[r + (ib + i) * ld] : T(0);
+  for (int k = 0; k < kCholW; ++k) x[k] = k < nbw ? W[r + (ib + k) * ld] : T(0);
+  T* out = W + r + ib * ld;
+  const int i_half = nbw < kCholW / 2 ? nbw : kCholW / 2;
+  int i = 0;
+  for (; i < i_half; ++i) {
+    const T l = mul_rn(rinv[i], x[0]);
+    out[(int64_t)i * ld] = l;
+    const T* li = Lr[i];
 #pragma unroll
-  for (int i = 0; i < kCholW; ++i) {
-    if (i < nbw) {
-      const T l = mul_rn(rinv[i], x[i]);
-      x[i] = l;
-#pragma unroll
-      for (int j = i + 1; j < kCholW; ++j)
-        if (j < nbw) x[j] = sub_rn(x[j], mul_rn(l, Lc[i][j]));
-    }
+    for (int k = 1; k < kCholW; ++k) x[k - 1] = sub_rn(x[k], mul_rn(l, li[k]));
+    x[kCholW - 1] = T(0);
   }
+  for (; i < nbw; ++i) {  // columns >= i + 32 are past the block: only x[0..31] live
+    const T l = mul_rn(rinv[i], x[0]);
+    out[(int64_t)i * ld] = l;
+    const T* li = Lr[i];
 #pragma unroll
-  for (int i = 0; i < kCholW; ++i)
-    if (i < nbw) W[r + (ib + i) * ld] = x[i];
+    for (int k = 1; k < kCholW / 2; ++k) x[k - 1] = sub_rn(x[k], mul_rn(l, li[k]));
+    x[kCholW / 2 - 1] = T(0);
+  }
 }
 
 // out[c + k * ldo] = in[k + c * ldi]  for k < rows, c < cols  (32x32 smem tiles):
@@ -191,7 +209,7 @@ int chol_factor_impl(ds_ctx* ctx, int64_t n, T* W, int64_t ld, int64_t b, long l
       for (int64_t sb = ib; sb < ibf; sb += kCholW) {
         const int64_t sbf = std::min<int64_t>(sb + kCholW, ibf);
         const int nbw = (int)(sbf - sb);
-        chol_diag_kernel<T><<<1, 256, 0, ctx->stream>>>(W, ld, sb, nbw, d_err);
+        chol_diag_kernel<T><<<1, kCholW, 0, ctx->stream>>>(W, ld, sb, nbw, d_err);
         count_launch(ctx);
         if (sbf < n) {
           const int64_t rows = n - sbf;
