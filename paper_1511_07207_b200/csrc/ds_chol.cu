@@ -45,7 +45,7 @@ __device__ __forceinline__ float sqrt_rn(float x) { return __fsqrt_rn(x); }
 template <typename T>
 __global__ void __launch_bounds__(kCholW)
     chol_diag_kernel(T* __restrict__ W, int64_t ld, int64_t ib, int nbw, long long* err) {
-  __shared__ T colv[2][kCholW + 1];  // step parity: column i of the scaled block, colv[.][j] = W[j, i]
+  __shared__ T colv[2][2 * kCholW];  // step parity: column i of the scaled block, colv[.][j] = W[j, i]
   __shared__ T s_rinv[2];
   __shared__ int s_fail;
   if (*((volatile long long*)err) >= 0) return;
@@ -77,14 +77,14 @@ __global__ void __launch_bounds__(kCholW)
     }
     if (mine && r >= i) W[(ib + r) + (ib + i) * ld] = x[0];  // column i of row r is final (lower part only)
     __syncthreads();
-    // ger restricted to the panel: x[k] (column j = i + k, i < j <= r) -= W[r, i] * W[j, i]
+    // ger restricted to the panel: x[k] (column j = i + k, i < j <= r) -= W[r, i] * W[j, i].
+    // Entries of columns j > r are updated too (unpredicated): they are never read for
+    // columns <= r (each register slot tracks one column) and never stored.
     if (mine && r > i) {
       const T l = x[0];
+      const T* cv = colv[par] + i;
 #pragma unroll
-      for (int k = 1; k < kCholW; ++k) {
-        const int j = i + k;
-        x[k - 1] = (j <= r) ? sub_rn(x[k], mul_rn(l, colv[par][j < kCholW ? j : kCholW])) : x[k];
-      }
+      for (int k = 1; k < kCholW; ++k) x[k - 1] = sub_rn(x[k], mul_rn(l, cv[k]));
       x[kCholW - 1] = T(0);
     }
   }
