@@ -139,7 +139,23 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- helpers
-def spd_fast_device(n, seed, torch, device):
+def lib_matvec(be, A_t, x_t):
+    """y = colmajor(A_t) @ x with the library's own GEMV (no cuBLAS even in the setup);
+    torch's row-major A_t read as column-major is A_t^T."""
+    from ctypes import c_void_p
+    import torch
+    from paper_1511_07207_b200 import _lib
+    n = x_t.shape[0]
+    code = _lib.DS_F64 if x_t.dtype == torch.float64 else _lib.DS_F32
+    y = torch.empty_like(x_t)
+    torch.cuda.synchronize()
+    _lib.check(be.ctx.lib.ds_gemv(be.ctx.handle, code, n, n, c_void_p(A_t.data_ptr()), n,
+                                  c_void_p(x_t.data_ptr()), c_void_p(y.data_ptr())))
+    be.ctx.synchronize()
+    return y
+
+
+def spd_fast_device(n, seed, torch, device, be):
     """Synthetic dense SPD: A = (R + R^T)/2 + sqrt(n) I, R ~ U[-1,1] (seeded, on the GPU).
     The symmetric part has a semicircle spectrum of radius ~0.82 sqrt(n), so
     lambda(A) in ~[0.18, 1.82] sqrt(n): SPD with kappa ~ 10, which keeps a
@@ -151,8 +167,7 @@ def spd_fast_device(n, seed, torch, device):
     A.add_(A.t().clone()).mul_(0.5)
     A.diagonal().add_(float(n) ** 0.5)
     xt = torch.rand(n, dtype=torch.float64, device=device, generator=g).mul_(2.0).sub_(1.0)
-    b = A @ xt
-    return A, b
+    return A, lib_matvec(be, A, xt)  # A symmetric: row-major == column-major
 
 
 def spd_fast_host(n, seed):
@@ -252,7 +267,7 @@ def run_b200(args):
         return bench_sharded_cg(args, torch, dev, be)
 
     # ---- inputs: synthetic SPD generated on the device, staged into a DeviceArray
-    At, bt = spd_fast_device(n, 0, torch, dev)
+    At, bt = spd_fast_device(n, 0, torch, dev, be)
     dA = DeviceArray(ctx, (n, n), np.float64)
     assert dA.ld == n
     ctx.lib.ds_memcpy_d2d(ctx.handle, dA.ptr, At.data_ptr(), 8 * n * n)
@@ -432,7 +447,7 @@ def bench_gmres(args, torch, stream, be, generate_problem, ProblemSpec, gmres_so
             "value": round(rep.iterations / (ms / 1e3), 1), "unit": "inner iters/s", "ms_per_step": round(ms, 4)}
 
 
-def nonsym_fast_device(n, seed, torch, device, dtype):
+def nonsym_fast_device(n, seed, torch, device, dtype, be):
     """Synthetic dense nonsymmetric A = R + 1.5 sqrt(n) I, R ~ U[-1,1] (seeded, on the GPU, in the
     target dtype; the harness recipe needs ~130 GB of fp64 temporaries at n=65536).  R's spectrum
     fills a disk of radius sqrt(n/3) (circular law), so GMRES contracts by ~0.38 per step: one
@@ -445,7 +460,7 @@ def nonsym_fast_device(n, seed, torch, device, dtype):
         A[c0:c0 + blk.shape[0]] = blk.mul_(2.0).sub_(1.0)
     A.diagonal().add_(1.5 * float(n) ** 0.5)
     xt = torch.rand(n, dtype=dtype, device=device, generator=g).mul_(2.0).sub_(1.0)
-    return A, A.t() @ xt  # A is stored transposed (torch row-major) -> column-major A^T; b = A^T x
+    return A, lib_matvec(be, A, xt)  # torch row-major A read column-major is A^T: b = A^T x
 
 
 def bench_gmres_c5(args, torch, dev, stream, be, gmres_solve, SolverConfig, hbm_peak):
@@ -454,7 +469,7 @@ def bench_gmres_c5(args, torch, dev, stream, be, gmres_solve, SolverConfig, hbm_
 
     n, m = args.gmres_n, 50
     ctx = be.ctx
-    At, bt = nonsym_fast_device(n, 3, torch, dev, torch.float32)
+    At, bt = nonsym_fast_device(n, 3, torch, dev, torch.float32, be)
     dA = DeviceArray(ctx, (n, n), np.float32)
     ctx.lib.ds_memcpy_d2d(ctx.handle, dA.ptr, At.data_ptr(), 4 * n * n)
     db = DeviceArray(ctx, (n,), np.float32)

@@ -1,8 +1,8 @@
 #!/bin/bash
 # Refresh the ncu evidence under gpurun_out/ (then summarised into profiles/):
 #   launch lists (gpu__time_duration.sum, --clock-control none) of the bench headline command,
-#   of LU n=16384 and of one GMRES(30) C2 cycle; --set full captures of the GEMV (bench n),
-#   the K=512 trailing GEMM and one LU panel launch.
+#   of LU n=16384, Cholesky n=16384 and of one GMRES(30) C2 cycle; --set full captures of the GEMV
+#   (bench n), the K=512 trailing GEMM, one LU panel launch of each kernel and the GMRES cluster step.
 tag=${1:-s3}
 out=gpurun_out
 mkdir -p $out
@@ -14,6 +14,12 @@ timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $out/launches_lu_$tag.csv python tools/profile_run.py lu 16384 > /dev/null 2>&1; echo "lu list $?"
 timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file $out/launches_gmres_$tag.csv python tools/profile_run.py gmres 4096 > /dev/null 2>&1; echo "gmres list $?"
+timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file $out/launches_chol_$tag.csv python tools/profile_run.py chol 16384 > /dev/null 2>&1; echo "chol list $?"
+timeout 600 $NCU --set full --clock-control none --import-source on -k regex:arnoldi_orth_cluster -s 25 -c 1 \
+  -o $out/orth_full_$tag -f python tools/profile_run.py gmres 4096 > /dev/null 2>&1; echo "orth full $?"
+timeout 600 $NCU --set full --clock-control none --import-source on -k regex:lu_panel_warp -s 10 -c 1 \
+  -o $out/panelw_full_$tag -f python tools/profile_run.py lu 16384 > /dev/null 2>&1; echo "poller panel full $?"
 timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemv_partial -s 2 -c 1 \
   -o $out/gemv_full_$tag -f python tools/profile_run.py gemv 32768 > /dev/null 2>&1; echo "gemv full $?"
 timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemm64 -s 1 -c 1 \

@@ -1,12 +1,12 @@
-"""Short driver for ncu captures: python tools/profile_run.py {cg,gemv,lu,gmres} [n]"""
+"""Short driver for ncu captures: python tools/profile_run.py {cg,gemv,lu,gmres,chol,gemm,trsm} [n]"""
 import os
 import sys
 
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_1511_07207_b200 import (SolverConfig, cg_solve, get_backend, gmres_solve,  # noqa: E402
-                                   lu_factor_blocked)
+from paper_1511_07207_b200 import (SolverConfig, cg_solve, cholesky_factor, get_backend,  # noqa: E402
+                                   gmres_solve, lu_factor_blocked)
 from paper_1511_07207_b200.device import DeviceArray  # noqa: E402
 from paper_1511_07207_b200.harness import ProblemSpec, generate_problem  # noqa: E402
 
@@ -57,5 +57,13 @@ elif what == "gmres":
     A, b, _ = generate_problem(ProblemSpec("general_nonsymmetric", n, 0))
     dA, db, dx0 = be.stage_in(A, b, np.zeros(n))
     gmres_solve(dA, db, dx0, SolverConfig(tolerance=1e-300, restart_m=30, max_iterations=30), be)
+    ctx.synchronize()
+elif what == "chol":
+    n = int(sys.argv[2]) if len(sys.argv) > 2 else 16384
+    R = rng.uniform(-1, 1, (n, n))
+    A = np.asfortranarray((R + R.T) * 0.5 + np.sqrt(n) * np.eye(n))
+    del R
+    dA = be.stage_in(A)
+    cholesky_factor(dA, 64, be)
     ctx.synchronize()
 print("done", what)
