@@ -536,16 +536,19 @@ template int ger_launch<float>(ds_ctx*, int64_t, int64_t, const float*, int64_t,
 // symmetry gate (krylov.py:41-44): max|A - A^T| (difference rounded in T, as
 // NumPy's A - A.T) and max|A|, over upper-triangular 32x32 tile pairs.
 // ============================================================================
+// max|A - A^T| and max|A| (krylov.py:42-44) over 64 x 64 tile pairs (bi <= bj): every
+// thread issues its 32 loads of both tiles at once (512-byte column runs), then the
+// transposed tile goes through shared memory.  Each element is read once.
+constexpr int kSymT = 64;
 template <typename T>
 __global__ void __launch_bounds__(256)
     symcheck_kernel(int64_t n, const T* __restrict__ A, int64_t lda, double* red) {
-  __shared__ T tl[32][33];
-  __shared__ T tu[32][33];
+  __shared__ T tu[kSymT][kSymT + 1];  // the transposed tile; the (bi,bj) tile stays in registers
   __shared__ double sm[32];
-  const int64_t nt = ceil_div(n, 32);
+  const int64_t nt = ceil_div(n, (int64_t)kSymT);
   const int64_t npairs = nt * (nt + 1) / 2;
   double dmax = 0.0, amax = 0.0;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4
   for (int64_t p = blockIdx.x; p < npairs; p += gridDim.x) {
     // p -> (bi, bj) with bi <= bj, row-major over the upper triangle
     int64_t bi = (int64_t)((2.0 * nt + 1.0 - sqrt((2.0 * nt + 1.0) * (2.0 * nt + 1.0) - 8.0 * p)) / 2.0);
@@ -553,21 +556,29 @@ __global__ void __launch_bounds__(256)
     while (bi > 0 && bi * nt - bi * (bi - 1) / 2 > p) --bi;
     while ((bi + 1) * nt - (bi + 1) * bi / 2 <= p) ++bi;
     const int64_t bj = bi + (p - (bi * nt - bi * (bi - 1) / 2));
-    const int64_t r0 = bi * 32, c0 = bj * 32;
-    __syncthreads();
-    for (int k = ty; k < 32; k += 8) {
-      const int64_t r = r0 + tx, c = c0 + k;  // tile (bi,bj): element (r, c)
-      tl[k][tx] = (r < n && c < n) ? A[r + c * lda] : T(0);
+    const int64_t r0 = bi * kSymT, c0 = bj * kSymT;
+    T vl[kSymT / 4], vu[kSymT / 4];
+#pragma unroll
+    for (int q = 0; q < kSymT / 4; ++q) {
+      const int k = ty + 4 * q;
+      const int64_t r = r0 + tx, c = c0 + k;    // tile (bi,bj): element (r, c)
+      vl[q] = (r < n && c < n) ? A[r + c * lda] : T(0);
       const int64_t r2 = c0 + tx, c2 = r0 + k;  // tile (bj,bi): element (r2, c2)
-      tu[k][tx] = (r2 < n && c2 < n) ? A[r2 + c2 * lda] : T(0);
+      vu[q] = (r2 < n && c2 < n) ? A[r2 + c2 * lda] : T(0);
+    }
+    __syncthreads();  // the previous pair's compare is done with the tiles
+#pragma unroll
+    for (int q = 0; q < kSymT / 4; ++q) {
+      tu[ty + 4 * q][tx] = vu[q];
+      amax = nanmax(amax, fabs((double)vl[q]));
+      amax = nanmax(amax, fabs((double)vu[q]));
     }
     __syncthreads();
-    for (int k = ty; k < 32; k += 8) {
+#pragma unroll
+    for (int q = 0; q < kSymT / 4; ++q) {
+      const int k = ty + 4 * q;
       // element (r0+tx, c0+k) vs its transpose (c0+k, r0+tx) = tu[tx][k]
-      const T a = tl[k][tx], b = tu[tx][k];
-      dmax = nanmax(dmax, fabs((double)sub_rn(a, b)));
-      amax = nanmax(amax, fabs((double)a));
-      amax = nanmax(amax, fabs((double)tu[k][tx]));
+      dmax = nanmax(dmax, fabs((double)sub_rn(vl[q], tu[tx][k])));
     }
   }
   dmax = block_nanmax(dmax, sm);
@@ -580,9 +591,9 @@ __global__ void __launch_bounds__(256)
 
 template <typename T>
 int symcheck_launch(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, double* red, int* nblk) {
-  const int64_t nt = ceil_div(n, 32);
+  const int64_t nt = ceil_div(n, (int64_t)kSymT);
   const int64_t npairs = nt * (nt + 1) / 2;
-  int g = (int)std::min<int64_t>(npairs, (int64_t)ctx->num_sms * 8);
+  int g = (int)std::min<int64_t>(npairs, (int64_t)ctx->num_sms * 6);  // 6 x 33 KB smem per SM
   *nblk = g;
   symcheck_kernel<T><<<g, 256, 0, ctx->stream>>>(n, A, lda, red);
   count_launch(ctx);
