@@ -721,6 +721,10 @@ __global__ void __launch_bounds__(kOrthThreads, 1)
   // w = A v_k: the GEMV's chunk partials summed here, in chunk order (gemv_reduce_kernel's
   // order, so w is bitwise the EPI_STORE result), up to 32 loads in flight
   for (int r = tid; r < nr; r += blockDim.x) {
+    if (gpart == nullptr) {  // w already summed by the GEMV's reduce kernel
+      wv[r] = (double)w[r0 + r];
+      continue;
+    }
     const double* pr = gpart + r0 + r;
     double s = 0.0;
     for (int64_t c0 = 0; c0 < nchunks; c0 += 32) {
@@ -963,6 +967,7 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
   // (16 non-portable, else 8) that the device can co-schedule; rows per CTA <= 4096
   int orth_cl = 0;
   size_t orth_smem = 0;
+  bool orth_fold = true;
   static const bool pdl_on = [] {  // programmatic dependent launch in the cluster path
     const char* e = getenv("DENSOLVE_PDL");
     return !(e && e[0] == '0');
@@ -1007,6 +1012,10 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
         }
         orth_cl = bc;
         orth_smem = (size_t)ceil_div(ceil_div(n, (int64_t)bc), 4) * 4 * sizeof(double);
+        // the cluster sums the GEMV partials of its rows itself only while that is a small
+        // read per CTA (C2: 128 KB); at n = 65536 (1.2 MB per CTA, ~40 us on 16 SMs) the
+        // reduce kernel on every SM is faster
+        orth_fold = ceil_div(n, (int64_t)bc) * gp.nchunks * (int64_t)sizeof(double) <= 256 * 1024;
       }
     }
   }
@@ -1146,7 +1155,9 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
         T* w = V + (k + 1) * ldv;
         const int kc = (int)k + 1;
         if (orth_cl > 0) {  // streamed GEMV on every SM + one-cluster orthogonalisation
-          if (pdl_on)
+          if (!orth_fold)  // large n: the reduce kernel on every SM writes w
+            DS_TRY(gemv_launch<T>(ctx, gp, A, lda, vk, w, part, EPI_STORE, nullptr, nullptr, nullptr, gt));
+          else if (pdl_on)
             DS_TRY(gemv_partial_pdl_launch<T>(ctx, gp, A, lda, vk, part, gt));
           else
             DS_TRY(gemv_launch<T>(ctx, gp, A, lda, vk, w, part, EPI_PARTIAL, nullptr, nullptr, nullptr, gt));
@@ -1166,8 +1177,9 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
           lc.numAttrs = pdl_on ? 2 : 1;
           const int passes = orth == DS_ORTH_CLASSICAL ? 1 : 2;
           DS_CUDA(cudaLaunchKernelEx(&lc, arnoldi_orth_cluster_kernel<T>, n, V, ldv, (int)k, passes, H, Hraw, ldh, g,
-                                     cs, sn, est, st, tol, total_it, cap, gt, (const double*)part,
-                                     (int64_t)gp.nchunks, orth_trace));
+                                     cs, sn, est, st, tol, total_it, cap, gt,
+                                     orth_fold ? (const double*)part : nullptr, (int64_t)gp.nchunks,
+                                     orth_trace));
           count_launch(ctx);
           continue;
         }
