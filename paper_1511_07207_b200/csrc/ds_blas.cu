@@ -754,6 +754,14 @@ __global__ void __launch_bounds__(gemm64::THREADS, 2)
                                (int64_t)s * BK);
     cp_async_commit();
   }
+  // interior tiles (the bulk of every LU / SYRK update): the cp.async sources are two
+  // running pointers plus constant strides, no per-chunk index math or bounds checks
+  const bool interior = VEC16 && m0 + BM <= m && n0 + BN <= n;
+  const int tid = threadIdx.x;
+  const double* a_src = A + (int64_t)(tid / (BM / 2)) * lda + m0 + (tid % (BM / 2)) * 2;  // chunk it: + it * 4 lda
+  const double* b_src = B + (n0 + tid / (BK / 2)) * ldb + (tid % (BK / 2)) * 2;             // chunk it: + it * 32 ldb
+  const int a_dst = (tid / (BM / 2)) * LDA_S + (tid % (BM / 2)) * 2;
+  const int b_dst = (tid / (BK / 2)) * LDB_S + (tid % (BK / 2)) * 2;
   for (int64_t kt = 0; kt < ktiles; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
@@ -761,8 +769,22 @@ __global__ void __launch_bounds__(gemm64::THREADS, 2)
     const int64_t pf = kt + STAGES - 1;
     if (pf < ktiles) {
       const int s = (int)(pf % STAGES);
-      gemm64_load_stage<VEC16>(As + s * A_STAGE, Bs + s * B_STAGE, A, lda, B, ldb, m, n, k, m0, n0,
-                               pf * BK);
+      if (interior && (pf + 1) * BK <= k) {
+        const int64_t k0 = pf * BK;
+        const double* ap = a_src + k0 * lda;
+        const double* bp = b_src + k0;
+        double* as_ = As + s * A_STAGE + a_dst;
+        double* bs_ = Bs + s * B_STAGE + b_dst;
+#pragma unroll
+        for (int it = 0; it < (BK * BM / 2) / THREADS; ++it)
+          cp_async_16(as_ + it * (THREADS / (BM / 2)) * LDA_S, ap + (int64_t)it * (THREADS / (BM / 2)) * lda, 16);
+#pragma unroll
+        for (int it = 0; it < (BK * BN / 2) / THREADS; ++it)
+          cp_async_16(bs_ + it * (THREADS / (BK / 2)) * LDB_S, bp + (int64_t)it * (THREADS / (BK / 2)) * ldb, 16);
+      } else {
+        gemm64_load_stage<VEC16>(As + s * A_STAGE, Bs + s * B_STAGE, A, lda, B, ldb, m, n, k, m0, n0,
+                                 pf * BK);
+      }
     }
     cp_async_commit();
     const int s = (int)(kt % STAGES);
