@@ -620,10 +620,10 @@ __global__ void finish_max2_kernel(const double* red, int nblk, double* out) {
 
 // ============================================================================
 // GEMM — FP64 on the DMMA tensor pipe.  out = beta*C + alpha*(A B).
-//   CTA tile 128x64, 8 warps (4x2) of 32x32, BK=16 k-slab, 4-stage cp.async (96 KB, 2 CTAs/SM;
-//   4 stages measured 32.3 vs 31.4 TFLOP/s for 3 at K = 512)
-//   pipeline, mma.sync.m8n8k4.row.col.f64 (native DMMA.8x8x4; the only FP64
-//   tensor-core instruction on sm_100a — tcgen05 has no kind::f64).
+//   CTA tile 128x64, 8 warps (4x2) of 32x32, BK=16 k-slab, 4-stage cp.async pipeline
+//   (96 KB, 2 CTAs/SM; 4 stages measured 32.3 vs 31.4 TFLOP/s for 3 at K = 512),
+//   mma.sync.m8n8k4.row.col.f64 (native DMMA.8x8x4; the only FP64 tensor-core
+//   instruction on sm_100a — tcgen05 has no kind::f64).
 // ============================================================================
 namespace gemm64 {
 constexpr int BM = 128, BN = 64, BK = 16, STAGES = 4;
