@@ -1391,6 +1391,7 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
   // plus host enqueue times; printed at the end
   const bool timeline = getenv("DENSOLVE_LU_TIMELINE") != nullptr;
   std::vector<cudaEvent_t> tev;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> side_ev;  // look-ahead panel factorizations
   std::vector<double> thost;
   auto host_us = [] {
     timespec ts;
@@ -1441,7 +1442,17 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
       DS_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_a, 0));
       cudaStream_t main = ctx->stream;
       ctx->stream = ctx->side;
+      cudaEvent_t s0 = nullptr, s1 = nullptr;
+      if (timeline) {
+        cudaEventCreate(&s0);
+        cudaEventCreate(&s1);
+        cudaEventRecord(s0, ctx->side);
+      }
       const int rc = factor_outer(bf, bf2);
+      if (timeline) {
+        cudaEventRecord(s1, ctx->side);
+        side_ev.push_back({s0, s1});
+      }
       ctx->stream = main;
       DS_TRY(rc);
       DS_CUDA(cudaEventRecord(ctx->ev_b, ctx->side));
@@ -1478,6 +1489,14 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
       float ms = 0;
       cudaEventElapsedTime(&ms, tev[k - 1], tev[k]);
       fprintf(stderr, " %.2f", ms);
+    }
+    fprintf(stderr, "\n[lu timeline] look-ahead panel factorization on the side stream (ms):");
+    for (auto& pe : side_ev) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, pe.first, pe.second);
+      fprintf(stderr, " %.2f", ms);
+      cudaEventDestroy(pe.first);
+      cudaEventDestroy(pe.second);
     }
     fprintf(stderr, "\n");
     for (auto e : tev) cudaEventDestroy(e);
