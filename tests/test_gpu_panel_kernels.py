@@ -4,7 +4,7 @@ rounding), so the whole blocked factorization must be BITWISE identical whicheve
 kernel runs each panel.  The kernel choice is read once per process
 (DENSOLVE_PANEL_KERNEL: 0 = size-based default, 1 = poller kernel wherever it fits,
 2 = CTA-synchronous kernel only), hence one subprocess per setting.  Sizes cover one
-CTA (rows <= 224), 2..40 CTAs, more than 40 CTAs, ragged tails and ragged b."""
+CTA (rows <= 224), 2..40 CTAs, more than 40 CTAs, ragged tails, ragged b, fp64 and fp32."""
 import os
 import subprocess
 import sys
@@ -24,14 +24,15 @@ import numpy as np
 sys.path.insert(0, {root!r})
 from paper_1511_07207_b200 import get_backend, lu_factor_blocked
 be = get_backend("b200")
-for n, b, seed in {cases!r}:
-    A = np.asfortranarray(np.random.default_rng(seed).uniform(-1, 1, (n, n)))
+for n, b, seed, dt in {cases!r}:
+    A = np.asfortranarray(np.random.default_rng(seed).uniform(-1, 1, (n, n)).astype(dt))
     f = lu_factor_blocked(A, b, be)
     h = hashlib.sha256(np.ascontiguousarray(f.packed).tobytes() + np.asarray(f.pivots, np.int64).tobytes())
     print(n, b, h.hexdigest())
 """
 
-CASES = [(200, 64, 1), (1000, 48, 2), (3000, 64, 3), (9000, 64, 4), (12000, 64, 5)]
+CASES = [(200, 64, 1, "float64"), (1000, 48, 2, "float64"), (3000, 64, 3, "float64"), (9000, 64, 4, "float64"),
+         (12000, 64, 5, "float64"), (3000, 64, 6, "float32"), (700, 40, 7, "float32")]
 
 
 def _run(force):
