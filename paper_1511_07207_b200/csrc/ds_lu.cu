@@ -1480,7 +1480,7 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
     }
     std::sort(d.begin(), d.end(), [](auto& x, auto& y) { return x.first > y.first; });
     fprintf(stderr, "[lu timeline] n=%lld steps=%zu device %.2f ms, host enqueue %.2f ms, host total %.2f ms; slowest:",
-            (long long)w, d.size(), tot, thost.back() - thost.front(), hend - thost.front());
+            (long long)w, d.size(), tot, (thost.back() - thost.front()) / 1e3, (hend - thost.front()) / 1e3);
     for (size_t k = 0; k < std::min<size_t>(6, d.size()); ++k)
       fprintf(stderr, " #%d %.2f ms (enq at %.2f ms)", d[k].second, d[k].first,
               (thost[d[k].second] - thost.front()) / 1e3);
