@@ -248,6 +248,10 @@ def run_b200(args):
     if sharded:
         import torch.distributed as dist
         if not dist.is_initialized():
+            # --force-sharded without torchrun: a world of one on 127.0.0.1
+            for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("LOCAL_RANK", "0"),
+                         ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29531")):
+                os.environ.setdefault(k, v)
             dist.init_process_group("nccl", device_id=dev)
     from paper_1511_07207_b200 import (SolverConfig, cg_solve, get_backend, gmres_solve,
                                        lu_factor_blocked, pinned_empty)
@@ -264,7 +268,12 @@ def run_b200(args):
     cfg = SolverConfig(tolerance=1e-300, max_iterations=iters)
 
     if sharded:
-        return bench_sharded_cg(args, torch, dev, be)
+        try:
+            return bench_sharded_cg(args, torch, dev, be)
+        finally:
+            import torch.distributed as dist
+            if dist.is_initialized():
+                dist.destroy_process_group()
 
     # ---- inputs: synthetic SPD generated on the device, staged into a DeviceArray
     At, bt = spd_fast_device(n, 0, torch, dev, be)
