@@ -265,14 +265,22 @@ def _symmetry_gate(A_blk, n, n_loc, comm, ops, dtype):
 
     G = comm.size
     N = G * n_loc
-    # send buffer: for each destination r, our block rows(q) x cols(r), column-major
-    send = torch.zeros((G, n_loc, n_loc), dtype=A_blk.dtype, device=A_blk.device)
-    for r in range(G):
-        c0, c1 = r * n_loc, min(n, (r + 1) * n_loc)
-        if c1 > c0:
-            send[r, : c1 - c0, :] = A_blk[c0:c1, :]
-    recv = torch.empty_like(send)
-    comm.alltoall(recv.reshape(-1), send.reshape(-1))
+    # send buffer: for each destination r, our block rows(q) x cols(r), column-major.  The
+    # row block is stored (N, n_loc) with zero rows past n, so those G blocks are already
+    # contiguous: a view, no copy of the local matrix; one rank compares A with itself
+    if A_blk.is_contiguous() and A_blk.shape[0] == N:
+        send = A_blk.view(G, n_loc, n_loc)
+    else:
+        send = torch.zeros((G, n_loc, n_loc), dtype=A_blk.dtype, device=A_blk.device)
+        for r in range(G):
+            c0, c1 = r * n_loc, min(n, (r + 1) * n_loc)
+            if c1 > c0:
+                send[r, : c1 - c0, :] = A_blk[c0:c1, :]
+    if G == 1:
+        recv = send
+    else:
+        recv = torch.empty_like(send)
+        comm.alltoall(recv.reshape(-1), send.reshape(-1))
     md, am = 0.0, 0.0
     for r in range(G):
         c0, c1 = r * n_loc, min(n, (r + 1) * n_loc)
