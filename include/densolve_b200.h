@@ -256,6 +256,27 @@ int ds_relative_residual(ds_ctx* ctx, int dtype, int64_t n, const void* d_A, int
 int ds_symmetry_check(ds_ctx* ctx, int dtype, int64_t n, const void* d_A, int64_t lda,
                       double* h_maxdiff, double* h_amax);
 
+/* ---- seeded input generators at config scale (harness.py:73-104) -----------
+ * Replaces harness.generate_problem / _rng (harness.py:70-104) for sizes whose
+ * host recipe is infeasible (spd n=32768 crashes in NumPy's syrk; C5 needs
+ * ~130 GB of fp64 temporaries).  h_pcg = {state_hi, state_lo,
+ * inc_hi, inc_lo} of np.random.default_rng([seed, n, kind]).bit_generator right
+ * after seeding (the SeedSequence hashing stays on the host).  The uniform draws,
+ * elementwise combinations, NumPy-pairwise row sums and dtype casts are bitwise
+ * NumPy's; M^T M (spd) and b = A x_true use the library's DMMA GEMM / GEMV. */
+#define DS_GEN_DIAG_DOMINANT 1        /* harness.py:84-87 */
+#define DS_GEN_SPD 2                  /* harness.py:88-91 */
+#define DS_GEN_GENERAL_NONSYMMETRIC 3 /* harness.py:92-98 */
+#define DS_GEN_UNIFORM 100            /* A = U[-1,1] (C3 pivoting family) */
+/* (rows x cols) C-order draw of Generator.uniform(low, high) starting at stream
+ * position `offset`; stored row-major (colmajor=0, out[i*ld+j]) or as
+ * np.asfortranarray of it (colmajor=1, out[i+j*ld]); dtype cast after the draw. */
+int ds_rng_uniform(ds_ctx* ctx, int dtype, const uint64_t* h_pcg, uint64_t offset, int64_t rows,
+                   int64_t cols, double low, double high, int colmajor, void* d_out, int64_t ld);
+/* A (F-order, lda), and optionally x_true and b = A x_true (NULL to skip). */
+int ds_generate(ds_ctx* ctx, int kind, int dtype, int64_t n, const uint64_t* h_pcg, void* d_A,
+                int64_t lda, void* d_b, void* d_x_true);
+
 /* ---- multi-GPU building blocks ---------------------------
  * One process per GPU; the host driver (paper_1511_07207_b200/distributed.py)
  * issues the collectives (torch.distributed / NCCL) between these calls.

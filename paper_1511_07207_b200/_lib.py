@@ -13,7 +13,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
-from ctypes import (POINTER, c_char_p, c_double, c_int, c_int8, c_int32, c_int64, c_size_t,
+from ctypes import (POINTER, c_char_p, c_double, c_int, c_int8, c_int32, c_int64, c_size_t, c_uint64,
                     c_void_p)
 
 import numpy as np
@@ -121,6 +121,10 @@ _SIGNATURES = {
                                      c_void_p, POINTER(c_double)]),
     "ds_symmetry_check": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, POINTER(c_double),
                                   POINTER(c_double)]),
+    # seeded generators at config scale (ds_gen.cu)
+    "ds_rng_uniform": (c_int, [c_void_p, c_int, c_void_p, c_uint64, c_int64, c_int64, c_double, c_double, c_int,
+                               c_void_p, c_int64]),
+    "ds_generate": (c_int, [c_void_p, c_int, c_int, c_int64, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
     # multi-GPU building blocks
     "ds_vec_parts": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p]),
     "ds_dot_dev": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p, c_void_p]),
