@@ -1,21 +1,26 @@
 #!/usr/bin/env python
 """Benchmark of the B200 densolve hot path (BASELINE.json metric).
 
-Headline (``value``): CG iterations/s on a dense SPD n=32768 fp64 system
-(config C4) with A resident in HBM; one *step* = one ``cg_solve`` call with
-tolerance 1e-300 and max_iterations=ITERS (the reference's own fixed-iteration
-idiom, tests/test_krylov.py:188-191), i.e. symmetry gate + setup + ITERS
-iterations.  ``e2e`` is the same metric through the public API with pinned
-HOST buffers (A, b, x0 uploaded and x downloaded inside every step).
-``components`` adds GMRES(30) n=4096 fp64 (C2) and GMRES(50) n=65536 fp32 (C5),
-one full cycle per step; blocked LU (b=64) fp64 GFLOP/s at n=16384 (C3) and
-n=32768 (C5 per-GPU size); BiCGSTAB and Cholesky on the C4 matrix.
+Headline (``value``): CG iterations/s on config C4, the reference's own spd recipe
+(harness.py:88-91: M ~ U[-1,1] from default_rng([0, n, 2]), A = M^T M + n I, exactly
+symmetric) at n=32768 fp64, generated on the device by the library's bit-identical
+PCG64 stream (csrc/ds_gen.cu), A resident in HBM.  One *step* = one ``cg_solve`` call
+with tolerance 1e-300 and max_iterations=ITERS (the reference's fixed-iteration idiom,
+tests/test_krylov.py:188-191): symmetry gate + setup + ITERS iterations.  ``e2e`` is the
+same metric through the public API with pinned HOST buffers (A, b, x0 uploaded and x
+downloaded inside every step).  ``components`` adds GMRES(30) C2 and fp64 n=32768,
+GMRES(50) n=65536 fp32 (C5), BiCGSTAB and Cholesky on the C4 matrix, blocked LU (b=64)
++ lu_solve at n=16384 (C3) and n=32768 (C5 per-GPU size) on the uniform recipe, each
+with the reference CPU path timed beside it on this host.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
---impl reference times the reference CPU path (the NumPy restatement in
-oracle/, which makes the same NumPy/BLAS calls as the reference package) on
-the host cores, same metric and workload, rank 0 only.
+--impl reference times the UNMODIFIED reference package (baseline/_ref, installed from
+/root/reference with pip) through its public API -- densolve.cg_solve(A, b, x0,
+SolverConfig(tolerance=1e-300, max_iterations=ITERS), get_backend("blocked")) -- on the
+same matrix bytes (generated once, outside the timed region, by the same device
+generator and downloaded), the same ITERS per step and the same config, on the host
+cores, rank 0 only.
 """
 from __future__ import annotations
 
@@ -139,47 +144,6 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- helpers
-def lib_matvec(be, A_t, x_t):
-    """y = colmajor(A_t) @ x with the library's own GEMV (no cuBLAS even in the setup);
-    torch's row-major A_t read as column-major is A_t^T."""
-    from ctypes import c_void_p
-    import torch
-    from paper_1511_07207_b200 import _lib
-    n = x_t.shape[0]
-    code = _lib.DS_F64 if x_t.dtype == torch.float64 else _lib.DS_F32
-    y = torch.empty_like(x_t)
-    torch.cuda.synchronize()
-    _lib.check(be.ctx.lib.ds_gemv(be.ctx.handle, code, n, n, c_void_p(A_t.data_ptr()), n,
-                                  c_void_p(x_t.data_ptr()), c_void_p(y.data_ptr())))
-    be.ctx.synchronize()
-    return y
-
-
-def spd_fast_device(n, seed, torch, device, be):
-    """Synthetic dense SPD: A = (R + R^T)/2 + sqrt(n) I, R ~ U[-1,1] (seeded, on the GPU).
-    The symmetric part has a semicircle spectrum of radius ~0.82 sqrt(n), so
-    lambda(A) in ~[0.18, 1.82] sqrt(n): SPD with kappa ~ 10, which keeps a
-    fixed 100-iteration CG far from underflow (rate ~0.5 per iteration)."""
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    A = torch.rand((n, n), dtype=torch.float64, device=device, generator=g)
-    A.mul_(2.0).sub_(1.0)
-    A.add_(A.t().clone()).mul_(0.5)
-    A.diagonal().add_(float(n) ** 0.5)
-    xt = torch.rand(n, dtype=torch.float64, device=device, generator=g).mul_(2.0).sub_(1.0)
-    return A, lib_matvec(be, A, xt)  # A symmetric: row-major == column-major
-
-
-def spd_fast_host(n, seed):
-    rng = np.random.default_rng([seed, n, 2])
-    A = rng.uniform(-1.0, 1.0, size=(n, n))
-    A += A.T.copy()
-    A *= 0.5
-    A[np.diag_indices(n)] += float(n) ** 0.5
-    xt = rng.uniform(-1.0, 1.0, size=n)
-    return np.asfortranarray(A), A @ xt
-
-
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -187,55 +151,145 @@ def dist_env():
     return ws, rank, local
 
 
+def host_info():
+    """CPU model, core count, RAM and the BLAS thread pools the CPU legs run on."""
+    info = {"cores": os.cpu_count() or 1}
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    info["cpu_model"] = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemTotal"):
+                    info["ram_gib"] = round(int(line.split()[1]) / 2 ** 20, 1)
+                    break
+    except OSError:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+        info["blas"] = [{k: d.get(k) for k in ("internal_api", "version", "num_threads", "threading_layer")}
+                        for d in threadpool_info()]
+    except Exception:  # noqa: BLE001 - informational
+        pass
+    return info
+
+
+def ref_densolve():
+    """The UNMODIFIED reference package, pip-installed from /root/reference into
+    baseline/_ref (__graft_entry__.build()); it travels to the GPU box with the repo."""
+    p = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(p, "densolve")):
+        raise ImportError(f"{p}/densolve is missing (install: see DESIGN.md §8)")
+    if p not in sys.path:
+        sys.path.insert(0, p)
+    import densolve
+    return densolve
+
+
+def c4_config(n, iters, ws):
+    """The workload both arms run (identical dicts: the driver compares them)."""
+    return {"workload": f"C4: CG dense SPD n={n} fp64, reference spd recipe (harness.py:88-91, "
+                        f"default_rng([0, n, 2])), fixed {iters} iterations per step (tolerance 1e-300)",
+            "n": n, "iters_per_step": iters, "seed": 0,
+            "l2_policy": f"inputs larger than L2 (A = {8 * n * n / 2 ** 30:.1f} GiB >> 126 MB L2)",
+            "parallelism": f"rows{ws}"}
+
+
+def c4_host_inputs(n):
+    """(A, b) of config C4 on the host, the bytes the B200 arm solves: generated by the
+    device generator when a GPU is present (the spd recipe's M^T M is then the DMMA SYRK),
+    else by the recipe in NumPy with M.T @ M.copy() (gemm; the reference's syrk call
+    crashes at n=32768)."""
+    try:
+        from paper_1511_07207_b200 import get_backend
+        from paper_1511_07207_b200.harness import generate_problem_device
+        be = get_backend("b200")
+        dA, db, _ = generate_problem_device("spd", n, 0, "f64", be)
+        A, b = dA.to_host(), db.to_host()
+        dA.free(), db.free()
+        be.ctx.synchronize()
+        return A, b, "device generator (ds_generate, same bytes as the B200 arm)"
+    except RuntimeError:
+        rng = np.random.default_rng([0, n, 2])
+        M = rng.uniform(-1.0, 1.0, size=(n, n))
+        S = M.T @ M.copy() + n * np.eye(n)
+        del M
+        A = np.asfortranarray(np.tril(S) + np.tril(S, -1).T)
+        xt = rng.uniform(-1.0, 1.0, size=n)
+        return A, A @ xt, "NumPy recipe (no GPU visible)"
+
+
+def ref_cg_step(densolve, A, b, x0, iters):
+    cfg = densolve.SolverConfig(tolerance=1e-300, max_iterations=iters)
+    be = densolve.get_backend("blocked")
+    t0 = time.perf_counter()
+    _, rep = densolve.cg_solve(A, b, x0, cfg, be)
+    dt = time.perf_counter() - t0
+    assert rep.iterations == iters, rep.iterations
+    return dt
+
+
 # ---------------------------------------------------------------------------- reference arm
+REF_MAX_STEPS = 3  # ~43 s per 100-iteration step at n=32768 on 16 cores: the run stays near 3 min
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    from oracle import densolve_oracle as O
-
-    n = args.n
-    # bounded sample: ~0.35 s per CPU iteration at n=32768, keep the whole run near 3 minutes
-    iters = max(10, min(args.iters, int(180.0 / ((args.steps + 1) * 0.35))))
-    cores = os.cpu_count() or 1
-    A, b = spd_fast_host(n, 0)
+    n, iters = args.n, args.iters
+    try:
+        densolve = ref_densolve()
+    except ImportError as e:
+        print(json.dumps({"impl": "reference", "unavailable": str(e)}), flush=True)
+        return
+    A, b, src = c4_host_inputs(n)
     x0 = np.zeros(n)
+    warm, steps = min(args.warmup, 1), max(1, min(args.steps, REF_MAX_STEPS))
     times = []
-    for k in range(min(args.warmup, 1) + args.steps):
-        t0 = time.perf_counter()
-        O.cg(A, b, x0, 1e-300, iters, O.Ops(threads=cores))
-        dt = time.perf_counter() - t0
-        if k >= min(args.warmup, 1):
+    for k in range(warm + steps):
+        dt = ref_cg_step(densolve, A, b, x0, iters)
+        if k >= warm:
             times.append(dt)
     tot = sum(times)
     val = iters * len(times) / tot
-    line = {"impl": "reference", "metric": BASELINE_METRIC, "value": val,
-            "unit": f"CG iters/s (n={n} fp64)", "n_gpus": ws, "steps": args.steps,
-            "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"C4 CG dense SPD n={n} fp64, fixed iterations per step (bounded CPU sample)",
-                       "n": n, "iters_per_step": iters, "b200_arm_iters_per_step": args.iters},
-            "cpu_baseline": {"value": val, "unit": f"CG iters/s (n={n} fp64)", "cores": cores, "kind": "port",
-                             "sample": f"oracle.cg (NumPy/OpenBLAS restatement of krylov.cg_solve incl. "
-                                       f"symmetry gate), n={n}, {iters} iterations per step"},
-            "e2e": {"value": val, "unit": f"CG iters/s (n={n} fp64)", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+    info = host_info()
+    unit = f"CG iters/s (n={n} fp64)"
+    sample = (f"densolve.cg_solve (unmodified reference, baseline/_ref) with get_backend('blocked'), "
+              f"{iters} iterations per call incl. its symmetry gate, {len(times)} timed call(s) after {warm} "
+              f"warm-up; A from the {src}")
+    line = {"impl": "reference", "metric": BASELINE_METRIC, "value": val, "unit": unit, "n_gpus": ws,
+            "steps": len(times), "steps_requested": args.steps, "warmup": warm,
+            "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": c4_config(n, iters, ws),
+            "cpu_baseline": {"value": val, "unit": unit, "cores": info["cores"], "kind": "reference",
+                             "sample": sample, "host": info},
+            "e2e": {"value": val, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------- B200 arm
-def cpu_baseline_sample(n, iters):
-    from oracle import densolve_oracle as O
-
-    cores = os.cpu_count() or 1
-    A, b = spd_fast_host(n, 0)
-    t0 = time.perf_counter()
-    O.cg(A, b, np.zeros(n), 1e-300, iters, O.Ops(threads=cores))
-    dt = time.perf_counter() - t0
-    del A
-    return {"value": iters / dt, "unit": f"CG iters/s (n={n} fp64)", "cores": cores, "kind": "port",
-            "sample": f"one step: oracle.cg (NumPy/OpenBLAS restatement of krylov.cg_solve incl. symmetry "
-                      f"gate) at n={n}, {iters} iterations, {dt:.1f} s"}
+def cpu_baseline_c4(A_h, b_h, n, iters):
+    """One bounded call of the reference CG on this host on the B200 arm's own bytes."""
+    info = host_info()
+    try:
+        densolve = ref_densolve()
+        dt = ref_cg_step(densolve, A_h, b_h, np.zeros(n), iters)
+        kind, what = "reference", "densolve.cg_solve (unmodified reference, baseline/_ref), get_backend('blocked')"
+    except ImportError:
+        from oracle import densolve_oracle as O
+        t0 = time.perf_counter()
+        O.cg(A_h, b_h, np.zeros(n), 1e-300, iters, O.Ops(threads=info["cores"]))
+        dt = time.perf_counter() - t0
+        kind, what = "port", "oracle.cg (NumPy restatement of krylov.cg_solve)"
+    return {"value": iters / dt, "unit": f"CG iters/s (n={n} fp64)", "cores": info["cores"], "kind": kind,
+            "sample": f"one call of {what} incl. its symmetry gate, n={n}, {iters} iterations, {dt:.1f} s, "
+                      "same matrix bytes", "host": info}
 
 
 def run_b200(args):
@@ -253,10 +307,9 @@ def run_b200(args):
                          ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29531")):
                 os.environ.setdefault(k, v)
             dist.init_process_group("nccl", device_id=dev)
-    from paper_1511_07207_b200 import (SolverConfig, cg_solve, get_backend, gmres_solve,
-                                       lu_factor_blocked, pinned_empty)
+    from paper_1511_07207_b200 import SolverConfig, cg_solve, get_backend, pinned_empty
     from paper_1511_07207_b200.device import DeviceArray
-    from paper_1511_07207_b200.harness import ProblemSpec, generate_problem
+    from paper_1511_07207_b200.harness import generate_problem_device
 
     be = get_backend("b200", device=local)
     ctx = be.ctx
@@ -275,30 +328,24 @@ def run_b200(args):
             if dist.is_initialized():
                 dist.destroy_process_group()
 
-    # ---- inputs: synthetic SPD generated on the device, staged into a DeviceArray
-    At, bt = spd_fast_device(n, 0, torch, dev, be)
-    dA = DeviceArray(ctx, (n, n), np.float64)
-    assert dA.ld == n
-    ctx.lib.ds_memcpy_d2d(ctx.handle, dA.ptr, At.data_ptr(), 8 * n * n)
-    db = DeviceArray(ctx, (n,), np.float64)
-    ctx.lib.ds_memcpy_d2d(ctx.handle, db.ptr, bt.data_ptr(), 8 * n)
+    # ---- inputs: the reference spd recipe, generated on the device (ds_generate)
+    dA, db, _ = generate_problem_device("spd", n, 0, "f64", be)
     dx0 = DeviceArray(ctx, (n,), np.float64)
     ctx.lib.ds_memset(ctx.handle, dx0.ptr, 0, 8 * n)
-    # host copies (pinned) for the end-to-end arm
+    # host copies (pinned) for the end-to-end arm and the CPU baseline
     A_h = pinned_empty((n, n), np.float64, order="F")
-    A_h_t = torch.from_numpy(A_h.reshape(-1, order="F").view(np.float64))
-    A_h_t.copy_(At.reshape(-1))  # A is symmetric: row-major bytes == column-major bytes
+    dA.to_host(out=A_h)
     b_h = pinned_empty((n,), np.float64)
-    b_h[:] = bt.cpu().numpy()
+    b_h[:] = db.to_host()
     x0_h = pinned_empty((n,), np.float64)
     x0_h[:] = 0.0
-    del At
     torch.cuda.synchronize()
 
     # ---- headline: device-resident fixed-iteration CG steps
     for _ in range(args.warmup):
         cg_solve(dA, db, dx0, cfg, be)
     torch.cuda.synchronize()
+
     def timed_region():
         l0 = ctx.launches()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -348,7 +395,7 @@ def run_b200(args):
             traffic = json.load(fh).get("dram_bytes_per_launch")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
-                "kernel": "gemv_partial_kernel<double,2,8> + gemv_reduce (ds_gemv)",
+                "kernel": "ds_colstream_mv_kernel<double,2,8> + ds_colstream_reduce_kernel (ds_gemv)",
                 "algorithmic_bytes_per_launch": gemv_bytes, "avg_launch_ms": round(gemv_ms, 4),
                 "peak_source": peak_src,
                 "cg_iteration_GBps": round(8.0 * (n * n + 10 * n) / (ms / 1e3 / (iters * args.steps)) / 1e9, 1)}
@@ -369,7 +416,7 @@ def run_b200(args):
     f1.record(stream)
     torch.cuda.synchronize()
     serial_ms = max(f0.elapsed_time(f1), 1e3 * (time.perf_counter() - t0))
-    del dx0  # free the resident operands' x0; A stays for the components below
+    del dx0  # the resident A stays for the components below
     bufs = [(DeviceArray(ctx, (n, n), np.float64), DeviceArray(ctx, (n,), np.float64),
              DeviceArray(ctx, (n,), np.float64)) for _ in range(2)]
     be.stage_in_async(A_h, b_h, x0_h, out=bufs[0])
@@ -396,36 +443,31 @@ def run_b200(args):
     del bufs
     dx0 = DeviceArray(ctx, (n,), np.float64)
     ctx.lib.ds_memset(ctx.handle, dx0.ptr, 0, 8 * n)
-    del A_h, A_h_t
 
+    cpu = None if args.no_cpu_baseline else cpu_baseline_c4(A_h, b_h, n, min(iters, 30))
     components = {}
     if not args.only_cg:
         from paper_1511_07207_b200 import bicgstab_solve, cholesky_factor
         components["bicgstab"] = bench_bicgstab(args, torch, stream, be, dA, db, dx0, n, bicgstab_solve,
-                                                SolverConfig, hbm_peak)
+                                                SolverConfig, hbm_peak, A_h, b_h)
         components["cholesky"] = bench_cholesky(args, torch, stream, be, dA, n, cholesky_factor)
-    del dA
+    del dA, A_h
     torch.cuda.empty_cache()
     if not args.only_cg:
-        components["gmres_c2"] = bench_gmres(args, torch, stream, be, generate_problem, ProblemSpec,
-                                             gmres_solve, SolverConfig)
-        components["gmres_c5"] = bench_gmres_c5(args, torch, dev, stream, be, gmres_solve, SolverConfig,
-                                                hbm_peak)
-        components["lu_c3"] = bench_lu(args, torch, dev, stream, be, lu_factor_blocked, args.lu_n)
-        components["lu_c5"] = bench_lu(args, torch, dev, stream, be, lu_factor_blocked, args.lu_n5)
-
-    cpu = None
-    if not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(n, min(iters, 30))  # ~15-25 s of host work
+        components["gmres_c2"] = bench_gmres(args, torch, stream, be, 4096, 30, "f64", "C2", hbm_peak)
+        components["gmres_fp64_n32768"] = bench_gmres(args, torch, stream, be, args.n, 30, "f64",
+                                                      "north_star GMRES fp64", hbm_peak)
+        components["gmres_c5"] = bench_gmres_c5(args, torch, dev, stream, be, hbm_peak)
+        lu_fit = None if args.no_cpu_baseline else reference_lu_fit()
+        components["lu_c3"] = bench_lu(args, torch, stream, be, args.lu_n, lu_fit, hbm_peak)
+        components["lu_c5"] = bench_lu(args, torch, stream, be, args.lu_n5, lu_fit, hbm_peak)
 
     line = {"metric": BASELINE_METRIC, "value": round(value, 3), "unit": f"CG iters/s (n={n} fp64)",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded dense SPD A=(R+R^T)/2+sqrt(n)I, R~U[-1,1], kappa~10, generated on device)",
-            "config": {"workload": f"C4: CG dense SPD n={n} fp64, fixed {iters} iterations per step "
-                                   f"(tolerance 1e-300), 1 GPU", "n": n, "iters_per_step": iters,
-                       "l2_policy": f"inputs larger than L2 (A = {8 * n * n / 2**30:.1f} GiB >> 126 MB L2)",
-                       "parallelism": f"rows{ws}"},
+            "data": "synthetic: the reference's seeded spd recipe (harness.py:88-91) generated on the device "
+                    "(ds_generate: bit-identical PCG64 stream, M^T M by the DMMA SYRK)",
+            "config": c4_config(n, iters, ws),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": dict(clk.summary(), remeasured=remeasured), "components": components}
     print(json.dumps(line), flush=True)
@@ -444,75 +486,116 @@ def _timed(torch, stream, fn, reps):
     return e0.elapsed_time(e1) / reps, out
 
 
-def bench_gmres(args, torch, stream, be, generate_problem, ProblemSpec, gmres_solve, SolverConfig):
-    """C2: GMRES(30) general_nonsymmetric n=4096 fp64 (the harness generator, host-built)."""
-    n, m = 4096, 30
-    A, b, _ = generate_problem(ProblemSpec(kind="general_nonsymmetric", n=n, seed=0))
-    dA, db, dx0 = be.stage_in(A, b, np.zeros_like(b))
+def _gmres_cycle_bytes(n, m, s):
+    """Algorithmic bytes of one GMRES(m) cycle: (m + 2) passes over A (m Arnoldi GEMVs +
+    residual + true residual), per step k the basis traffic (2k + 7) n, and the x update."""
+    return s * ((m + 2) * n * n + sum((2 * k + 7) * n for k in range(m)) + (m + 2) * n)
+
+
+def _ref_gmres_cycle(A, b, m, reps=1):
+    """Seconds of one full GMRES(m) cycle of the unmodified reference (best of reps)."""
+    densolve = ref_densolve()
+    cfg = densolve.SolverConfig(tolerance=1e-300, restart_m=m, max_iterations=m)
+    be = densolve.get_backend("blocked")
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        _, rep = densolve.gmres_solve(A, b, np.zeros_like(b), cfg, be)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return best, rep.iterations
+
+
+def bench_gmres(args, torch, stream, be, n, m, prec, tag, hbm_peak):
+    """GMRES(m) on the reference general_nonsymmetric recipe (harness.py:92-98), one full cycle
+    per step (residual + m Arnoldi steps + update + true residual)."""
+    from paper_1511_07207_b200 import SolverConfig, gmres_solve
+    from paper_1511_07207_b200.harness import generate_problem_device
+
+    dA, db, _ = generate_problem_device("general_nonsymmetric", n, 0, prec, be)
+    dx0 = be.stage_in(np.zeros(n, dtype=dA.dtype))
     cfg = SolverConfig(tolerance=1e-300, restart_m=m, max_iterations=m)
-    ms, (x, rep) = _timed(torch, stream, lambda: gmres_solve(dA, db, dx0, cfg, be), 10)
-    return {"workload": f"C2: GMRES({m}) general_nonsymmetric n={n} fp64, one full cycle per step "
-                        "(residual + 30 Arnoldi steps + update + true residual)",
-            "value": round(rep.iterations / (ms / 1e3), 1), "unit": "inner iters/s", "ms_per_step": round(ms, 4)}
+    ms, (x, rep) = _timed(torch, stream, lambda: gmres_solve(dA, db, dx0, cfg, be), 10 if n <= 8192 else 3)
+    s = dA.dtype.itemsize
+    gbs = _gmres_cycle_bytes(n, m, s) / (ms / 1e3) / 1e9
+    out = {"workload": f"{tag}: GMRES({m}) general_nonsymmetric recipe n={n} {prec}, one full cycle per step",
+           "value": round(rep.iterations / (ms / 1e3), 1), "unit": "inner iters/s", "ms_per_step": round(ms, 4),
+           "iterations": rep.iterations, "GBps": round(gbs, 1), "frac_of_hbm_peak": round(gbs / hbm_peak, 4)}
+    if not args.no_cpu_baseline:
+        A, b = dA.to_host(), db.to_host()
+        del dA
+        dt, its = _ref_gmres_cycle(A, b, m, reps=3 if n <= 8192 else 1)
+        out["cpu_baseline"] = {"value": round(its / dt, 2), "unit": "inner iters/s", "cores": os.cpu_count(),
+                               "kind": "reference",
+                               "sample": f"one cycle of densolve.gmres_solve (baseline/_ref, 'blocked'), same bytes, "
+                                         f"{dt:.2f} s"}
+    torch.cuda.empty_cache()
+    return out
 
 
-def nonsym_fast_device(n, seed, torch, device, dtype, be):
-    """Synthetic dense nonsymmetric A = R + 1.5 sqrt(n) I, R ~ U[-1,1] (seeded, on the GPU, in the
-    target dtype; the harness recipe needs ~130 GB of fp64 temporaries at n=65536).  R's spectrum
-    fills a disk of radius sqrt(n/3) (circular law), so GMRES contracts by ~0.38 per step: one
-    full 50-step cycle stays far above the fp32 underflow of the Givens estimate."""
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    A = torch.empty((n, n), dtype=dtype, device=device)
-    for c0 in range(0, n, 4096):  # column blocks keep the fp32 temporaries small
-        blk = torch.rand((min(4096, n - c0), n), dtype=dtype, device=device, generator=g)
-        A[c0:c0 + blk.shape[0]] = blk.mul_(2.0).sub_(1.0)
-    A.diagonal().add_(1.5 * float(n) ** 0.5)
-    xt = torch.rand(n, dtype=dtype, device=device, generator=g).mul_(2.0).sub_(1.0)
-    return A, lib_matvec(be, A, xt)  # torch row-major A read column-major is A^T: b = A^T x
-
-
-def bench_gmres_c5(args, torch, dev, stream, be, gmres_solve, SolverConfig, hbm_peak):
-    """C5: GMRES(50) n=65536 fp32, one full cycle per step (HBM-capacity sizing, 1 GPU)."""
-    from paper_1511_07207_b200.device import DeviceArray
+def bench_gmres_c5(args, torch, dev, stream, be, hbm_peak):
+    """C5: GMRES(50) n=65536 fp32, one full cycle per step (HBM-capacity sizing, 1 GPU).
+    Matrix: the uniform recipe's stream (default_rng([3, n, 1]), ds_generate) shifted by
+    1.5 sqrt(n) I.  The reference general_nonsymmetric recipe contracts ~300x per step, so a
+    FIXED 50-step cycle underflows the fp32 Givens estimate after ~16 steps; the shifted
+    uniform matrix (circular-law spectrum, ~0.38 per step) keeps every step meaningful.
+    (Parity on the general_nonsymmetric recipe itself: tests/test_gpu_config_parity.py.)"""
+    from paper_1511_07207_b200 import SolverConfig, gmres_solve
+    from paper_1511_07207_b200.harness import generate_problem_device
 
     n, m = args.gmres_n, 50
-    ctx = be.ctx
-    At, bt = nonsym_fast_device(n, 3, torch, dev, torch.float32, be)
-    dA = DeviceArray(ctx, (n, n), np.float32)
-    ctx.lib.ds_memcpy_d2d(ctx.handle, dA.ptr, At.data_ptr(), 4 * n * n)
-    db = DeviceArray(ctx, (n,), np.float32)
-    ctx.lib.ds_memcpy_d2d(ctx.handle, db.ptr, bt.data_ptr(), 4 * n)
-    dx0 = DeviceArray(ctx, (n,), np.float32)
-    ctx.lib.ds_memset(ctx.handle, dx0.ptr, 0, 4 * n)
-    del At, bt
+    dA, db, dxt = generate_problem_device("uniform", n, 3, "f32", be)
+    tA = torch.as_tensor(dA, device=dev)
     torch.cuda.synchronize()
+    tA.diagonal().add_(1.5 * float(n) ** 0.5)
+    torch.cuda.synchronize()
+    from ctypes import c_void_p
+    from paper_1511_07207_b200 import _lib
+    _lib.check(be.ctx.lib.ds_gemv(be.ctx.handle, _lib.DS_F32, n, n, c_void_p(dA.ptr), dA.ld,
+                                  c_void_p(dxt.ptr), c_void_p(db.ptr)))  # b = A x_true (library GEMV)
+    dx0 = be.stage_in(np.zeros(n, dtype=np.float32))
     cfg = SolverConfig(tolerance=1e-300, restart_m=m, max_iterations=m)
     ms, (x, rep) = _timed(torch, stream, lambda: gmres_solve(dA, db, dx0, cfg, be), 3)
-    # algorithmic bytes of one cycle: (m + 2) passes over A (m Arnoldi GEMVs + residual + true
-    # residual) + per step k the basis traffic (2k + 7) n + the x update (m + 2) n
-    s = 4.0
-    byts = s * ((m + 2) * n * n + sum((2 * k + 7) * n for k in range(m)) + (m + 2) * n)
-    gbs = byts / (ms / 1e3) / 1e9
-    del dA
+    gbs = _gmres_cycle_bytes(n, m, 4.0) / (ms / 1e3) / 1e9
+    out = {"workload": f"C5: GMRES({m}) dense nonsymmetric n={n} fp32, uniform recipe + 1.5 sqrt(n) I "
+                       "(device-generated), one full cycle per step", "cycles": len(rep.restart_cycles or []),
+           "iterations": rep.iterations, "value": round(rep.iterations / (ms / 1e3), 1), "unit": "inner iters/s",
+           "ms_per_step": round(ms, 3), "GBps": round(gbs, 1), "frac_of_hbm_peak": round(gbs / hbm_peak, 4)}
+    if not args.no_cpu_baseline:
+        A, b = dA.to_host(), db.to_host()
+        del tA, dA
+        dt, its = _ref_gmres_cycle(A, b, m)
+        out["cpu_baseline"] = {"value": round(its / dt, 2), "unit": "inner iters/s", "cores": os.cpu_count(),
+                               "kind": "reference",
+                               "sample": f"one 50-step cycle of densolve.gmres_solve (baseline/_ref, 'blocked'), "
+                                         f"same bytes, {dt:.1f} s"}
+        del A
     torch.cuda.empty_cache()
-    return {"workload": f"C5: GMRES({m}) dense nonsymmetric A = R + 1.5 sqrt(n) I, n={n} fp32 (device-generated), "
-                        "one full cycle per step", "cycles": len(rep.restart_cycles or []), "value": round(rep.iterations / (ms / 1e3), 1),
-            "unit": "inner iters/s", "ms_per_step": round(ms, 3), "GBps": round(gbs, 1),
-            "frac_of_hbm_peak": round(gbs / hbm_peak, 4)}
+    return out
 
 
-def bench_bicgstab(args, torch, stream, be, dA, db, dx0, n, bicgstab_solve, SolverConfig, hbm_peak):
+def bench_bicgstab(args, torch, stream, be, dA, db, dx0, n, bicgstab_solve, SolverConfig, hbm_peak, A_h, b_h):
     """BiCGSTAB on the C4 matrix, fixed 50 iterations per step."""
     iters = 50
     cfg = SolverConfig(tolerance=1e-300, max_iterations=iters)
     ms, (x, rep) = _timed(torch, stream, lambda: bicgstab_solve(dA, db, dx0, cfg, be), 2)
     its = rep.iterations
     gbs = 8.0 * (2 * its + 1) * (n * n) / (ms / 1e3) / 1e9
-    return {"workload": f"BiCGSTAB dense SPD n={n} fp64 (C4 matrix), fixed {iters} iterations per step",
-            "value": round(its / (ms / 1e3), 2), "unit": "iters/s", "ms_per_step": round(ms, 3),
-            "iterations": its, "breakdown": rep.breakdown, "GBps_A_stream": round(gbs, 1),
-            "frac_of_hbm_peak": round(gbs / hbm_peak, 4)}
+    out = {"workload": f"BiCGSTAB dense SPD n={n} fp64 (C4 matrix), fixed {iters} iterations per step",
+           "value": round(its / (ms / 1e3), 2), "unit": "iters/s", "ms_per_step": round(ms, 3),
+           "iterations": its, "breakdown": rep.breakdown, "GBps_A_stream": round(gbs, 1),
+           "frac_of_hbm_peak": round(gbs / hbm_peak, 4)}
+    if not args.no_cpu_baseline:
+        densolve = ref_densolve()
+        k = 10
+        t0 = time.perf_counter()
+        _, r = densolve.bicgstab_solve(A_h, b_h, np.zeros(n), densolve.SolverConfig(tolerance=1e-300,
+                                       max_iterations=k), densolve.get_backend("blocked"))
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": round(r.iterations / dt, 3), "unit": "iters/s", "cores": os.cpu_count(),
+                               "kind": "reference",
+                               "sample": f"densolve.bicgstab_solve (baseline/_ref), {r.iterations} iterations, {dt:.1f} s"}
+    return out
 
 
 def bench_cholesky(args, torch, stream, be, dA, n, cholesky_factor):
@@ -526,31 +609,72 @@ def bench_cholesky(args, torch, stream, be, dA, n, cholesky_factor):
             "fp64_peak_tflops": FP64_PEAK_TFLOPS, "frac_of_fp64_peak": round(tf / FP64_PEAK_TFLOPS, 4)}
 
 
-def bench_lu(args, torch, dev, stream, be, lu_factor_blocked, n):
-    from paper_1511_07207_b200.device import DeviceArray
+def reference_lu_fit():
+    """The reference lu_factor_blocked (b=64, 'blocked' backend, all cores) on the uniform
+    recipe at n = 2048 and 4096, fitted to t = a n^3 (full n needs hours)."""
+    from paper_1511_07207_b200.harness import generate_uniform
+    densolve = ref_densolve()
+    be = densolve.get_backend("blocked")
+    pts = []
+    for n in (2048, 4096):
+        A, _, _ = generate_uniform(n, 1)
+        t0 = time.perf_counter()
+        densolve.lu_factor_blocked(A, 64, be)
+        pts.append((n, time.perf_counter() - t0))
+    a = sum(t * n ** 3 for n, t in pts) / sum(n ** 6 for n, _ in pts)  # least squares through 0
+    return {"a": a, "points": [{"n": n, "s": round(t, 3), "GFLOP/s": round(2 * n ** 3 / 3 / t / 1e9, 3)}
+                               for n, t in pts]}
 
-    ctx = be.ctx
-    g = torch.Generator(device=dev)
-    g.manual_seed(1)
-    At = torch.rand((n, n), dtype=torch.float64, device=dev, generator=g).mul_(2.0).sub_(1.0)
-    dA = DeviceArray(ctx, (n, n), np.float64)
-    ctx.lib.ds_memcpy_d2d(ctx.handle, dA.ptr, At.data_ptr(), 8 * n * n)
-    del At
+
+def bench_lu(args, torch, stream, be, n, lu_fit, hbm_peak):
+    """Blocked LU b=64 on the uniform recipe (C3 pivoting family, default_rng([1, n, 1]),
+    ds_generate) + lu_solve of b = A x_true; CPU: the reference extrapolated from n=2048/4096
+    and LAPACK getrf (scipy) at full n as a labelled comparator."""
+    from paper_1511_07207_b200 import lu_factor_blocked, lu_solve
+    from paper_1511_07207_b200.harness import generate_problem_device
+
+    dA, db, dxt = generate_problem_device("uniform", n, 1, "f64", be)
     torch.cuda.synchronize()
     f = lu_factor_blocked(dA, 64, be)  # warm-up
     del f
     # 1 warm-up + best-of-3, the reference's own timing protocol (harness.py:281-294)
     runs = [_timed(torch, stream, lambda: lu_factor_blocked(dA, 64, be), 1)[0] for _ in range(3)]
     ms = min(runs)
-    del dA
-    torch.cuda.empty_cache()
+    f = lu_factor_blocked(dA, 64, be)
+    sms, x = _timed(torch, stream, lambda: lu_solve(f, db), 5)
+    err = float(np.max(np.abs(x.to_host() - dxt.to_host())))
+    sbytes = 8.0 * n * n  # one pass over each triangle of the packed factors
     flops = 2.0 * n ** 3 / 3.0
     tf = flops / (ms / 1e3) / 1e12
-    return {"workload": f"blocked LU b=64, uniform U[-1,1] n={n} fp64 (pivoting family), device-resident "
-                        "(includes the device copy of A, direct.py:61); best of 3 after 1 warm-up",
-            "value": round(tf * 1e3, 1), "unit": "GFLOP/s", "ms": round(ms, 2),
-            "ms_runs": [round(r, 2) for r in runs],
-            "fp64_peak_tflops": FP64_PEAK_TFLOPS, "frac_of_fp64_peak": round(tf / FP64_PEAK_TFLOPS, 4)}
+    out = {"workload": f"blocked LU b=64, uniform recipe n={n} fp64 (pivoting family), device-resident "
+                       "(includes the device copy of A, direct.py:61); best of 3 after 1 warm-up",
+           "value": round(tf * 1e3, 1), "unit": "GFLOP/s", "ms": round(ms, 2), "ms_runs": [round(r, 2) for r in runs],
+           "fp64_peak_tflops": FP64_PEAK_TFLOPS, "frac_of_fp64_peak": round(tf / FP64_PEAK_TFLOPS, 4),
+           "lu_solve": {"ms": round(sms, 4), "GBps": round(sbytes / (sms / 1e3) / 1e9, 1),
+                        "frac_of_hbm_peak": round(sbytes / (sms / 1e3) / 1e9 / hbm_peak, 4),
+                        "algorithmic_bytes": sbytes, "max_abs_err_vs_x_true": err}}
+    del f
+    if lu_fit is not None:
+        import scipy.linalg
+        A = dA.to_host()
+        del dA
+        torch.cuda.empty_cache()
+        t0 = time.perf_counter()
+        scipy.linalg.lu_factor(A, overwrite_a=True, check_finite=False)
+        tl = time.perf_counter() - t0
+        del A
+        te = lu_fit["a"] * n ** 3
+        out["cpu_baseline"] = {"value": round(flops / te / 1e9, 3), "unit": "GFLOP/s", "cores": os.cpu_count(),
+                               "kind": "reference",
+                               "sample": f"EXTRAPOLATED: densolve.lu_factor_blocked (baseline/_ref, b=64, 'blocked') "
+                                         f"timed at n=2048/4096, t = a n^3 -> {te:.0f} s at n={n}",
+                               "points": lu_fit["points"],
+                               "lapack_comparator": {"value": round(flops / tl / 1e9, 1), "unit": "GFLOP/s",
+                                                     "s": round(tl, 2),
+                                                     "what": "scipy.linalg.lu_factor (LAPACK dgetrf, OpenBLAS) at "
+                                                             "full n on the same bytes; NOT the reference"}}
+    torch.cuda.empty_cache()
+    return out
 
 
 # ---------------------------------------------------------------------------- N > 1 (torchrun)
@@ -563,8 +687,8 @@ def bench_sharded_cg(args, torch, dev, be):
     import torch.distributed as dist
 
     from paper_1511_07207_b200.core import SolverConfig
-    from paper_1511_07207_b200.distributed import (CudaShardOps, TorchComm, cg_solve_sharded, row_partition,
-                                                   spd_block_device)
+    from paper_1511_07207_b200.distributed import CudaShardOps, TorchComm, cg_solve_sharded, row_partition
+    from paper_1511_07207_b200.harness import generate_problem_device
 
     comm = TorchComm()
     ops = CudaShardOps(be.ctx)
@@ -574,11 +698,17 @@ def bench_sharded_cg(args, torch, dev, be):
     G, q = comm.size, comm.rank
     n_loc, N = row_partition(n, G)
     r0, r1 = q * n_loc, min(n, (q + 1) * n_loc)
+    # every rank generates the full C4 matrix (the reference spd recipe, same bytes as the
+    # 1-GPU arm) and keeps its row block: A is symmetric, so rows r0:r1 are columns r0:r1
+    dA, db, _ = generate_problem_device("spd", n, 0, "f64", be)
+    tA, tb = torch.as_tensor(dA, device=dev), torch.as_tensor(db, device=dev)
     A_blk = torch.zeros((n, n_loc), dtype=torch.float64, device=dev)
-    if r1 > r0:
-        A_blk[:, : r1 - r0] = spd_block_device(n, r0, r1, torch, dev)
     b = torch.zeros(n_loc, dtype=torch.float64, device=dev)
-    b[: r1 - r0] = 1.0
+    if r1 > r0:
+        A_blk[:, : r1 - r0].copy_(tA[:, r0:r1])
+        b[: r1 - r0].copy_(tb[r0:r1])
+    torch.cuda.synchronize()
+    del tA, tb, dA, db
     x0 = torch.zeros(n_loc, dtype=torch.float64, device=dev)
     cfg = SolverConfig(tolerance=1e-300, max_iterations=iters)
     for _ in range(args.warmup):
@@ -649,10 +779,9 @@ def bench_sharded_cg(args, torch, dev, be):
             "metric": BASELINE_METRIC, "value": round(value, 3), "unit": unit, "n_gpus": G, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (hash-generated symmetric A = S + 1.5 sqrt(n) I, row blocks generated per rank)",
-            "config": {"workload": f"C4: CG dense SPD n={n} fp64 row-sharded over {G} GPUs, {iters} iterations/step",
-                       "n": n, "iters_per_step": iters, "parallelism": f"rows{G}",
-                       "l2_policy": "inputs larger than L2"},
+            "data": "synthetic: the reference's seeded spd recipe (harness.py:88-91) generated on the device "
+                    "(ds_generate), each rank keeping its row block",
+            "config": c4_config(n, iters, G),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4), "traffic": None,
                          "kernel": "per-rank ds_gemv on the n x n_loc block (max over ranks)",

@@ -91,7 +91,7 @@ GemvPlan gemv_plan(ds_ctx* ctx, int64_t m, int64_t n, size_t elem) {
 
 template <typename T, int VEC, int UNR>
 __global__ void __launch_bounds__(kGemvThreads)
-    gemv_partial_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t n,
+    ds_colstream_mv_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t n,
                         const T* __restrict__ x, int64_t chunk, double* __restrict__ part,
                         Gate gate) {
   pdl_wait();  // x and the stop word come from the previous kernel
@@ -152,7 +152,7 @@ constexpr int kRedThreads = 256;
 
 template <typename T, int EPI>
 __global__ void __launch_bounds__(kRedThreads)
-    gemv_reduce_kernel(const double* __restrict__ part, int64_t m, int64_t nchunks, T* y,
+    ds_colstream_reduce_kernel(const double* __restrict__ part, int64_t m, int64_t nchunks, T* y,
                        const T* __restrict__ v, double* __restrict__ red, Gate gate) {
   if (gated(gate)) return;
   __shared__ double sm[64];
@@ -235,11 +235,11 @@ int gemv_launch(ds_ctx* ctx, const GemvPlan& p, const T* A, int64_t lda, const T
     constexpr int VEC = sizeof(T) == 8 ? 2 : 4;
     const bool aligned = (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (lda % VEC == 0);
     if (aligned) {
-      gemv_partial_kernel<T, VEC, 8>
+      ds_colstream_mv_kernel<T, VEC, 8>
           <<<grid, kGemvThreads, smem, ctx->stream>>>(A, lda, m, n, x, p.chunk, part, stop);
     } else {
       dim3 g1((unsigned)ceil_div(m, kGemvThreads), (unsigned)p.nchunks);
-      gemv_partial_kernel<T, 1, 8>
+      ds_colstream_mv_kernel<T, 1, 8>
           <<<g1, kGemvThreads, smem, ctx->stream>>>(A, lda, m, n, x, p.chunk, part, stop);
     }
     count_launch(ctx);
@@ -249,23 +249,23 @@ int gemv_launch(ds_ctx* ctx, const GemvPlan& p, const T* A, int64_t lda, const T
   const int64_t nch = n == 0 ? 1 : p.nchunks;
   switch (epi) {
     case EPI_STORE:
-      gemv_reduce_kernel<T, EPI_STORE>
+      ds_colstream_reduce_kernel<T, EPI_STORE>
           <<<rblocks, kRedThreads, 0, ctx->stream>>>(part, m, nch, y, v, red, stop);
       break;
     case EPI_DOT:
-      gemv_reduce_kernel<T, EPI_DOT>
+      ds_colstream_reduce_kernel<T, EPI_DOT>
           <<<rblocks, kRedThreads, 0, ctx->stream>>>(part, m, nch, y, v, red, stop);
       break;
     case EPI_RESID:
-      gemv_reduce_kernel<T, EPI_RESID>
+      ds_colstream_reduce_kernel<T, EPI_RESID>
           <<<rblocks, kRedThreads, 0, ctx->stream>>>(part, m, nch, y, v, red, stop);
       break;
     case EPI_AXPY_INTO:
-      gemv_reduce_kernel<T, EPI_AXPY_INTO>
+      ds_colstream_reduce_kernel<T, EPI_AXPY_INTO>
           <<<rblocks, kRedThreads, 0, ctx->stream>>>(part, m, nch, y, v, red, stop);
       break;
     case EPI_DOT2:
-      gemv_reduce_kernel<T, EPI_DOT2>
+      ds_colstream_reduce_kernel<T, EPI_DOT2>
           <<<rblocks, kRedThreads, 0, ctx->stream>>>(part, m, nch, y, v, red, stop);
       break;
     default:
@@ -294,7 +294,7 @@ int gemv_partial_pdl_launch(ds_ctx* ctx, const GemvPlan& p, const T* A, int64_t 
   lc.attrs = at;
   lc.numAttrs = 1;
   const int64_t m = p.m, n = p.n, chunk = p.chunk;
-  DS_CUDA(cudaLaunchKernelEx(&lc, gemv_partial_kernel<T, VEC, 8>, A, lda, m, n, x, chunk, part, stop));
+  DS_CUDA(cudaLaunchKernelEx(&lc, ds_colstream_mv_kernel<T, VEC, 8>, A, lda, m, n, x, chunk, part, stop));
   count_launch(ctx);
   DS_CHECK_LAUNCH();
   return DS_OK;
@@ -1212,19 +1212,19 @@ extern "C" {
 
 int ds_axpy(ds_ctx* ctx, int dtype, int64_t n, double alpha, const void* x, const void* y,
             void* out) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   DS_DISPATCH(dtype, T, DS_TRY(axpy_launch<T>(ctx, n, alpha, (const T*)x, (const T*)y, (T*)out)));
   return DS_OK;
 }
 
 int ds_scal(ds_ctx* ctx, int dtype, int64_t n, double alpha, const void* x, void* out) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   DS_DISPATCH(dtype, T, DS_TRY(scal_launch<T>(ctx, n, alpha, (const T*)x, (T*)out)));
   return DS_OK;
 }
 
 int ds_dot(ds_ctx* ctx, int dtype, int64_t n, const void* x, const void* y, double* result) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   Scratch s;
   DS_TRY(get_scratch(ctx, (size_t)ctx->num_sms * 4, &s));
   int nblk = 0;
@@ -1234,7 +1234,7 @@ int ds_dot(ds_ctx* ctx, int dtype, int64_t n, const void* x, const void* y, doub
 }
 
 int ds_nrm2(ds_ctx* ctx, int dtype, int64_t n, const void* x, double* result) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (n == 0) {
     *result = 0.0;
     return DS_OK;
@@ -1248,7 +1248,7 @@ int ds_nrm2(ds_ctx* ctx, int dtype, int64_t n, const void* x, double* result) {
 }
 
 int ds_iamax(ds_ctx* ctx, int dtype, int64_t n, const void* x, int64_t* result) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (n <= 0) {
     set_error("iamax of empty vector");
     return DS_EDIM;
@@ -1267,7 +1267,7 @@ int ds_iamax(ds_ctx* ctx, int dtype, int64_t n, const void* x, int64_t* result) 
 
 int ds_gemv(ds_ctx* ctx, int dtype, int64_t m, int64_t n, const void* A, int64_t lda,
             const void* x, void* y) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (m == 0) return DS_OK;
   const GemvPlan p = gemv_plan(ctx, m, n, dtype_size(dtype));
   void* ws = nullptr;
@@ -1280,7 +1280,7 @@ int ds_gemv(ds_ctx* ctx, int dtype, int64_t m, int64_t n, const void* A, int64_t
 
 int ds_ger(ds_ctx* ctx, int dtype, int64_t m, int64_t n, const void* A, int64_t lda, double alpha,
            const void* x, const void* y, void* out, int64_t ldo) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   DS_DISPATCH(dtype, T,
               DS_TRY(ger_launch<T>(ctx, m, n, (const T*)A, lda, alpha, (const T*)x, (const T*)y,
                                    (T*)out, ldo)));
@@ -1290,7 +1290,7 @@ int ds_ger(ds_ctx* ctx, int dtype, int64_t m, int64_t n, const void* A, int64_t 
 int ds_gemm(ds_ctx* ctx, int dtype, int64_t m, int64_t n, int64_t k, double alpha, const void* A,
             int64_t lda, const void* B, int64_t ldb, double beta, const void* C, int64_t ldc,
             void* out, int64_t ldo) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   DS_DISPATCH(dtype, T,
               DS_TRY(gemm_launch<T>(ctx, m, n, k, alpha, (const T*)A, lda, (const T*)B, ldb, beta,
                                     (const T*)C, ldc, (T*)out, ldo)));
@@ -1299,7 +1299,7 @@ int ds_gemm(ds_ctx* ctx, int dtype, int64_t m, int64_t n, int64_t k, double alph
 
 int ds_trsm_lower_unit(ds_ctx* ctx, int dtype, int64_t b, int64_t m, const void* L, int64_t ldl,
                        const void* B, int64_t ldb, void* Z, int64_t ldz) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   DS_DISPATCH(dtype, T,
               DS_TRY(trsm_lower_unit_launch<T>(ctx, b, m, (const T*)L, ldl, (const T*)B, ldb,
                                                (T*)Z, ldz)));
@@ -1308,7 +1308,7 @@ int ds_trsm_lower_unit(ds_ctx* ctx, int dtype, int64_t b, int64_t m, const void*
 
 int ds_trsm_upper(ds_ctx* ctx, int dtype, int64_t b, int64_t m, const void* U, int64_t ldu,
                   const void* B, int64_t ldb, void* Z, int64_t ldz) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   DS_DISPATCH(dtype, T,
               DS_TRY(trsm_upper_launch<T>(ctx, b, m, (const T*)U, ldu, (const T*)B, ldb, (T*)Z,
                                           ldz)));
@@ -1317,7 +1317,7 @@ int ds_trsm_upper(ds_ctx* ctx, int dtype, int64_t b, int64_t m, const void* U, i
 
 int ds_symmetry_check(ds_ctx* ctx, int dtype, int64_t n, const void* A, int64_t lda,
                       double* maxdiff, double* amax) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (n == 0) {
     *maxdiff = 0.0;
     *amax = 0.0;
@@ -1339,7 +1339,7 @@ int ds_symmetry_check(ds_ctx* ctx, int dtype, int64_t n, const void* A, int64_t 
 
 int ds_relative_residual(ds_ctx* ctx, int dtype, int64_t n, const void* A, int64_t lda,
                          const void* x, const void* b, double* result) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   const GemvPlan p = gemv_plan(ctx, n, n, dtype_size(dtype));
   const int rblocks = (int)ceil_div(std::max<int64_t>(n, 1), 256);
   const size_t es = dtype_size(dtype);

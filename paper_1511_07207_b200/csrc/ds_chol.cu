@@ -309,7 +309,7 @@ extern "C" {
 
 int ds_cholesky_factor(ds_ctx* ctx, int dtype, int64_t n, void* A, int64_t lda, int64_t nb,
                        int64_t* h_bad_index) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (h_bad_index) *h_bad_index = -1;
   if (n < 0 || lda < std::max<int64_t>(n, 1)) {
     set_error("cholesky: bad shape n=%lld lda=%lld", (long long)n, (long long)lda);
@@ -349,7 +349,7 @@ int ds_cholesky_factor(ds_ctx* ctx, int dtype, int64_t n, void* A, int64_t lda, 
 
 int ds_cholesky_solve(ds_ctx* ctx, int dtype, int64_t n, const void* L, int64_t ldl, const void* b,
                       void* x, int64_t* h_bad_row) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (h_bad_row) *h_bad_row = -1;
   if (n == 0) return DS_OK;
   int64_t bad = -1;

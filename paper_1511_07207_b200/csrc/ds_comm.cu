@@ -82,7 +82,7 @@ int ds_comm_unique_id(unsigned char* out) {
 }
 
 int ds_comm_create(ds_ctx* ctx, int nranks, int rank, const unsigned char* id, ds_comm** out) {
-  DS_TRY(ds::ctx_begin(ctx));
+  DS_ENTER(ctx);
   DS_TRY(nccl_load());
   if (nranks < 1 || rank < 0 || rank >= nranks) {
     ds::set_error("bad communicator rank %d of %d", rank, nranks);
@@ -114,7 +114,7 @@ int ds_cg_shard_iterations(ds_ctx* ctx, ds_comm* comm, int dtype, int64_t n_loc,
                            int64_t lda, void* full, void* x, void* r, void* p, void* Ap, double* d_state,
                            double* d_hist, double* d_pap, double* d_pap_all, double* d_parts, double* d_rparts,
                            double tol, int64_t cap, int64_t k0, int64_t k1) {
-  DS_TRY(ds::ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (!comm) {
     ds::set_error("null communicator");
     return DS_EINVAL;

@@ -16,6 +16,7 @@
 
 #include <cmath>
 #include <cstdarg>
+#include <mutex>
 #include <string>
 
 #include "../../include/densolve_b200.h"
@@ -271,6 +272,10 @@ struct ds_ctx {
   cudaStream_t copy = nullptr;  // asynchronous host->device staging (ds_upload_async)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
   unsigned panel_seq = 0;  // LU panel launches (epochs of the LL exchange words)
+  // Serialises the entry points on this context: its workspace, streams, pinned buffer
+  // and events are shared state ("one solve at a time" per backend, backends.py:80-81).
+  // Recursive: a GMRES workspace sink may call back into the library on this thread.
+  std::recursive_mutex mu;
 };
 
 namespace ds {
@@ -279,6 +284,11 @@ int ctx_hostbuf(ds_ctx* ctx, size_t bytes, void** out);
 int ctx_begin(ds_ctx* ctx);  // cudaSetDevice
 inline void count_launch(ds_ctx* ctx, int n = 1) { ctx->launches += n; }
 }  // namespace ds
+
+// Entry-point prologue: select the device and hold the context's lock until return.
+#define DS_ENTER(ctx)                 \
+  DS_TRY(::ds::ctx_begin(ctx));       \
+  std::lock_guard<std::recursive_mutex> _ds_ctx_guard((ctx)->mu)
 
 #define DS_DISPATCH(dtype, T, ...)                              \
   do {                                                          \

@@ -156,7 +156,7 @@ int ds_ctx_destroy(ds_ctx* ctx) {
 }
 
 int ds_ctx_set_stream(ds_ctx* ctx, void* stream) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   DS_CUDA(cudaStreamSynchronize(ctx->stream));
   if (stream == nullptr) {
     if (!ctx->own_stream) {
@@ -172,7 +172,7 @@ int ds_ctx_set_stream(ds_ctx* ctx, void* stream) {
 }
 
 int ds_ctx_synchronize(ds_ctx* ctx) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   DS_CUDA(cudaStreamSynchronize(ctx->stream));
   return DS_OK;
 }
@@ -187,7 +187,7 @@ int ds_ctx_kernel_launches(ds_ctx* ctx, int64_t* out) {
 // release threshold: a multi-GB operand freed and re-allocated between solves is
 // recycled without a cudaMalloc / cudaFree round trip (no implicit device sync).
 int ds_malloc(ds_ctx* ctx, size_t bytes, void** out) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   *out = nullptr;
   if (bytes == 0) bytes = 16;
   DS_CUDA(cudaMallocAsync(out, bytes, ctx->stream));
@@ -196,7 +196,7 @@ int ds_malloc(ds_ctx* ctx, size_t bytes, void** out) {
 }
 
 int ds_free(ds_ctx* ctx, void* p) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (p) DS_CUDA(cudaFreeAsync(p, ctx->stream));
   return DS_OK;
 }
@@ -223,7 +223,7 @@ int ds_host_unregister(void* p) {
 }
 
 int ds_memcpy_h2d(ds_ctx* ctx, void* dst, const void* src, size_t bytes) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (bytes == 0) return DS_OK;
   DS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
   DS_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -231,7 +231,7 @@ int ds_memcpy_h2d(ds_ctx* ctx, void* dst, const void* src, size_t bytes) {
 }
 
 int ds_memcpy_d2h(ds_ctx* ctx, void* dst, const void* src, size_t bytes) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (bytes == 0) return DS_OK;
   DS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
   DS_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -239,14 +239,14 @@ int ds_memcpy_d2h(ds_ctx* ctx, void* dst, const void* src, size_t bytes) {
 }
 
 int ds_memcpy_d2d(ds_ctx* ctx, void* dst, const void* src, size_t bytes) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (bytes == 0) return DS_OK;
   DS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
   return DS_OK;
 }
 
 int ds_memset(ds_ctx* ctx, void* dst, int value, size_t bytes) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (bytes == 0) return DS_OK;
   DS_CUDA(cudaMemsetAsync(dst, value, bytes, ctx->stream));
   return DS_OK;
@@ -257,7 +257,7 @@ int ds_memset(ds_ctx* ctx, void* dst, int value, size_t bytes) {
 // destination is not in use by pending work; ds_wait_event orders a later solve after it.
 int ds_upload_async(ds_ctx* ctx, int dtype, const void* src, int64_t rows, int64_t cols, int64_t ld_host,
                     void* dst, int64_t ld_dev, void** event_out) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   *event_out = nullptr;
   if (rows < 0 || cols < 0 || ld_dev < (rows > 0 ? rows : 1) || ld_host < (rows > 0 ? rows : 1)) {
     set_error("upload_async: bad shape %lld x %lld", (long long)rows, (long long)cols);
@@ -276,7 +276,7 @@ int ds_upload_async(ds_ctx* ctx, int dtype, const void* src, int64_t rows, int64
 }
 
 int ds_wait_event(ds_ctx* ctx, void* event) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (event) DS_CUDA(cudaStreamWaitEvent(ctx->stream, (cudaEvent_t)event, 0));
   return DS_OK;
 }
@@ -288,7 +288,7 @@ int ds_event_destroy(void* event) {
 
 int ds_upload_matrix(ds_ctx* ctx, int dtype, const void* src, int64_t rows, int64_t cols,
                      int64_t ld_host, int order, void* dst, int64_t ld_dev) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (rows < 0 || cols < 0 || ld_dev < (rows > 0 ? rows : 1)) {
     set_error("upload: bad shape %lld x %lld ld_dev %lld", (long long)rows, (long long)cols,
               (long long)ld_dev);
@@ -318,7 +318,7 @@ int ds_upload_matrix(ds_ctx* ctx, int dtype, const void* src, int64_t rows, int6
 
 int ds_download_matrix(ds_ctx* ctx, int dtype, const void* src, int64_t rows, int64_t cols,
                        int64_t ld_dev, void* dst, int64_t ld_host) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (rows == 0 || cols == 0) return DS_OK;
   size_t es = dtype_size(dtype);
   DS_CUDA(cudaMemcpy2DAsync(dst, ld_host * es, src, ld_dev * es, rows * es, cols,

@@ -381,7 +381,7 @@ using namespace ds;
 extern "C" {
 
 int ds_vec_parts(ds_ctx* ctx, int dtype, int64_t n, const void* x, double* d_out3) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   void* ws = nullptr;
   const int g = vgrid(ctx, n);
   DS_TRY(ctx_workspace(ctx, (size_t)g * 3 * sizeof(double) + 256, &ws));
@@ -393,7 +393,7 @@ int ds_vec_parts(ds_ctx* ctx, int dtype, int64_t n, const void* x, double* d_out
 }
 
 int ds_dot_dev(ds_ctx* ctx, int dtype, int64_t n, const void* x, const void* y, double* d_out) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   void* ws = nullptr;
   DS_TRY(ctx_workspace(ctx, (size_t)ctx->num_sms * 8 * sizeof(double) + 256, &ws));
   int nb = 0;
@@ -403,7 +403,7 @@ int ds_dot_dev(ds_ctx* ctx, int dtype, int64_t n, const void* x, const void* y, 
 }
 
 int ds_gemv_acc(ds_ctx* ctx, int dtype, int64_t m, int64_t n, const void* A, int64_t lda, const void* x, void* y) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (m == 0) return DS_OK;
   const GemvPlan p = gemv_plan(ctx, m, n, dtype_size(dtype));
   void* ws = nullptr;
@@ -416,7 +416,7 @@ int ds_gemv_acc(ds_ctx* ctx, int dtype, int64_t m, int64_t n, const void* A, int
 
 int ds_resid_parts(ds_ctx* ctx, int dtype, int64_t m, int64_t n, const void* A, int64_t lda, const void* x,
                    const void* b, void* r, double* d_out3) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (m == 0) {
     DS_CUDA(cudaMemsetAsync(d_out3, 0, 3 * sizeof(double), ctx->stream));
     return DS_OK;
@@ -434,7 +434,7 @@ int ds_resid_parts(ds_ctx* ctx, int dtype, int64_t m, int64_t n, const void* A, 
 
 int ds_cg_shard_init(ds_ctx* ctx, const double* d_bparts, const double* d_rparts, int nranks, double* d_state,
                      double* d_hist, double tol, int64_t cap) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   cg_shard_init_kernel<<<1, 32, 0, ctx->stream>>>(d_bparts, d_rparts, nranks, d_state, d_hist, tol, cap);
   count_launch(ctx);
   DS_CHECK_LAUNCH();
@@ -443,7 +443,7 @@ int ds_cg_shard_init(ds_ctx* ctx, const double* d_bparts, const double* d_rparts
 
 int ds_cg_shard_update(ds_ctx* ctx, int dtype, int64_t n_loc, int nranks, const double* d_pap_parts,
                        double* d_state, int64_t k, void* x, void* r, const void* p, const void* Ap, double* d_out3) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   const int g = vgrid(ctx, n_loc);
   void* ws = nullptr;
   DS_TRY(ctx_workspace(ctx, (size_t)g * 3 * sizeof(double) + 256, &ws));
@@ -459,7 +459,7 @@ int ds_cg_shard_update(ds_ctx* ctx, int dtype, int64_t n_loc, int nranks, const 
 
 int ds_cg_shard_finish(ds_ctx* ctx, int dtype, int64_t n_loc, int nranks, const double* d_parts3, double* d_state,
                        int64_t k, const void* r, void* p, double* d_hist, double tol, int64_t cap) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   const int g = vgrid(ctx, n_loc);
   DS_DISPATCH(dtype, T,
               cg_shard_finish_kernel<T><<<g, kDT, 0, ctx->stream>>>(n_loc, nranks, d_parts3, d_state, k,
@@ -472,7 +472,7 @@ int ds_cg_shard_finish(ds_ctx* ctx, int dtype, int64_t n_loc, int nranks, const 
 
 int ds_multidot_dev(ds_ctx* ctx, int dtype, int64_t n_loc, const void* V, int64_t ldv, int kc, const void* w,
                     double* d_out) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (kc > 64) {
     set_error("multidot: kc > 64");
     return DS_EINVAL;
@@ -492,7 +492,7 @@ int ds_multidot_dev(ds_ctx* ctx, int dtype, int64_t n_loc, const void* V, int64_
 int ds_cgs_update_shard(ds_ctx* ctx, int dtype, int64_t n_loc, const void* V, int64_t ldv, int kc, void* w,
                         int nranks, const double* d_parts, void* Hcol, double* d_hsave, int pass, double* d_out3,
                         const double* d_state, int64_t k) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   const int g = vgrid(ctx, n_loc);
   void* ws = nullptr;
   DS_TRY(ctx_workspace(ctx, (size_t)g * 3 * sizeof(double) + 256, &ws));
@@ -510,7 +510,7 @@ int ds_cgs_update_shard(ds_ctx* ctx, int dtype, int64_t n_loc, const void* V, in
 int ds_gmres_shard_step(ds_ctx* ctx, int dtype, int64_t n_loc, void* w, int nranks, const double* d_parts3,
                         void* H, void* Hraw, int64_t ldh, void* g, void* cs, void* sn, int k, double* d_est,
                         double* d_state, double tol, int64_t total_before, int64_t cap) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   const int gr = vgrid(ctx, n_loc);
   DS_DISPATCH(dtype, T,
               gm_shard_normalize_kernel<T><<<gr, kDT, 0, ctx->stream>>>(n_loc, (T*)w, nranks, d_parts3, d_state, k));
@@ -525,7 +525,7 @@ int ds_gmres_shard_step(ds_ctx* ctx, int dtype, int64_t n_loc, void* w, int nran
 
 int ds_gmres_shard_start(ds_ctx* ctx, int dtype, int64_t n_loc, const void* r, void* v0, int nranks,
                          const double* d_parts3, void* g, double* d_state) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   const int gr = vgrid(ctx, n_loc);
   DS_DISPATCH(dtype, T,
               gm_shard_start_kernel<T><<<gr, kDT, 0, ctx->stream>>>(n_loc, (const T*)r, (T*)v0, nranks, d_parts3,
@@ -537,7 +537,7 @@ int ds_gmres_shard_start(ds_ctx* ctx, int dtype, int64_t n_loc, const void* r, v
 
 int ds_gmres_lsq(ds_ctx* ctx, int dtype, const void* H, int64_t ldh, const void* g, int inner, void* y,
                  double* d_state) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   DS_DISPATCH(dtype, T,
               gm_shard_lsq_kernel<T><<<1, 32, 0, ctx->stream>>>((const T*)H, ldh, (const T*)g, inner, (T*)y, d_state));
   count_launch(ctx);
@@ -547,7 +547,7 @@ int ds_gmres_lsq(ds_ctx* ctx, int dtype, const void* H, int64_t ldh, const void*
 
 int ds_absdiff_transposed(ds_ctx* ctx, int dtype, int64_t m, int64_t n, const void* A, int64_t lda, const void* B,
                           int64_t ldb, double* h_out2) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (m == 0 || n == 0) {
     h_out2[0] = h_out2[1] = 0.0;
     return DS_OK;
@@ -570,7 +570,7 @@ int ds_absdiff_transposed(ds_ctx* ctx, int dtype, int64_t m, int64_t n, const vo
 
 int ds_lu_panel(ds_ctx* ctx, int dtype, int64_t m, int64_t w, void* P, int64_t ldp, int64_t b, int64_t* d_piv,
                 int8_t* d_zero) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (m < w || ldp < std::max<int64_t>(m, 1) || b < 1) {
     set_error("lu_panel: need m >= w, ldp >= m, b >= 1 (m=%lld w=%lld)", (long long)m, (long long)w);
     return DS_EDIM;
@@ -582,7 +582,7 @@ int ds_lu_panel(ds_ctx* ctx, int dtype, int64_t m, int64_t w, void* P, int64_t l
 
 int ds_laswp(ds_ctx* ctx, int dtype, int64_t ncols, void* A, int64_t lda, int64_t k0, int64_t k1,
              const int64_t* d_piv) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (ncols <= 0 || k1 <= k0) return DS_OK;
   DS_DISPATCH(dtype, T, DS_TRY(laswp_range<T>(ctx, (T*)A, lda, ncols, k0, k1, d_piv)));
   return DS_OK;

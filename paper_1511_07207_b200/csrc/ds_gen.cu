@@ -418,7 +418,7 @@ extern "C" {
 
 int ds_rng_uniform(ds_ctx* ctx, int dtype, const uint64_t* h_pcg, uint64_t offset, int64_t rows, int64_t cols,
                    double low, double high, int colmajor, void* d_out, int64_t ld) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (dtype != DS_F64 && dtype != DS_F32) {
     set_error("unsupported dtype code %d", dtype);
     return DS_EPREC;
@@ -433,7 +433,7 @@ int ds_rng_uniform(ds_ctx* ctx, int dtype, const uint64_t* h_pcg, uint64_t offse
 
 int ds_generate(ds_ctx* ctx, int kind, int dtype, int64_t n, const uint64_t* h_pcg, void* d_A, int64_t lda,
                 void* d_b, void* d_x_true) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (n < 1 || lda < n) {
     set_error("generate: bad size n=%lld lda=%lld", (long long)n, (long long)lda);
     return DS_EDIM;

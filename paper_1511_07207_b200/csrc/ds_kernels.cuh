@@ -6,10 +6,10 @@ namespace ds {
 
 // ---- GEMV ------------------------------------------------------------------
 // y = A x for a column-major m x n matrix, streamed once from HBM.
-// Stage 1 (gemv_partial): grid (row tiles, column chunks); each CTA streams an
+// Stage 1 (ds_colstream_mv_kernel): grid (row tiles, column chunks); each CTA streams an
 //   (R x C) tile with 128-bit loads, x chunk staged in shared memory by a bulk
 //   async copy (cp.async.bulk, the 1-D TMA path), fp64 accumulation.
-// Stage 2 (gemv_reduce): sums the chunk partials in fixed chunk order (bitwise
+// Stage 2 (ds_colstream_reduce_kernel): sums the chunk partials in fixed chunk order (bitwise
 //   deterministic) and applies a fused epilogue.
 enum GemvEpi : int {
   EPI_STORE = 0,      // y = A x

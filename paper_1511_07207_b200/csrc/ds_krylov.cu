@@ -277,16 +277,20 @@ __global__ void __launch_bounds__(kT)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const double wi = i < n ? (double)w[i] : 0.0;
-  for (int j = 0; j < kc; ++j) {
-    double s = i < n ? (double)V[i + (int64_t)j * ldv] * wi : 0.0;
-    s = warp_sum(s);
-    if (lane == 0) sm[wid][j] = s;
-  }
-  __syncthreads();
-  for (int j = threadIdx.x; j < kc; j += blockDim.x) {
-    double s = 0.0;
-    for (int q = 0; q < kT / 32; ++q) s += sm[q][j];
-    part[(int64_t)blockIdx.x * ldp + j] = s;
+  for (int c0 = 0; c0 < kc; c0 += 64) {  // columns in chunks of 64 (restart_m > 62)
+    const int cn = min(64, kc - c0);
+    if (c0 > 0) __syncthreads();
+    for (int j = 0; j < cn; ++j) {
+      double s = i < n ? (double)V[i + (int64_t)(c0 + j) * ldv] * wi : 0.0;
+      s = warp_sum(s);
+      if (lane == 0) sm[wid][j] = s;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < cn; j += blockDim.x) {
+      double s = 0.0;
+      for (int q = 0; q < kT / 32; ++q) s += sm[q][j];
+      part[(int64_t)blockIdx.x * ldp + c0 + j] = s;
+    }
   }
 }
 
@@ -299,7 +303,7 @@ __global__ void __launch_bounds__(kT)
                       const double* __restrict__ part, int ldp, int nparts, T* Hcol,
                       double* hsave, int pass, double* red_ssq, Gate gate) {
   if (gated(gate)) return;
-  __shared__ double hs[64];
+  extern __shared__ double hs[];  // kc coefficients (dynamic: restart_m > 62)
   __shared__ double sm[64];
   for (int j = threadIdx.x; j < kc; j += blockDim.x) {
     double s = 0.0;
@@ -718,7 +722,7 @@ __global__ void __launch_bounds__(kOrthThreads, 1)
   const int nr = (int)max((int64_t)0, min(per, n - r0));
   const int kc = k + 1;
   T* w = V + (int64_t)(k + 1) * ldv;
-  // w = A v_k: the GEMV's chunk partials summed here, in chunk order (gemv_reduce_kernel's
+  // w = A v_k: the GEMV's chunk partials summed here, in chunk order (ds_colstream_reduce_kernel's
   // order, so w is bitwise the EPI_STORE result), up to 32 loads in flight
   for (int r = tid; r < nr; r += blockDim.x) {
     if (gpart == nullptr) {  // w already summed by the GEMV's reduce kernel
@@ -910,6 +914,29 @@ __global__ void gm_lsq_kernel(const T* H, int64_t ldh, const T* g, int inner, T*
   for (int k = 0; k < inner; ++k) y[k] = ys[k];
 }
 
+// the same recurrence for inner > 64 (restart_m > 62), straight from global memory
+template <typename T>
+__global__ void gm_lsq_global_kernel(const T* H, int64_t ldh, const T* g, int inner, T* y, GmDev* st) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int i = 0; i < inner; ++i) y[i] = g[i];
+  for (int i = inner - 1; i >= 0; --i) {
+    T yi = y[i];
+    if (i + 1 < inner) {
+      double s = 0.0;
+      for (int j = i + 1; j < inner; ++j) s = fma((double)H[i + (int64_t)j * ldh], (double)y[j], s);
+      yi = sub_rn(yi, (T)s);
+    }
+    y[i] = yi;
+    const T d = H[i + (int64_t)i * ldh];
+    if (d == T(0)) {
+      st->status = DS_ESINGULAR;
+      st->bad_row = i;
+      return;
+    }
+    y[i] = div_rn(yi, d);
+  }
+}
+
 // cycle start: V[:,0] = scal(1/beta, r); g = beta e1 (krylov.py:116-123)
 template <typename T>
 __global__ void gm_cycle_start_kernel(int64_t n, const T* __restrict__ r, T* __restrict__ v0,
@@ -945,9 +972,12 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
                ds_solve_info* info) {
   const int64_t launches0 = ctx->launches;
   const double u = (sizeof(T) == 8 ? 1.1102230246251565e-16 : 5.960464477539063e-08);
-  if (m > 62) {
-    // the on-device Givens/multi-dot kernels keep <= 64 coefficients in shared memory
-    set_error("restart_m = %lld exceeds the device limit of 62", (long long)m);
+  // restart_m > 62: the fused step kernel and the cluster kernel keep <= 64 coefficients
+  // on chip, so large m runs the split multidot / cgs_update / step_finish kernels
+  // (coefficients in dynamic shared / global memory) and the global-memory LS solve.
+  const bool big_m = m > 62;
+  if (m + 1 > 6144) {  // the CGS coefficients of one step live in <= 48 KB of shared memory
+    set_error("restart_m = %lld exceeds the supported maximum of 6143", (long long)m);
     return DS_EINVAL;
   }
   const GemvPlan gp = gemv_plan(ctx, n, n, sizeof(T));
@@ -956,13 +986,13 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
   const int mdb = (int)ceil_div(std::max<int64_t>(n, 1), kT);  // multidot blocks
   const int64_t ldv = ceil_div(std::max<int64_t>(n, 1), 4) * 4;
   const int64_t ldh = m + 1;
-  const int ldp = 64;
+  const int ldp = (int)std::max<int64_t>(64, ceil_div(m + 1, 64) * 64);
   // fused one-kernel Arnoldi step for n <= 148 * 128 (latency-bound sizes, e.g. C2)
   const char* fz = getenv("DENSOLVE_GMRES_FUSED");
   int64_t arn_g = std::min<int64_t>((int64_t)ctx->num_sms, ceil_div(n, 4));
   int64_t arn_per = ceil_div(ceil_div(n, arn_g), 4) * 4;  // 32-byte aligned row blocks
   arn_g = ceil_div(n, arn_per);
-  const bool fused = !(fz && fz[0] == '0') && arn_per <= kArnMaxRows;
+  const bool fused = !(fz && fz[0] == '0') && arn_per <= kArnMaxRows && !big_m;
   // cluster orthogonalisation (DENSOLVE_GMRES_ORTH=cluster|grid): the largest cluster
   // (16 non-portable, else 8) that the device can co-schedule; rows per CTA <= 4096
   int orth_cl = 0;
@@ -975,7 +1005,7 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
   unsigned long long* orth_trace = nullptr;
   {
     const char* oe = getenv("DENSOLVE_GMRES_ORTH");
-    const bool want = !(oe && strcmp(oe, "grid") == 0) && n <= 16 * 4096;
+    const bool want = !(oe && strcmp(oe, "grid") == 0) && n <= 16 * 4096 && !big_m;
     if (want) {
       static int best[2] = {-1, -1};
       int& bc = best[sizeof(T) == 8];
@@ -1023,7 +1053,7 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
                                                                            : (int)std::min<int64_t>(4, ceil_div(arn_per, 32));
   size_t need = gp.part_bytes + (size_t)ldv * (m + 1) * sizeof(T) + (size_t)n * sizeof(T) +
                 (fused ? ((size_t)2 * arn_g * 128 + 256) * sizeof(uint64_t) + 256 : 0) +
-                (size_t)(ldh * m * 2 + 3 * (m + 2) + 64) * sizeof(T) +
+                (size_t)(ldh * m * 2 + 3 * (m + 2) + m + 64) * sizeof(T) + (size_t)(2 * m + 2) * sizeof(double) +
                 ((size_t)mdb * ldp + (size_t)rblocks * 3 + (size_t)vg * 2 + 512) * sizeof(double) +
                 sizeof(GmDev) + 16 * 256;
   void* ws = nullptr;
@@ -1037,12 +1067,12 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
   T* g = cv.take<T>((size_t)(m + 2) * sizeof(T));
   T* cs = cv.take<T>((size_t)(m + 2) * sizeof(T));
   T* sn = cv.take<T>((size_t)(m + 2) * sizeof(T));
-  T* y = cv.take<T>((size_t)64 * sizeof(T));
+  T* y = cv.take<T>((size_t)std::max<int64_t>(m, 64) * sizeof(T));
   double* mpart = cv.take<double>((size_t)mdb * ldp * sizeof(double));
   double* red_a = cv.take<double>(((size_t)rblocks * 3 + 64) * sizeof(double));
   double* red_b = cv.take<double>(((size_t)std::max(vg, rblocks) * 2 + 64) * sizeof(double));
-  double* hsave = cv.take<double>(64 * sizeof(double));
-  double* est = cv.take<double>(64 * sizeof(double));
+  double* hsave = cv.take<double>((size_t)std::max<int64_t>(m + 1, 64) * sizeof(double));
+  double* est = cv.take<double>((size_t)std::max<int64_t>(m, 64) * sizeof(double));
   double* scal = cv.take<double>(64 * sizeof(double));
   GmDev* st = cv.take<GmDev>(sizeof(GmDev));
   uint64_t* arn_ll = fused ? cv.take<uint64_t>(((size_t)2 * arn_g * 128 + 256) * sizeof(uint64_t)) : nullptr;
@@ -1053,7 +1083,7 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
   }
 
   double* hbuf = nullptr;
-  DS_TRY(ctx_hostbuf(ctx, 4096, (void**)&hbuf));
+  DS_TRY(ctx_hostbuf(ctx, (size_t)(128 + m + 64) * sizeof(double), (void**)&hbuf));
 
   // ||b|| via nrm2 (krylov.py:87) and the plain ||b|| of relative_residual (core.py:207)
   int nb = 0;
@@ -1229,7 +1259,7 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
         const int passes = orth == DS_ORTH_CLASSICAL ? 1 : 2;
         for (int ps = 0; ps < passes; ++ps) {
           multidot_kernel<T><<<mdb, kT, 0, ctx->stream>>>(n, V, ldv, kc, w, mpart, ldp, gt);
-          cgs_update_kernel<T><<<vg, kT, 0, ctx->stream>>>(
+          cgs_update_kernel<T><<<vg, kT, (size_t)kc * sizeof(double), ctx->stream>>>(
               n, V, ldv, kc, w, mpart, ldp, mdb, H + k * ldh, hsave, ps,
               ps == passes - 1 ? red_b : nullptr, gt);
           count_launch(ctx, 2);
@@ -1249,7 +1279,10 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
     total_it += inner;
 
     // cycle end: y = H^-1 g ; x += V y   (krylov.py:166-167)
-    gm_lsq_kernel<T><<<1, 256, 0, ctx->stream>>>(H, ldh, g, inner, y, st);
+    if (inner <= 64)
+      gm_lsq_kernel<T><<<1, 256, 0, ctx->stream>>>(H, ldh, g, inner, y, st);
+    else
+      gm_lsq_global_kernel<T><<<1, 32, 0, ctx->stream>>>(H, ldh, g, inner, y, st);
     count_launch(ctx);
     {
       const GemvPlan gp2 = gemv_plan(ctx, n, inner, sizeof(T));
@@ -1704,7 +1737,7 @@ extern "C" {
 int ds_cg(ds_ctx* ctx, int dtype, int64_t n, const void* A, int64_t lda, const void* b,
           const void* x0, void* x, double tol, int64_t max_it, int check_sym, double* h_hist,
           int64_t hist_cap, ds_solve_info* info) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   *info = ds_solve_info{};
   info->error_index = -1;
   if (n <= 0) {
@@ -1728,7 +1761,7 @@ int ds_gmres(ds_ctx* ctx, int dtype, int64_t n, const void* A, int64_t lda, cons
              const void* x0, void* x, double tol, int64_t max_it, int64_t restart_m, int orth,
              double* h_hist, int64_t hist_cap, int64_t* h_cycles, int64_t cycles_cap,
              ds_sink_fn sink, void* sink_user, ds_solve_info* info) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   *info = ds_solve_info{};
   info->error_index = -1;
   if (n <= 0) {
@@ -1749,7 +1782,7 @@ int ds_gmres(ds_ctx* ctx, int dtype, int64_t n, const void* A, int64_t lda, cons
 int ds_bicgstab(ds_ctx* ctx, int dtype, int64_t n, const void* A, int64_t lda, const void* b,
                 const void* x0, void* x, double tol, int64_t max_it, double* h_hist,
                 int64_t hist_cap, ds_solve_info* info) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   *info = ds_solve_info{};
   info->error_index = -1;
   if (n <= 0) {

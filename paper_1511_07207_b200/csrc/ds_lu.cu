@@ -1530,27 +1530,6 @@ template int laswp_range<float>(ds_ctx*, float*, int64_t, int64_t, int64_t, int6
 // ----------------------------------------------------------------------------
 // pivots -> gather permutation: idx = apply_pivots(piv, arange(n))  (core.py:94-100)
 // ----------------------------------------------------------------------------
-__global__ void perm_build_kernel(int64_t n, const int64_t* __restrict__ piv, int* idx_g,
-                                  int use_smem) {
-  extern __shared__ int idx_s[];
-  int* idx = use_smem ? idx_s : idx_g;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) idx[i] = (int)i;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int64_t k = 0; k < n; ++k) {
-      const int64_t p = piv[k];
-      if (p != k) {
-        const int t = idx[k];
-        idx[k] = idx[p];
-        idx[p] = t;
-      }
-    }
-  }
-  __syncthreads();
-  if (use_smem)
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) idx_g[i] = idx_s[i];
-}
-
 template <typename T>
 __global__ void gather_kernel(int64_t n, const int* __restrict__ idx, const T* __restrict__ b,
                               T* __restrict__ out) {
@@ -1570,17 +1549,37 @@ constexpr int kTrsvThreads = 256;
 
 // TRANS (upper only): solve with U = M^T, i.e. U[i,j] = M[j + i*ld] (the
 // backward sweep of cholesky_solve on L^T, direct.py:166-171, without forming
-// L^T); the off-diagonal tiles are staged transposed through shared memory so
-// the loads stay coalesced.
+// L^T); tiles are staged transposed through shared memory so loads stay coalesced.
+//
+// Critical path per block = wait for the previous block's flag, one 64 x 64 tile
+// product from shared memory, the diagonal solve from shared memory, publish.  The
+// diagonal tile and the tile of the immediately preceding block are staged into
+// shared memory BEFORE the wait (they do not depend on the solution); the other
+// tiles' contributions are accumulated while earlier blocks are still solving.
+// The diagonal solve runs column by column in one warp (lane l owns rows l and
+// l + 32; the new unknown is broadcast with a shuffle and every owner folds it into
+// its row sum), so the chain has no global-memory load.
+template <typename T, bool TRANS>
+__device__ __forceinline__ void trsv_stage_tile(T (*tile)[kTrsvNB + 1], const T* __restrict__ M, int64_t ld,
+                                                int64_t r0, int nr, int64_t c0, int nc) {
+  // tile[r][c] = U[r0 + r, c0 + c]
+  for (int e = threadIdx.x; e < kTrsvNB * kTrsvNB; e += kTrsvThreads) {
+    const int fast = e % kTrsvNB, slow = e / kTrsvNB;
+    const int r = TRANS ? slow : fast, c = TRANS ? fast : slow;
+    if (r < nr && c < nc) tile[r][c] = TRANS ? M[(c0 + c) + (r0 + r) * ld] : M[(r0 + r) + (c0 + c) * ld];
+  }
+}
+
 template <typename T, bool LOWER, bool UNIT, bool TRANS = false>
 __global__ void __launch_bounds__(kTrsvThreads)
     trsv_kernel(int64_t n, const T* __restrict__ M, int64_t ld, const T* __restrict__ rhs,
                 T* out, int* flags, int* ticket) {
+  extern __shared__ __align__(16) unsigned char trsv_smem[];
+  T (*dg)[kTrsvNB + 1] = reinterpret_cast<T (*)[kTrsvNB + 1]>(trsv_smem);
+  T (*pv)[kTrsvNB + 1] = dg + kTrsvNB;  // tile of the previous block in the sweep
   __shared__ int s_blk;
   __shared__ double part[kTrsvThreads / kTrsvNB][kTrsvNB];
   __shared__ T xs[kTrsvNB];
-  __shared__ T ysol[kTrsvNB];
-  __shared__ T tile[TRANS ? kTrsvNB : 1][TRANS ? kTrsvNB + 1 : 1];
   const int64_t nblk = ceil_div(n, kTrsvNB);
   if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1);
   __syncthreads();
@@ -1589,77 +1588,92 @@ __global__ void __launch_bounds__(kTrsvThreads)
   const int64_t r0 = bi * kTrsvNB;
   const int nr = (int)min((int64_t)kTrsvNB, n - r0);
   const int rr = threadIdx.x % kTrsvNB, cg = threadIdx.x / kTrsvNB;
+  trsv_stage_tile<T, TRANS>(dg, M, ld, r0, nr, r0, nr);
+  int64_t cprev = 0;
+  int ncprev = 0;
+  if (t > 0) {
+    const int64_t bj = LOWER ? t - 1 : nblk - t;
+    cprev = bj * kTrsvNB;
+    ncprev = (int)min((int64_t)kTrsvNB, n - cprev);
+    trsv_stage_tile<T, TRANS>(pv, M, ld, r0, nr, cprev, ncprev);
+  }
   double acc = 0.0;
-  // contributions of the already-solved blocks
-  for (int64_t s = 0; s < t; ++s) {
+  // contributions of the blocks solved earlier (all but the immediately preceding one)
+  for (int64_t s = 0; s + 1 < t; ++s) {
     const int64_t bj = LOWER ? s : nblk - 1 - s;
     const int64_t c0 = bj * kTrsvNB;
     const int nc = (int)min((int64_t)kTrsvNB, n - c0);
     if (threadIdx.x == 0) {
-      while (((volatile int*)flags)[bj] == 0) __nanosleep(64);
+      while (((volatile int*)flags)[bj] == 0) __nanosleep(32);
       __threadfence();
     }
     __syncthreads();
     if (threadIdx.x < nc) xs[threadIdx.x] = ((volatile T*)out)[c0 + threadIdx.x];
-    if (TRANS) {
-      // tile[r][c] = U[r0 + r, c0 + c] = M[(c0 + c) + (r0 + r) * ld]; consecutive threads read
-      // consecutive c (contiguous in M)
-      for (int e = threadIdx.x; e < kTrsvNB * kTrsvNB; e += kTrsvThreads) {
-        const int c = e % kTrsvNB, r = e / kTrsvNB;
-        if (r < nr && c < nc) tile[r][c] = M[(c0 + c) + (r0 + r) * ld];
+    __syncthreads();
+    if (rr < nr) {
+      if (TRANS) {
+        // coalesced along c for the transposed view: thread (rr, cg) reads U[r0+rr, c0+c] = M[c0+c + (r0+rr) ld]
+        for (int c = cg; c < nc; c += kTrsvThreads / kTrsvNB)
+          acc = fma((double)M[(c0 + c) + (r0 + rr) * ld], (double)xs[c], acc);
+      } else {
+        for (int c = cg; c < nc; c += kTrsvThreads / kTrsvNB)
+          acc = fma((double)M[(r0 + rr) + (c0 + c) * ld], (double)xs[c], acc);
       }
     }
+  }
+  if (t > 0) {  // the preceding block: wait, then its staged tile
+    if (threadIdx.x == 0) {
+      const int64_t bj = LOWER ? t - 1 : nblk - t;
+      while (((volatile int*)flags)[bj] == 0) __nanosleep(16);
+      __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x < ncprev) xs[threadIdx.x] = ((volatile T*)out)[cprev + threadIdx.x];
     __syncthreads();
     if (rr < nr)
-      for (int c = cg; c < nc; c += kTrsvThreads / kTrsvNB) {
-        const T mv = TRANS ? tile[rr][c] : M[(r0 + rr) + (c0 + c) * ld];
-        acc = fma((double)mv, (double)xs[c], acc);
-      }
-    __syncthreads();
+      for (int c = cg; c < ncprev; c += kTrsvThreads / kTrsvNB) acc = fma((double)pv[rr][c], (double)xs[c], acc);
   }
   part[cg][rr] = acc;
   __syncthreads();
-  // diagonal block: one warp, sequential rows
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
-    if (LOWER) {
-      for (int r = 0; r < nr; ++r) {
-        double s = 0.0;
-        for (int c = lane; c < r; c += 32) s = fma((double)M[(r0 + r) + (r0 + c) * ld], (double)ysol[c], s);
-        s = warp_sum(s);
-        if (lane == 0) {
-          double off = s;
-          for (int q = 0; q < kTrsvThreads / kTrsvNB; ++q) off += part[q][r];
-          T v = sub_rn(rhs[r0 + r], (T)off);  // y[i] -= L[i,:i] @ y[:i]
-          if (!UNIT) v = div_rn(v, M[(r0 + r) + (r0 + r) * ld]);
-          ysol[r] = v;
-        }
-        __syncwarp();
-      }
-    } else {
-      for (int r = nr - 1; r >= 0; --r) {
-        double s = 0.0;
-        for (int c = r + 1 + lane; c < nr; c += 32) {
-          const T mv = TRANS ? M[(r0 + c) + (r0 + r) * ld] : M[(r0 + r) + (r0 + c) * ld];
-          s = fma((double)mv, (double)ysol[c], s);
-        }
-        s = warp_sum(s);
-        if (lane == 0) {
-          double off = s;
-          for (int q = 0; q < kTrsvThreads / kTrsvNB; ++q) off += part[q][r];
-          T v = sub_rn(rhs[r0 + r], (T)off);  // x[i] -= U[i,i+1:] @ x[i+1:]
-          v = div_rn(v, M[(r0 + r) + (r0 + r) * ld]);  // x[i] /= U[i,i]
-          ysol[r] = v;
-        }
-        __syncwarp();
-      }
+    // off-diagonal sums of my two rows, then the column sweep of the diagonal block
+    double off0 = 0.0, off1 = 0.0;
+    for (int q = 0; q < kTrsvThreads / kTrsvNB; ++q) {
+      off0 += part[q][lane];
+      off1 += part[q][lane + 32];
     }
+    const T b0 = lane < nr ? rhs[r0 + lane] : T(0);
+    const T b1 = lane + 32 < nr ? rhs[r0 + lane + 32] : T(0);
+    T y0 = T(0), y1 = T(0);
+    for (int step = 0; step < nr; ++step) {
+      const int c = LOWER ? step : nr - 1 - step;
+      const bool mine1 = c >= 32;
+      const int owner = c & 31;
+      T v = T(0);
+      if (lane == owner) {
+        const double off = mine1 ? off1 : off0;
+        v = sub_rn(mine1 ? b1 : b0, (T)off);  // y[i] -= L[i,:i] @ y[:i] / x[i] -= U[i,i+1:] @ x[i+1:]
+        if (!UNIT) v = div_rn(v, dg[c][c]);   // x[i] /= U[i,i]
+        if (mine1) y1 = v; else y0 = v;
+      }
+      v = __shfl_sync(0xffffffffu, v, owner);
+      // fold the new unknown into the rows still to be solved
+      const int ra = lane, rb = lane + 32;
+      if (LOWER ? (ra > c && ra < nr) : (ra < c)) off0 = fma((double)dg[ra][c], (double)v, off0);
+      if (LOWER ? (rb > c && rb < nr) : (rb < c)) off1 = fma((double)dg[rb][c], (double)v, off1);
+    }
+    if (lane < nr) out[r0 + lane] = y0;
+    if (lane + 32 < nr) out[r0 + lane + 32] = y1;
   }
-  __syncthreads();
-  if (threadIdx.x < nr) out[r0 + threadIdx.x] = ysol[threadIdx.x];
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) atomicExch(flags + bi, 1);
+}
+
+template <typename T>
+static int trsv_smem_bytes() {
+  return (int)(2 * kTrsvNB * (kTrsvNB + 1) * sizeof(T));
 }
 
 // zero-diagonal scan: first offending row in the reference's sweep order
@@ -1684,7 +1698,9 @@ int trsv_upper_trans_launch(ds_ctx* ctx, int64_t n, const T* M, int64_t ld, cons
   int* ticket = (int*)scratch;
   int* flags = ticket + 64;
   DS_CUDA(cudaMemsetAsync(scratch, 0, (64 + nblk) * sizeof(int), ctx->stream));
-  trsv_kernel<T, false, false, true><<<(unsigned)nblk, kTrsvThreads, 0, ctx->stream>>>(
+  const int sm = trsv_smem_bytes<T>();
+  DS_CUDA(cudaFuncSetAttribute(trsv_kernel<T, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+  trsv_kernel<T, false, false, true><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(
       n, M, ld, rhs, out, flags, ticket);
   count_launch(ctx);
   DS_CHECK_LAUNCH();
@@ -1703,15 +1719,17 @@ int trsv_launch(ds_ctx* ctx, int64_t n, const T* M, int64_t ld, const T* rhs, T*
   int* ticket = (int*)scratch;
   int* flags = ticket + 64;
   DS_CUDA(cudaMemsetAsync(scratch, 0, (64 + nblk) * sizeof(int), ctx->stream));
-  if (lower && unit)
-    trsv_kernel<T, true, true><<<(unsigned)nblk, kTrsvThreads, 0, ctx->stream>>>(n, M, ld, rhs, out,
-                                                                                 flags, ticket);
-  else if (lower)
-    trsv_kernel<T, true, false><<<(unsigned)nblk, kTrsvThreads, 0, ctx->stream>>>(n, M, ld, rhs,
-                                                                                  out, flags, ticket);
-  else
-    trsv_kernel<T, false, false><<<(unsigned)nblk, kTrsvThreads, 0, ctx->stream>>>(n, M, ld, rhs,
-                                                                                   out, flags, ticket);
+  const int sm = trsv_smem_bytes<T>();
+  if (lower && unit) {
+    DS_CUDA(cudaFuncSetAttribute(trsv_kernel<T, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    trsv_kernel<T, true, true><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(n, M, ld, rhs, out, flags, ticket);
+  } else if (lower) {
+    DS_CUDA(cudaFuncSetAttribute(trsv_kernel<T, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    trsv_kernel<T, true, false><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(n, M, ld, rhs, out, flags, ticket);
+  } else {
+    DS_CUDA(cudaFuncSetAttribute(trsv_kernel<T, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    trsv_kernel<T, false, false><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(n, M, ld, rhs, out, flags, ticket);
+  }
   count_launch(ctx);
   DS_CHECK_LAUNCH();
   return DS_OK;
@@ -1740,8 +1758,7 @@ int diag_check(ds_ctx* ctx, int64_t n, const T* M, int64_t ld, bool lower, int64
 }
 
 template <typename T>
-int lu_solve_impl(ds_ctx* ctx, int64_t n, const T* LU, int64_t ld, const int64_t* d_piv,
-                  const T* b, T* x) {
+int lu_solve_impl(ds_ctx* ctx, int64_t n, const T* LU, int64_t ld, const int* h_idx, const T* b, T* x) {
   void* ws = nullptr;
   const size_t need = (size_t)n * (sizeof(int) + sizeof(T) * 2) + (size_t)(ceil_div(n, 64) + 64) * 4 + 8 * 256;
   DS_TRY(ctx_workspace(ctx, need, &ws));
@@ -1750,16 +1767,10 @@ int lu_solve_impl(ds_ctx* ctx, int64_t n, const T* LU, int64_t ld, const int64_t
   T* pb = cv.take<T>((size_t)n * sizeof(T));
   T* y = cv.take<T>((size_t)n * sizeof(T));
   char* scratch = cv.take<char>((size_t)(ceil_div(n, 64) + 64) * 4);
-  const size_t smem = (size_t)n * sizeof(int);
-  const int use_smem = smem <= ctx->smem_optin ? 1 : 0;
-  if (use_smem) {
-    DS_CUDA(cudaFuncSetAttribute(perm_build_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-  }
-  perm_build_kernel<<<1, 1024, use_smem ? smem : 0, ctx->stream>>>(n, d_piv, idx, use_smem);
+  DS_CUDA(cudaMemcpyAsync(idx, h_idx, (size_t)n * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
   gather_kernel<T><<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 1024), 256, 0, ctx->stream>>>(
       n, idx, b, pb);
-  count_launch(ctx, 2);
+  count_launch(ctx, 1);
   DS_CHECK_LAUNCH();
   DS_TRY(trsv_launch<T>(ctx, n, LU, ld, pb, y, true, true, scratch));
   DS_TRY(trsv_launch<T>(ctx, n, LU, ld, y, x, false, false, scratch));
@@ -1774,7 +1785,7 @@ extern "C" {
 
 int ds_lu_factor_dev(ds_ctx* ctx, int dtype, int64_t n, void* A, int64_t lda, int64_t nb,
                      int64_t* d_piv, int32_t* h_singular) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (n < 0 || lda < std::max<int64_t>(n, 1)) {
     set_error("lu: bad shape n=%lld lda=%lld", (long long)n, (long long)lda);
     return DS_EDIM;
@@ -1808,7 +1819,7 @@ int ds_lu_factor_dev(ds_ctx* ctx, int dtype, int64_t n, void* A, int64_t lda, in
 
 int ds_lu_factor(ds_ctx* ctx, int dtype, int64_t n, void* A, int64_t lda, int64_t nb,
                  int64_t* h_piv, int8_t* h_zero_cols, int32_t* h_singular) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (n < 0 || lda < std::max<int64_t>(n, 1)) {
     set_error("lu: bad shape n=%lld lda=%lld", (long long)n, (long long)lda);
     return DS_EDIM;
@@ -1846,23 +1857,31 @@ int ds_lu_factor(ds_ctx* ctx, int dtype, int64_t n, void* A, int64_t lda, int64_
 
 int ds_lu_solve(ds_ctx* ctx, int dtype, int64_t n, const void* LU, int64_t lda,
                 const int64_t* h_piv, const void* b, void* x) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (n == 0) return DS_OK;
-  int64_t* d_piv = nullptr;
-  DS_CUDA(cudaMallocAsync((void**)&d_piv, (size_t)n * sizeof(int64_t), ctx->stream));
-  DS_CUDA(cudaMemcpyAsync(d_piv, h_piv, (size_t)n * sizeof(int64_t), cudaMemcpyHostToDevice,
-                          ctx->stream));
+  // gather permutation idx = apply_pivots(piv, arange(n)) (core.py:94-100): the swap
+  // sequence is inherently serial, so it is composed here on the host (n int swaps)
+  // into the context's pinned buffer and shipped with one copy
+  int* h_idx = nullptr;
+  DS_TRY(ctx_hostbuf(ctx, (size_t)n * sizeof(int), (void**)&h_idx));
+  for (int64_t i = 0; i < n; ++i) h_idx[i] = (int)i;
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t p = h_piv[k];
+    if (p < 0 || p >= n) {
+      set_error("lu_solve: pivot %lld at row %lld out of range", (long long)p, (long long)k);
+      return DS_EINVAL;
+    }
+    if (p != k) std::swap(h_idx[k], h_idx[p]);
+  }
   int rc = DS_OK;
-  DS_DISPATCH(dtype, T,
-              rc = lu_solve_impl<T>(ctx, n, (const T*)LU, lda, d_piv, (const T*)b, (T*)x));
-  DS_CUDA(cudaFreeAsync(d_piv, ctx->stream));
-  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  DS_DISPATCH(dtype, T, rc = lu_solve_impl<T>(ctx, n, (const T*)LU, lda, h_idx, (const T*)b, (T*)x));
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));  // also keeps h_idx alive until the copy ran
   return rc;
 }
 
 int ds_forward_substitution(ds_ctx* ctx, int dtype, int64_t n, const void* L, int64_t ldl,
                             const void* b, void* y, int unit_diagonal, int64_t* h_bad_row) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (h_bad_row) *h_bad_row = -1;
   if (n == 0) return DS_OK;
   void* ws = nullptr;
@@ -1885,7 +1904,7 @@ int ds_forward_substitution(ds_ctx* ctx, int dtype, int64_t n, const void* L, in
 
 int ds_backward_substitution(ds_ctx* ctx, int dtype, int64_t n, const void* U, int64_t ldu,
                              const void* y, void* x, int64_t* h_bad_row) {
-  DS_TRY(ctx_begin(ctx));
+  DS_ENTER(ctx);
   if (h_bad_row) *h_bad_row = -1;
   if (n == 0) return DS_OK;
   void* ws = nullptr;

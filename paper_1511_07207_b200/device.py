@@ -67,6 +67,16 @@ class DeviceArray:
     def dcode(self) -> int:
         return _lib.dtype_code(self.dtype)
 
+    @property
+    def __cuda_array_interface__(self):
+        """Zero-copy view for CUDA-aware consumers (e.g. ``torch.as_tensor(d, device="cuda")``):
+        a 2-d array is column-major with the padded leading dimension.  No stream is named;
+        the consumer orders its work after the library's stream itself."""
+        it = self.dtype.itemsize
+        strides = None if self.ndim == 1 else (it, self.ld * it)
+        return {"shape": self.shape, "typestr": self.dtype.str, "data": (self.ptr, False),
+                "strides": strides, "version": 2}
+
     def free(self):
         self._fin()
 

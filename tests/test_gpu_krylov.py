@@ -280,3 +280,26 @@ def test_cross_validation_with_lu(backend):
             x, rep = cg_solve(A, b, np.zeros_like(b), SolverConfig(tolerance=1e-4), backend)
             x_lu = lu_solve(lu_factor_blocked(A, 64, backend), b)
             assert np.linalg.norm(x - x_lu, np.inf) / np.linalg.norm(x_lu, np.inf) <= 1e-2
+
+
+@pytest.mark.parametrize("orth", ["modified", "classical"])
+@pytest.mark.parametrize("m", [63, 100])
+def test_gmres_large_restart_m(backend, orth, m):
+    """restart_m > 62 (the reference accepts any m >= 1, core.py:180): the split kernels
+    with dynamic shared memory and, for inner > 64, the global-memory LS solve.  A =
+    U[-1,1] + 12 I at n=300 contracts ~0.8 per step, so tol 1e-10 needs > 100 inner steps
+    (two cycles at m=100, the first one 100 steps long)."""
+    n = 300
+    rng = np.random.default_rng(11)
+    A = np.asfortranarray(rng.uniform(-1, 1, (n, n)) + 12.0 * np.eye(n))
+    b = rng.uniform(-1, 1, n)
+    cfg = SolverConfig(tolerance=1e-10, restart_m=m, orthogonalization=orth)
+    x, rep = gmres_solve(A, b, np.zeros(n), cfg, backend)
+    xo, ro = O.gmres(A, b, np.zeros(n), 1e-10, m, orth=orth)
+    assert rep.converged and ro["converged"]
+    assert abs(rep.iterations - ro["iterations"]) <= 1
+    assert rep.iterations > 64 or m == 63
+    assert rep.restart_cycles == ro["cycles"]
+    k = min(len(rep.residual_history), len(ro["history"])) - 1
+    np.testing.assert_allclose(rep.residual_history[:k], ro["history"][:k], rtol=1e-6)
+    assert np.max(np.abs(x - xo)) <= 1e-8 * np.max(np.abs(xo))

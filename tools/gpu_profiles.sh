@@ -20,7 +20,7 @@ timeout 600 $NCU --set full --clock-control none --import-source on -k regex:arn
   -o $out/orth_full_$tag -f python tools/profile_run.py gmres 4096 > /dev/null 2>&1; echo "orth full $?"
 timeout 600 $NCU --set full --clock-control none --import-source on -k regex:lu_panel_warp -s 10 -c 1 \
   -o $out/panelw_full_$tag -f python tools/profile_run.py lu 16384 > /dev/null 2>&1; echo "poller panel full $?"
-timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemv_partial -s 2 -c 1 \
+timeout 600 $NCU --set full --clock-control none --import-source on -k regex:colstream_mv -s 2 -c 1 \
   -o $out/gemv_full_$tag -f python tools/profile_run.py gemv 32768 > /dev/null 2>&1; echo "gemv full $?"
 timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemm64 -s 1 -c 1 \
   -o $out/gemm_full_$tag -f python tools/profile_run.py gemm 16384 16384 512 > /dev/null 2>&1; echo "gemm full $?"

@@ -33,7 +33,7 @@ if [[ $ph == *l* ]]; then
   python tools/launch_summary.py $out/launches_lu_$tag.csv | head -20
 fi
 if [[ $ph == *f* ]]; then
-  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:gemv_partial -s 2 -c 1 \
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:colstream_mv -s 2 -c 1 \
     -o $out/gemv_full_$tag -f python tools/profile_run.py gemv 32768 > $out/ncu_full_$tag.log 2>&1
   echo "ncu full gemv exit $?"
   timeout 900 $NCU --set full --clock-control none --import-source on -k regex:gemm64 -s 10 -c 1 \
