@@ -275,7 +275,7 @@ __global__ void diag_zero_first_kernel(int64_t n, const T* M, int64_t ld, long l
 template <typename T>
 int chol_solve_impl(ds_ctx* ctx, int64_t n, const T* L, int64_t ld, const T* b, T* x, int64_t* bad) {
   void* ws = nullptr;
-  const size_t sc = (size_t)(ceil_div(n, 64) + 128) * 4;
+  const size_t sc = trsv_scratch_bytes(n);
   DS_TRY(ctx_workspace(ctx, (size_t)n * sizeof(T) + sc + 1024, &ws));
   Carver cv{(char*)ws};
   long long* d_bad = cv.take<long long>(sizeof(long long) * 2);

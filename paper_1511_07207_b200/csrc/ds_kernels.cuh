@@ -116,7 +116,8 @@ int ger_launch(ds_ctx* ctx, int64_t m, int64_t n, const T* A, int64_t lda, doubl
                const T* x, const T* y, T* out, int64_t ldo);
 
 // ---- triangular vector solves (ds_lu.cu) -------------------------------------
-// scratch: (ceil(n/64) + 64) ints
+// scratch: trsv_scratch_bytes(n) (ticket, done counter, 16 B of LL words per unknown)
+inline size_t trsv_scratch_bytes(int64_t n) { return 512 + 16 * (size_t)(n > 0 ? n : 1); }
 template <typename T>
 int trsv_launch(ds_ctx* ctx, int64_t n, const T* M, int64_t ld, const T* rhs, T* out, bool lower,
                 bool unit, char* scratch);

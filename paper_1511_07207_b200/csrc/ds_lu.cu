@@ -1548,17 +1548,18 @@ constexpr int kTrsvNB = 64;
 constexpr int kTrsvThreads = 256;
 
 // TRANS (upper only): solve with U = M^T, i.e. U[i,j] = M[j + i*ld] (the
-// backward sweep of cholesky_solve on L^T, direct.py:166-171, without forming
-// L^T); tiles are staged transposed through shared memory so loads stay coalesced.
+// backward sweep of cholesky_solve on L^T, direct.py:166-171, without forming L^T).
 //
-// Critical path per block = wait for the previous block's flag, one 64 x 64 tile
-// product from shared memory, the diagonal solve from shared memory, publish.  The
-// diagonal tile and the tile of the immediately preceding block are staged into
-// shared memory BEFORE the wait (they do not depend on the solution); the other
-// tiles' contributions are accumulated while earlier blocks are still solving.
-// The diagonal solve runs column by column in one warp (lane l owns rows l and
-// l + 32; the new unknown is broadcast with a shuffle and every owner folds it into
-// its row sum), so the chain has no global-memory load.
+// Blocks finish strictly in sweep order (block t waits for block t-1), so ONE
+// monotonic counter `done` (= blocks solved) replaces per-block flags: a CTA reads it
+// once and folds in every solved block up to it as one flat, deep-unrolled stream over
+// columns (no per-tile handshake).  Critical path per block = the counter reaching
+// t, the tile of block t-1 (staged in shared memory before the wait, like the
+// diagonal tile), the diagonal solve from shared memory, publish.  The diagonal solve
+// runs column by column in one warp (lane l owns rows l and l + 32; the new unknown is
+// broadcast with a shuffle and folded into the rows still to solve).
+// Summation order is fixed (each column always goes to the same warp / lane, visited in
+// sweep order), so results are bitwise reproducible run to run.
 template <typename T, bool TRANS>
 __device__ __forceinline__ void trsv_stage_tile(T (*tile)[kTrsvNB + 1], const T* __restrict__ M, int64_t ld,
                                                 int64_t r0, int nr, int64_t c0, int nc) {
@@ -1570,16 +1571,53 @@ __device__ __forceinline__ void trsv_stage_tile(T (*tile)[kTrsvNB + 1], const T*
   }
 }
 
+// LL words: each 8-byte word carries 32 data bits and a 32-bit flag (1; the buffer is zeroed
+// per launch), so a reader polling the word needs no fence: fp64 values use two words.
+template <typename T>
+__device__ __forceinline__ void trsv_ll_write(uint64_t* p, T v) {
+  uint64_t bits = sizeof(T) == 8 ? (uint64_t)__double_as_longlong((double)v) : (uint64_t)__float_as_uint((float)v);
+  const uint64_t w0 = (1ull << 32) | (bits & 0xffffffffull);
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;\n" ::"l"(p), "l"(w0) : "memory");
+  if (sizeof(T) == 8) {
+    const uint64_t w1 = (1ull << 32) | (bits >> 32);
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;\n" ::"l"(p + 1), "l"(w1) : "memory");
+  }
+}
+template <typename T>
+__device__ __forceinline__ T trsv_ll_read(const uint64_t* p) {
+  uint64_t w0, w1 = 0;
+  do {
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(w0) : "l"(p) : "memory");
+  } while ((w0 >> 32) != 1u);
+  if (sizeof(T) == 8) {
+    do {
+      asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(w1) : "l"(p + 1) : "memory");
+    } while ((w1 >> 32) != 1u);
+    return (T)__longlong_as_double((long long)((w1 << 32) | (w0 & 0xffffffffull)));
+  }
+  return (T)__uint_as_float((unsigned)(w0 & 0xffffffffull));
+}
+
+__device__ __forceinline__ int ld_acquire_s32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 template <typename T, bool LOWER, bool UNIT, bool TRANS = false>
 __global__ void __launch_bounds__(kTrsvThreads)
     trsv_kernel(int64_t n, const T* __restrict__ M, int64_t ld, const T* __restrict__ rhs,
-                T* out, int* flags, int* ticket) {
+                T* out, int* done, int* ticket, uint64_t* __restrict__ ll) {
   extern __shared__ __align__(16) unsigned char trsv_smem[];
   T (*dg)[kTrsvNB + 1] = reinterpret_cast<T (*)[kTrsvNB + 1]>(trsv_smem);
   T (*pv)[kTrsvNB + 1] = dg + kTrsvNB;  // tile of the previous block in the sweep
+  constexpr int NW = kTrsvThreads / 32;
   __shared__ int s_blk;
-  __shared__ double part[kTrsvThreads / kTrsvNB][kTrsvNB];
+  __shared__ double part[NW][kTrsvNB];
   __shared__ T xs[kTrsvNB];
+  __shared__ double rv[kTrsvNB];
+  __shared__ double rdiag[kTrsvNB];
+  double (*dinv)[kTrsvNB + 1] = reinterpret_cast<double (*)[kTrsvNB + 1]>(pv + kTrsvNB);
   const int64_t nblk = ceil_div(n, kTrsvNB);
   if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1);
   __syncthreads();
@@ -1587,7 +1625,7 @@ __global__ void __launch_bounds__(kTrsvThreads)
   const int64_t bi = LOWER ? t : nblk - 1 - t;
   const int64_t r0 = bi * kTrsvNB;
   const int nr = (int)min((int64_t)kTrsvNB, n - r0);
-  const int rr = threadIdx.x % kTrsvNB, cg = threadIdx.x / kTrsvNB;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   trsv_stage_tile<T, TRANS>(dg, M, ld, r0, nr, r0, nr);
   int64_t cprev = 0;
   int ncprev = 0;
@@ -1597,83 +1635,197 @@ __global__ void __launch_bounds__(kTrsvThreads)
     ncprev = (int)min((int64_t)kTrsvNB, n - cprev);
     trsv_stage_tile<T, TRANS>(pv, M, ld, r0, nr, cprev, ncprev);
   }
-  double acc = 0.0;
-  // contributions of the blocks solved earlier (all but the immediately preceding one)
-  for (int64_t s = 0; s + 1 < t; ++s) {
-    const int64_t bj = LOWER ? s : nblk - 1 - s;
-    const int64_t c0 = bj * kTrsvNB;
-    const int nc = (int)min((int64_t)kTrsvNB, n - c0);
-    if (threadIdx.x == 0) {
-      while (((volatile int*)flags)[bj] == 0) __nanosleep(32);
-      __threadfence();
+  // rhs of my row (threads < 64), loaded before any wait
+  const T bme = threadIdx.x < nr ? rhs[r0 + threadIdx.x] : T(0);
+  // D^-1 of the diagonal block in fp64 (unit: the stored diagonal is ignored), one thread
+  // per column, before any wait: off the critical path of the sweep
+  __syncthreads();
+  if (threadIdx.x < kTrsvNB) rdiag[threadIdx.x] = (UNIT || threadIdx.x >= nr) ? 1.0 : 1.0 / (double)dg[threadIdx.x][threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x < nr) {
+    const int j = threadIdx.x;
+    if (LOWER) {
+      for (int i = 0; i < nr; ++i) {
+        double v = 0.0;
+        if (i >= j) {
+          v = i == j ? 1.0 : 0.0;
+          for (int k = j; k < i; ++k) v = fma(-(double)dg[i][k], dinv[k][j], v);
+          v *= rdiag[i];
+        }
+        dinv[i][j] = v;
+      }
+    } else {
+      for (int i = nr - 1; i >= 0; --i) {
+        double v = 0.0;
+        if (i <= j) {
+          v = i == j ? 1.0 : 0.0;
+          for (int k = i + 1; k <= j; ++k) v = fma(-(double)dg[i][k], dinv[k][j], v);
+          v *= rdiag[i];
+        }
+        dinv[i][j] = v;
+      }
     }
-    __syncthreads();
-    if (threadIdx.x < nc) xs[threadIdx.x] = ((volatile T*)out)[c0 + threadIdx.x];
-    __syncthreads();
-    if (rr < nr) {
-      if (TRANS) {
-        // coalesced along c for the transposed view: thread (rr, cg) reads U[r0+rr, c0+c] = M[c0+c + (r0+rr) ld]
-        for (int c = cg; c < nc; c += kTrsvThreads / kTrsvNB)
-          acc = fma((double)M[(c0 + c) + (r0 + rr) * ld], (double)xs[c], acc);
+  }
+  if (threadIdx.x < kTrsvNB) {  // padding rows / columns of a partial block stay zero
+    for (int i = nr; i < kTrsvNB; ++i) dinv[i][threadIdx.x] = 0.0;
+    if (threadIdx.x >= nr)
+      for (int i = 0; i < kTrsvNB; ++i) dinv[i][threadIdx.x] = 0.0;
+  }
+  // non-TRANS: thread owns rows 2 lane, 2 lane + 1; warp owns the columns c = warp (mod NW)
+  // TRANS:     thread owns the columns c = lane (mod 32); warp owns rows warp + NW j
+  const int ra = 2 * lane, rb = 2 * lane + 1;
+  double a0 = 0.0, a1 = 0.0;
+  double at[kTrsvNB / NW];
+#pragma unroll
+  for (int j = 0; j < kTrsvNB / NW; ++j) at[j] = 0.0;
+  // blocks solved before the preceding one, in sweep order.  Per block, a warp reads the
+  // unknowns it needs as LL words in ONE batch (spinning only while that block is still
+  // being solved: no per-block handshake, no fence anywhere on the chain) and the matrix
+  // values of the NEXT block are loaded before the current block's unknowns are
+  // validated, so HBM latency overlaps the wait.
+  //   non-TRANS: warp w owns columns c0 + w + NW j (j < 8) of each block; lane j < 8 reads
+  //              unknown j and broadcasts it; the thread's rows are 2 lane, 2 lane + 1.
+  //   TRANS:     lane l owns columns c0 + l, c0 + l + 32; warp w owns rows w + NW j.
+  if (t > 1) {
+    auto block_col0 = [&](int64_t sidx) -> int64_t { return (LOWER ? sidx : nblk - 1 - sidx) * kTrsvNB; };
+    constexpr int CPW = kTrsvNB / NW;  // columns per warp per block (non-TRANS)
+    double mv[2 * CPW];
+    uint64_t xw0[2], xw1[2];
+    auto issue = [&](int64_t sidx) {
+      const int64_t c0 = block_col0(sidx);
+      const int nc = (int)min((int64_t)kTrsvNB, n - c0);
+      if (!TRANS) {
+#pragma unroll
+        for (int j = 0; j < CPW; ++j) {
+          const int c = warp + NW * j;
+          const T* col = M + (c0 + c) * ld + r0;
+          mv[2 * j] = (c < nc && ra < nr) ? (double)col[ra] : 0.0;
+          mv[2 * j + 1] = (c < nc && rb < nr) ? (double)col[rb] : 0.0;
+        }
+        const int c = warp + NW * (lane & (CPW - 1));
+        const uint64_t* p = ll + 2 * (c0 + min(c, nc - 1));
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(xw0[0]) : "l"(p) : "memory");
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(xw1[0]) : "l"(p + 1) : "memory");
       } else {
-        for (int c = cg; c < nc; c += kTrsvThreads / kTrsvNB)
-          acc = fma((double)M[(r0 + rr) + (c0 + c) * ld], (double)xs[c], acc);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = lane + 32 * h;
+#pragma unroll
+          for (int j = 0; j < CPW; ++j) {
+            const int r = warp + NW * j;
+            mv[h * CPW + j] = (c < nc && r < nr) ? (double)M[(c0 + c) + (r0 + r) * ld] : 0.0;
+          }
+          const uint64_t* p = ll + 2 * (c0 + min(c, nc - 1));
+          asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(xw0[h]) : "l"(p) : "memory");
+          asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(xw1[h]) : "l"(p + 1) : "memory");
+        }
+      }
+    };
+    auto validate = [&](int64_t sidx, int h) -> double {
+      // re-poll the LL words of my unknown until both carry the flag
+      const int64_t c0 = block_col0(sidx);
+      const int nc = (int)min((int64_t)kTrsvNB, n - c0);
+      const int c = TRANS ? lane + 32 * h : warp + NW * (lane & (CPW - 1));
+      const uint64_t* p = ll + 2 * (c0 + min(c, nc - 1));
+      while ((xw0[h] >> 32) != 1u)
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(xw0[h]) : "l"(p) : "memory");
+      if (sizeof(T) == 8) {
+        while ((xw1[h] >> 32) != 1u)
+          asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(xw1[h]) : "l"(p + 1) : "memory");
+        return __longlong_as_double((long long)((xw1[h] << 32) | (xw0[h] & 0xffffffffull)));
+      }
+      return (double)__uint_as_float((unsigned)(xw0[h] & 0xffffffffull));
+    };
+    issue(0);
+    for (int64_t sidx = 0; sidx + 1 < t; ++sidx) {
+      double cur[2 * CPW];
+#pragma unroll
+      for (int j = 0; j < 2 * CPW; ++j) cur[j] = mv[j];
+      uint64_t c0w0[2] = {xw0[0], xw0[1]}, c0w1[2] = {xw1[0], xw1[1]};
+      if (sidx + 2 < t) issue(sidx + 1);  // prefetch the next block
+      uint64_t nw0[2] = {xw0[0], xw0[1]}, nw1[2] = {xw1[0], xw1[1]};
+      xw0[0] = c0w0[0]; xw0[1] = c0w0[1]; xw1[0] = c0w1[0]; xw1[1] = c0w1[1];
+      if (!TRANS) {
+        const double xmine = validate(sidx, 0);
+#pragma unroll
+        for (int j = 0; j < CPW; ++j) {
+          const double xv = __shfl_sync(0xffffffffu, xmine, j);
+          a0 = fma(cur[2 * j], xv, a0);
+          a1 = fma(cur[2 * j + 1], xv, a1);
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double xv = validate(sidx, h);
+#pragma unroll
+          for (int j = 0; j < CPW; ++j) at[j] = fma(cur[h * CPW + j], xv, at[j]);
+        }
+      }
+      xw0[0] = nw0[0]; xw0[1] = nw0[1]; xw1[0] = nw1[0]; xw1[1] = nw1[1];
+    }
+  }
+  if (t > 0) {  // the preceding block: its unknowns arrive as LL words, then its staged tile
+    if (threadIdx.x < ncprev) xs[threadIdx.x] = trsv_ll_read<T>(ll + 2 * (cprev + threadIdx.x));
+    __syncthreads();
+    if (!TRANS) {
+      for (int c = warp; c < ncprev; c += NW) {
+        const double xv = (double)xs[c];
+        if (ra < nr) a0 = fma((double)pv[ra][c], xv, a0);
+        if (rb < nr) a1 = fma((double)pv[rb][c], xv, a1);
+      }
+    } else {
+      for (int c = lane; c < ncprev; c += 32) {
+        const double xv = (double)xs[c];
+#pragma unroll
+        for (int j = 0; j < kTrsvNB / NW; ++j) {
+          const int r = warp + NW * j;
+          if (r < nr) at[j] = fma((double)pv[r][c], xv, at[j]);
+        }
       }
     }
   }
-  if (t > 0) {  // the preceding block: wait, then its staged tile
-    if (threadIdx.x == 0) {
-      const int64_t bj = LOWER ? t - 1 : nblk - t;
-      while (((volatile int*)flags)[bj] == 0) __nanosleep(16);
-      __threadfence();
+  if (!TRANS) {
+    part[warp][ra] = a0;
+    part[warp][rb] = a1;
+  } else {
+#pragma unroll
+    for (int j = 0; j < kTrsvNB / NW; ++j) {
+      const double v = warp_sum(at[j]);
+      if (lane == 0) part[0][warp + NW * j] = v;
     }
-    __syncthreads();
-    if (threadIdx.x < ncprev) xs[threadIdx.x] = ((volatile T*)out)[cprev + threadIdx.x];
-    __syncthreads();
-    if (rr < nr)
-      for (int c = cg; c < ncprev; c += kTrsvThreads / kTrsvNB) acc = fma((double)pv[rr][c], (double)xs[c], acc);
   }
-  part[cg][rr] = acc;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    // off-diagonal sums of my two rows, then the column sweep of the diagonal block
-    double off0 = 0.0, off1 = 0.0;
-    for (int q = 0; q < kTrsvThreads / kTrsvNB; ++q) {
-      off0 += part[q][lane];
-      off1 += part[q][lane + 32];
-    }
-    const T b0 = lane < nr ? rhs[r0 + lane] : T(0);
-    const T b1 = lane + 32 < nr ? rhs[r0 + lane + 32] : T(0);
-    T y0 = T(0), y1 = T(0);
-    for (int step = 0; step < nr; ++step) {
-      const int c = LOWER ? step : nr - 1 - step;
-      const bool mine1 = c >= 32;
-      const int owner = c & 31;
-      T v = T(0);
-      if (lane == owner) {
-        const double off = mine1 ? off1 : off0;
-        v = sub_rn(mine1 ? b1 : b0, (T)off);  // y[i] -= L[i,:i] @ y[:i] / x[i] -= U[i,i+1:] @ x[i+1:]
-        if (!UNIT) v = div_rn(v, dg[c][c]);   // x[i] /= U[i,i]
-        if (mine1) y1 = v; else y0 = v;
-      }
-      v = __shfl_sync(0xffffffffu, v, owner);
-      // fold the new unknown into the rows still to be solved
-      const int ra = lane, rb = lane + 32;
-      if (LOWER ? (ra > c && ra < nr) : (ra < c)) off0 = fma((double)dg[ra][c], (double)v, off0);
-      if (LOWER ? (rb > c && rb < nr) : (rb < c)) off1 = fma((double)dg[rb][c], (double)v, off1);
-    }
-    if (lane < nr) out[r0 + lane] = y0;
-    if (lane + 32 < nr) out[r0 + lane + 32] = y1;
+  // r = b - (off-diagonal sums) in fp64, then y = D^-1 r with the inverse computed before
+  // any wait: the chain step is one 64 x 64 product from shared memory
+  if (threadIdx.x < kTrsvNB) {
+    double off = 0.0;
+    for (int q = 0; q < (TRANS ? 1 : NW); ++q) off += part[q][threadIdx.x];
+    rv[threadIdx.x] = threadIdx.x < nr ? (double)bme - off : 0.0;
   }
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) atomicExch(flags + bi, 1);
+  {
+    const int i = threadIdx.x % kTrsvNB, g = threadIdx.x / kTrsvNB;
+    constexpr int KG = kTrsvNB / (kTrsvThreads / kTrsvNB);
+    double p = 0.0;
+#pragma unroll
+    for (int k = g * KG; k < (g + 1) * KG; ++k) p = fma(dinv[i][k], rv[k], p);
+    part[g][i] = p;
+  }
+  __syncthreads();
+  if (threadIdx.x < nr) {
+    const int i = threadIdx.x;
+    double y = part[0][i];
+    for (int g = 1; g < kTrsvThreads / kTrsvNB; ++g) y += part[g][i];
+    const T yt = (T)y;
+    // the next block's critical path reads these LL words (no fence, no counter round trip)
+    trsv_ll_write<T>(ll + 2 * (r0 + i), yt);
+    out[r0 + i] = yt;
+  }
 }
 
 template <typename T>
-static int trsv_smem_bytes() {
-  return (int)(2 * kTrsvNB * (kTrsvNB + 1) * sizeof(T));
+static int trsv_smem_bytes() {  // diagonal tile + previous block's tile (T) + D^-1 (fp64)
+  return (int)(2 * kTrsvNB * (kTrsvNB + 1) * sizeof(T) + kTrsvNB * (kTrsvNB + 1) * sizeof(double));
 }
 
 // zero-diagonal scan: first offending row in the reference's sweep order
@@ -1696,12 +1848,13 @@ int trsv_upper_trans_launch(ds_ctx* ctx, int64_t n, const T* M, int64_t ld, cons
   if (n == 0) return DS_OK;
   const int64_t nblk = ceil_div(n, kTrsvNB);
   int* ticket = (int*)scratch;
-  int* flags = ticket + 64;
-  DS_CUDA(cudaMemsetAsync(scratch, 0, (64 + nblk) * sizeof(int), ctx->stream));
+  int* flags = (int*)(scratch + 256);  // the `done` counter
+  uint64_t* ll = (uint64_t*)(scratch + 512);
+  DS_CUDA(cudaMemsetAsync(scratch, 0, trsv_scratch_bytes(n), ctx->stream));
   const int sm = trsv_smem_bytes<T>();
   DS_CUDA(cudaFuncSetAttribute(trsv_kernel<T, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
   trsv_kernel<T, false, false, true><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(
-      n, M, ld, rhs, out, flags, ticket);
+      n, M, ld, rhs, out, flags, ticket, ll);
   count_launch(ctx);
   DS_CHECK_LAUNCH();
   return DS_OK;
@@ -1717,18 +1870,19 @@ int trsv_launch(ds_ctx* ctx, int64_t n, const T* M, int64_t ld, const T* rhs, T*
   if (n == 0) return DS_OK;
   const int64_t nblk = ceil_div(n, kTrsvNB);
   int* ticket = (int*)scratch;
-  int* flags = ticket + 64;
-  DS_CUDA(cudaMemsetAsync(scratch, 0, (64 + nblk) * sizeof(int), ctx->stream));
+  int* flags = (int*)(scratch + 256);  // the `done` counter
+  uint64_t* ll = (uint64_t*)(scratch + 512);
+  DS_CUDA(cudaMemsetAsync(scratch, 0, trsv_scratch_bytes(n), ctx->stream));
   const int sm = trsv_smem_bytes<T>();
   if (lower && unit) {
     DS_CUDA(cudaFuncSetAttribute(trsv_kernel<T, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    trsv_kernel<T, true, true><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(n, M, ld, rhs, out, flags, ticket);
+    trsv_kernel<T, true, true><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(n, M, ld, rhs, out, flags, ticket, ll);
   } else if (lower) {
     DS_CUDA(cudaFuncSetAttribute(trsv_kernel<T, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    trsv_kernel<T, true, false><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(n, M, ld, rhs, out, flags, ticket);
+    trsv_kernel<T, true, false><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(n, M, ld, rhs, out, flags, ticket, ll);
   } else {
     DS_CUDA(cudaFuncSetAttribute(trsv_kernel<T, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    trsv_kernel<T, false, false><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(n, M, ld, rhs, out, flags, ticket);
+    trsv_kernel<T, false, false><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(n, M, ld, rhs, out, flags, ticket, ll);
   }
   count_launch(ctx);
   DS_CHECK_LAUNCH();
@@ -1760,13 +1914,13 @@ int diag_check(ds_ctx* ctx, int64_t n, const T* M, int64_t ld, bool lower, int64
 template <typename T>
 int lu_solve_impl(ds_ctx* ctx, int64_t n, const T* LU, int64_t ld, const int* h_idx, const T* b, T* x) {
   void* ws = nullptr;
-  const size_t need = (size_t)n * (sizeof(int) + sizeof(T) * 2) + (size_t)(ceil_div(n, 64) + 64) * 4 + 8 * 256;
+  const size_t need = (size_t)n * (sizeof(int) + sizeof(T) * 2) + trsv_scratch_bytes(n) + 8 * 256;
   DS_TRY(ctx_workspace(ctx, need, &ws));
   Carver cv{(char*)ws};
   int* idx = cv.take<int>((size_t)n * sizeof(int));
   T* pb = cv.take<T>((size_t)n * sizeof(T));
   T* y = cv.take<T>((size_t)n * sizeof(T));
-  char* scratch = cv.take<char>((size_t)(ceil_div(n, 64) + 64) * 4);
+  char* scratch = cv.take<char>(trsv_scratch_bytes(n));
   DS_CUDA(cudaMemcpyAsync(idx, h_idx, (size_t)n * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
   gather_kernel<T><<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 1024), 256, 0, ctx->stream>>>(
       n, idx, b, pb);
@@ -1885,7 +2039,7 @@ int ds_forward_substitution(ds_ctx* ctx, int dtype, int64_t n, const void* L, in
   if (h_bad_row) *h_bad_row = -1;
   if (n == 0) return DS_OK;
   void* ws = nullptr;
-  DS_TRY(ctx_workspace(ctx, (size_t)(ceil_div(n, 64) + 128) * 4 + 512, &ws));
+  DS_TRY(ctx_workspace(ctx, trsv_scratch_bytes(n) + 512, &ws));
   if (!unit_diagonal) {
     int64_t bad = -1;
     DS_DISPATCH(dtype, T, DS_TRY(diag_check<T>(ctx, n, (const T*)L, ldl, true, &bad, (char*)ws)));
@@ -1908,7 +2062,7 @@ int ds_backward_substitution(ds_ctx* ctx, int dtype, int64_t n, const void* U, i
   if (h_bad_row) *h_bad_row = -1;
   if (n == 0) return DS_OK;
   void* ws = nullptr;
-  DS_TRY(ctx_workspace(ctx, (size_t)(ceil_div(n, 64) + 128) * 4 + 512, &ws));
+  DS_TRY(ctx_workspace(ctx, trsv_scratch_bytes(n) + 512, &ws));
   int64_t bad = -1;
   DS_DISPATCH(dtype, T, DS_TRY(diag_check<T>(ctx, n, (const T*)U, ldu, false, &bad, (char*)ws)));
   if (bad >= 0) {
