@@ -23,6 +23,10 @@
 #include <ctime>
 #include <vector>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "ds_common.cuh"
 #include "ds_kernels.cuh"
 
@@ -212,6 +216,27 @@ __device__ __forceinline__ void cta_argmax_key(unsigned long long& key, int64_t&
 // into the shared-memory array Ls (the final L / U values of columns < c) and the
 // row shifts by one.  Per column every CTA publishes, as LL words, its local
 // candidate header (|v|, row; one 128-byte line per CTA) and the candidate row
+
+// Forward-progress watchdog of the panel kernels' LL spin loops.  The exchange needs every
+// CTA of the panel grid resident at once; the host asserts that with the occupancy
+// calculator before each plain launch (panel_launch) and otherwise takes the cooperative
+// kernel.  Should residency still fail (another context, MPS partitioning), a poll would
+// spin forever: after 10 s of wall time (%globaltimer) the kernel traps instead, which the
+// host sees as a CUDA error (DS_ECUDA -> RuntimeError), not a hung device.
+struct SpinGuard {
+  unsigned n = 0;
+  unsigned long long t0 = 0;
+  __device__ __forceinline__ void tick() {
+    if ((++n & 4095u) == 0) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (t0 == 0)
+        t0 = now;
+      else if (now - t0 > 10000000000ull)
+        __trap();
+    }
+  }
+};
 // (written by the owning thread); the owner of row i publishes row i.  Every CTA
 // polls the G headers (the only grid-wide synchronisation), reduces them in a
 // fixed order (the same first-max pivot everywhere), polls the winner's row and
@@ -314,10 +339,12 @@ __global__ void __launch_bounds__(kPanelRegThreads, 1) lu_panel_smem_kernel(T* _
     for (int b = t; G > 1 && b < (int)G; b += nt) {
       const uint64_t* h = hdr + ((size_t)par * G + b) * kHdrWords;
       uint64_t x0, x1, x2;
+      SpinGuard sg;
       do {
         x0 = ll_load(h);
         x1 = ll_load(h + 1);
         x2 = ll_load(h + 2);
+        sg.tick();
       } while (!(ll_ok(x0, ep) && ll_ok(x1, ep) && ll_ok(x2, ep)));
       const unsigned long long k2 = (x0 & 0xffffffffull) | (x1 << 32);
       const int64_t i2 = (uint32_t)x2 == 0xffffffffu ? INT64_MAX : (int64_t)(uint32_t)x2;
@@ -353,7 +380,9 @@ __global__ void __launch_bounds__(kPanelRegThreads, 1) lu_panel_smem_kernel(T* _
           }
         } else if (j < ncol) {
           uint64_t pw[VW], dw[VW];
+          SpinGuard sg;
           while (true) {
+            sg.tick();
             bool ok = true;
 #pragma unroll
             for (int qq = 0; qq < VW; ++qq) {
@@ -568,7 +597,9 @@ __global__ void __launch_bounds__(kPanelWarpThreads, 1) lu_panel_warp_kernel(T* 
 #pragma unroll
         for (int s2 = 0; s2 < kHdrPerLane; ++s2)
           if (lane + 32 * s2 < (int)G) pending |= 1u << s2;
+        SpinGuard sg;
         while (pending) {
+          sg.tick();
 #pragma unroll
           for (int s2 = 0; s2 < kHdrPerLane; ++s2)
             if (pending >> s2 & 1u) {
@@ -613,7 +644,9 @@ __global__ void __launch_bounds__(kPanelWarpThreads, 1) lu_panel_warp_kernel(T* 
       {
         uint64_t pw[2][VW], dw[2][VW];
         unsigned pending = (lane < ncol ? 1u : 0u) | (lane + 32 < ncol ? 2u : 0u);
+        SpinGuard sg;
         while (pending) {
+          sg.tick();
 #pragma unroll
           for (int s2 = 0; s2 < 2; ++s2)
             if (pending >> s2 & 1u) {
@@ -1149,6 +1182,32 @@ size_t panel_scratch_bytes(int64_t b) {
          sizeof(uint64_t) * 2 * 1024 * kPanelMaxW * 2 + sizeof(uint64_t) * 2 * kPanelMaxW * 2 + 16 * 256;
 }
 
+// Can all g CTAs of a panel kernel be resident at once (the LL exchange's forward-progress
+// condition)?  Occupancy per (kernel, block, smem) is cached; the kernel attributes are set
+// first so the query sees the opted-in shared memory.
+static bool panel_fits_resident(ds_ctx* ctx, void* kfn, int nthr, size_t smem, size_t smem_cap, int64_t g,
+                                bool f64) {
+  static std::mutex mu;
+  static std::map<std::tuple<void*, int, size_t>, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(kfn, nthr, smem);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    (void)f64;
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, nthr, smem) != cudaSuccess) {
+      cudaGetLastError();
+      per_sm = 0;
+    }
+    it = cache.emplace(key, per_sm).first;
+  }
+  return (int64_t)it->second * ctx->num_sms >= g;
+}
+
 template <typename T>
 int panel_launch(ds_ctx* ctx, T* W, int64_t n, int64_t ld, int64_t kb, int64_t bf, int64_t* piv,
                  int8_t* zero_cols, char* scratch) {
@@ -1206,7 +1265,13 @@ int panel_launch(ds_ctx* ctx, T* W, int64_t n, int64_t ld, int64_t kb, int64_t b
     const int ldt = (int)(per | 1);
     const size_t smem = (size_t)ncol * ldt * sizeof(T);
     const int tpr = warp_k ? 1 : per <= kPanelRegThreads / 4 ? 4 : 2;
-    if (smem <= smem_cap && per * tpr <= kPanelRegThreads) {
+    const int nthr_pre = warp_k ? (int)(32 + ceil_div(per, 32) * 32)
+                                : (int)std::max<int64_t>(ceil_div(per * tpr, 32) * 32, ceil_div(g, 32) * 32);
+    void* kfn_pre = warp_k     ? (void*)lu_panel_warp_kernel<T>
+                    : tpr == 4 ? (void*)lu_panel_smem_kernel<T, 4>
+                               : (void*)lu_panel_smem_kernel<T, 2>;
+    if (smem <= smem_cap && per * tpr <= kPanelRegThreads &&
+        panel_fits_resident(ctx, kfn_pre, nthr_pre, smem, smem_cap, g, sizeof(T) == 8)) {
       a.per = (int)per;
       a.ldt = ldt;
       static bool attr_set[2] = {false, false};
@@ -1550,16 +1615,19 @@ constexpr int kTrsvThreads = 256;
 // TRANS (upper only): solve with U = M^T, i.e. U[i,j] = M[j + i*ld] (the
 // backward sweep of cholesky_solve on L^T, direct.py:166-171, without forming L^T).
 //
-// Blocks finish strictly in sweep order (block t waits for block t-1), so ONE
-// monotonic counter `done` (= blocks solved) replaces per-block flags: a CTA reads it
-// once and folds in every solved block up to it as one flat, deep-unrolled stream over
-// columns (no per-tile handshake).  Critical path per block = the counter reaching
-// t, the tile of block t-1 (staged in shared memory before the wait, like the
-// diagonal tile), the diagonal solve from shared memory, publish.  The diagonal solve
-// runs column by column in one warp (lane l owns rows l and l + 32; the new unknown is
-// broadcast with a shuffle and folded into the rows still to solve).
-// Summation order is fixed (each column always goes to the same warp / lane, visited in
-// sweep order), so results are bitwise reproducible run to run.
+// One CTA per 64-row block, blocks taken in sweep order from an atomic ticket (a CTA
+// only ever waits on blocks with smaller tickets, which are resident or done).
+//   * Unknowns are published as LL words (32 data bits + flag per 8-byte word, the
+//     buffer zeroed per launch): a reader polls the words themselves, so no fence and
+//     no counter round trip sits on the chain.
+//   * Before any wait a CTA stages its diagonal tile and the tile of the preceding
+//     block in shared memory, and inverts the diagonal tile in fp64 (one thread per
+//     column).  Then it folds in all earlier blocks (batched LL reads per block, next
+//     block's matrix values prefetched), the preceding block from shared memory as soon
+//     as its unknowns appear, and finishes with y = D^-1 (b - sums): one 64 x 64 product.
+//   * Summation order is fixed (each column always goes to the same warp / lane, in
+//     sweep order): results are bitwise reproducible run to run.  They differ from the
+//     reference's row-by-row substitution (direct.py:123-152) by rounding only.
 template <typename T, bool TRANS>
 __device__ __forceinline__ void trsv_stage_tile(T (*tile)[kTrsvNB + 1], const T* __restrict__ M, int64_t ld,
                                                 int64_t r0, int nr, int64_t c0, int nc) {
@@ -1598,16 +1666,11 @@ __device__ __forceinline__ T trsv_ll_read(const uint64_t* p) {
   return (T)__uint_as_float((unsigned)(w0 & 0xffffffffull));
 }
 
-__device__ __forceinline__ int ld_acquire_s32(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
 template <typename T, bool LOWER, bool UNIT, bool TRANS = false>
 __global__ void __launch_bounds__(kTrsvThreads)
     trsv_kernel(int64_t n, const T* __restrict__ M, int64_t ld, const T* __restrict__ rhs,
-                T* out, int* done, int* ticket, uint64_t* __restrict__ ll) {
+                T* out, int* ticket, uint64_t* __restrict__ ll) {
   extern __shared__ __align__(16) unsigned char trsv_smem[];
   T (*dg)[kTrsvNB + 1] = reinterpret_cast<T (*)[kTrsvNB + 1]>(trsv_smem);
   T (*pv)[kTrsvNB + 1] = dg + kTrsvNB;  // tile of the previous block in the sweep
@@ -1848,13 +1911,12 @@ int trsv_upper_trans_launch(ds_ctx* ctx, int64_t n, const T* M, int64_t ld, cons
   if (n == 0) return DS_OK;
   const int64_t nblk = ceil_div(n, kTrsvNB);
   int* ticket = (int*)scratch;
-  int* flags = (int*)(scratch + 256);  // the `done` counter
   uint64_t* ll = (uint64_t*)(scratch + 512);
   DS_CUDA(cudaMemsetAsync(scratch, 0, trsv_scratch_bytes(n), ctx->stream));
   const int sm = trsv_smem_bytes<T>();
   DS_CUDA(cudaFuncSetAttribute(trsv_kernel<T, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
   trsv_kernel<T, false, false, true><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(
-      n, M, ld, rhs, out, flags, ticket, ll);
+      n, M, ld, rhs, out, ticket, ll);
   count_launch(ctx);
   DS_CHECK_LAUNCH();
   return DS_OK;
@@ -1870,19 +1932,18 @@ int trsv_launch(ds_ctx* ctx, int64_t n, const T* M, int64_t ld, const T* rhs, T*
   if (n == 0) return DS_OK;
   const int64_t nblk = ceil_div(n, kTrsvNB);
   int* ticket = (int*)scratch;
-  int* flags = (int*)(scratch + 256);  // the `done` counter
   uint64_t* ll = (uint64_t*)(scratch + 512);
   DS_CUDA(cudaMemsetAsync(scratch, 0, trsv_scratch_bytes(n), ctx->stream));
   const int sm = trsv_smem_bytes<T>();
   if (lower && unit) {
     DS_CUDA(cudaFuncSetAttribute(trsv_kernel<T, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    trsv_kernel<T, true, true><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(n, M, ld, rhs, out, flags, ticket, ll);
+    trsv_kernel<T, true, true><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(n, M, ld, rhs, out, ticket, ll);
   } else if (lower) {
     DS_CUDA(cudaFuncSetAttribute(trsv_kernel<T, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    trsv_kernel<T, true, false><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(n, M, ld, rhs, out, flags, ticket, ll);
+    trsv_kernel<T, true, false><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(n, M, ld, rhs, out, ticket, ll);
   } else {
     DS_CUDA(cudaFuncSetAttribute(trsv_kernel<T, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-    trsv_kernel<T, false, false><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(n, M, ld, rhs, out, flags, ticket, ll);
+    trsv_kernel<T, false, false><<<(unsigned)nblk, kTrsvThreads, sm, ctx->stream>>>(n, M, ld, rhs, out, ticket, ll);
   }
   count_launch(ctx);
   DS_CHECK_LAUNCH();

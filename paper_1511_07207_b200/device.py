@@ -23,6 +23,16 @@ from . import _lib, core
 LD_ALIGN = 4
 
 
+def _release_device(lib, handle, ptr, inflight):
+    """Finalizer of a DeviceArray: the context stream first waits for a still pending
+    asynchronous upload into the buffer (copy stream), then frees it stream-ordered."""
+    if inflight[0] is not None:
+        lib.ds_wait_event(handle, inflight[0])
+        lib.ds_event_destroy(inflight[0])
+        inflight[0] = inflight[1] = None
+    lib.ds_free(handle, c_void_p(ptr))
+
+
 def _padded_ld(rows: int) -> int:
     return max(LD_ALIGN, (rows + LD_ALIGN - 1) // LD_ALIGN * LD_ALIGN)
 
@@ -30,7 +40,7 @@ def _padded_ld(rows: int) -> int:
 class DeviceArray:
     """A 1-d vector or 2-d column-major matrix in device memory."""
 
-    __slots__ = ("ctx", "shape", "dtype", "ld", "ptr", "_fin", "_pending", "_src", "__weakref__")
+    __slots__ = ("ctx", "shape", "dtype", "ld", "ptr", "_fin", "_inflight", "__weakref__")
 
     def __init__(self, ctx: _lib.Context, shape, dtype, ld: int | None = None):
         self.ctx = ctx
@@ -48,9 +58,10 @@ class DeviceArray:
         p = c_void_p()
         _lib.check(ctx.lib.ds_malloc(ctx.handle, max(nbytes, 16), ctypes.byref(p)))
         self.ptr = p.value
-        self._pending = None  # event of an in-flight asynchronous upload (upload_async)
-        self._src = None      # the host array it reads (kept alive until consumed)
-        self._fin = weakref.finalize(self, ctx.lib.ds_free, ctx.handle, c_void_p(self.ptr))
+        # [event, host array] of an in-flight asynchronous upload (upload_async); shared with
+        # the finalizer so a handle dropped before its copy finished is freed only after it
+        self._inflight = [None, None]
+        self._fin = weakref.finalize(self, _release_device, ctx.lib, ctx.handle, self.ptr, self._inflight)
 
     # -- numpy-like metadata used by the validators -------------------------------------
     @property
@@ -132,15 +143,15 @@ class DeviceArray:
         _lib.check(self.ctx.lib.ds_upload_async(self.ctx.handle, self.dcode, a.ctypes.data_as(c_void_p), rows, cols,
                                                 max(rows, 1), c_void_p(self.ptr), self.ld if self.ndim == 2
                                                 else max(rows, 1), ctypes.byref(ev)))
-        self._pending, self._src = ev, a
+        self._inflight[0], self._inflight[1] = ev, a
         return self
 
     def settle(self):
         """Order the context stream after a pending asynchronous upload into this array."""
-        if self._pending is not None:
-            _lib.check(self.ctx.lib.ds_wait_event(self.ctx.handle, self._pending))
-            self.ctx.lib.ds_event_destroy(self._pending)
-            self._pending, self._src = None, None
+        if self._inflight[0] is not None:
+            _lib.check(self.ctx.lib.ds_wait_event(self.ctx.handle, self._inflight[0]))
+            self.ctx.lib.ds_event_destroy(self._inflight[0])
+            self._inflight[0] = self._inflight[1] = None
 
     def to_host(self, out: np.ndarray | None = None) -> np.ndarray:
         self.settle()
@@ -186,29 +197,26 @@ def is_device(a) -> bool:
 
 # ---- pinned host memory (for end-to-end transfers at full PCIe rate) ---------------------
 class _PinnedOwner:
-    def __init__(self, ptr, lib):
+    """Owns a page-locked allocation and exposes it through the array interface, so every
+    NumPy array or view made from it keeps it (and the allocation) alive."""
+
+    def __init__(self, ptr, nbytes, lib):
         self.ptr = ptr
+        self.__array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3}
         self._fin = weakref.finalize(self, lib.ds_host_free, c_void_p(ptr))
 
 
 def pinned_empty(shape, dtype, order="F") -> np.ndarray:
-    """A NumPy array backed by page-locked host memory."""
+    """A NumPy array backed by page-locked host memory (freed when the last array or view
+    that refers to it goes away)."""
     lib = _lib.load_library()
     dt = np.dtype(dtype)
-    nbytes = int(np.prod(shape)) * dt.itemsize
+    count = int(np.prod(shape))
+    nbytes = max(count * dt.itemsize, 16)
     p = c_void_p()
-    _lib.check(lib.ds_host_alloc(max(nbytes, 16), ctypes.byref(p)))
-    owner = _PinnedOwner(p.value, lib)
-    buf = (ctypes.c_char * max(nbytes, 16)).from_address(p.value)
-    arr = np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape, order=order)
-    # keep the owner alive with the array
-    arr_base = arr
-    _pinned_keepalive[id(arr_base)] = owner
-    weakref.finalize(arr_base, _pinned_keepalive.pop, id(arr_base), None)
-    return arr
-
-
-_pinned_keepalive: dict = {}
+    _lib.check(lib.ds_host_alloc(nbytes, ctypes.byref(p)))
+    raw = np.asarray(_PinnedOwner(p.value, nbytes, lib))  # base chain ends at the owner
+    return raw[: count * dt.itemsize].view(dt).reshape(shape, order=order)
 
 
 def relative_residual_device(A, x, b) -> float:

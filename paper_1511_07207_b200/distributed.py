@@ -266,9 +266,11 @@ def _symmetry_gate(A_blk, n, n_loc, comm, ops, dtype):
     G = comm.size
     N = G * n_loc
     # send buffer: for each destination r, our block rows(q) x cols(r), column-major.  The
-    # row block is stored (N, n_loc) with zero rows past n, so those G blocks are already
-    # contiguous: a view, no copy of the local matrix; one rank compares A with itself
-    if A_blk.is_contiguous() and A_blk.shape[0] == N:
+    # row block is stored as a torch (n, n_loc) tensor (column-major n_loc x n, ld n_loc);
+    # when n == N (n divisible by G) its G column groups are already contiguous blocks: a
+    # view, no copy of the local matrix.  Otherwise (or for any other shape) the blocks are
+    # copied into a zeroed buffer, so padding never enters the comparison.
+    if A_blk.is_contiguous() and tuple(A_blk.shape) == (n, n_loc) and n == N:
         send = A_blk.view(G, n_loc, n_loc)
     else:
         send = torch.zeros((G, n_loc, n_loc), dtype=A_blk.dtype, device=A_blk.device)

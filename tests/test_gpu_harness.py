@@ -69,3 +69,21 @@ def test_cli_solve_and_bench(tmp_path, capsys):
     assert len(parse_report_csv(out.read_text())) == 4
     mtx = os.path.join(HERE, "golden", "mtx", "coord_diag.mtx")
     assert cli.main(["solve", "--method", "lu", "--matrix", mtx]) == 0
+
+
+def test_sweep_against_the_reference_backend():
+    """b200 beside the unmodified reference's CPU backend in one sweep (baseline/_ref): the
+    speedup column is relative to the first backend, and both solve the same system."""
+    import sys
+    ref = os.path.join(os.path.dirname(HERE), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "densolve")):
+        pytest.skip("baseline/_ref not installed")
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    recs = run_benchmark(["cg", "lu-blocked"], [512], ["f64"], ["reference", "b200"],
+                         SolverConfig(tolerance=1e-8), repeats=1)
+    assert [(r.method, r.backend) for r in recs] == [("cg", "reference"), ("cg", "b200"),
+                                                     ("lu-blocked", "reference"), ("lu-blocked", "b200")]
+    assert all(r.converged for r in recs)
+    assert recs[0].iterations == recs[1].iterations
+    assert recs[0].speedup_vs_reference == 1.0 and recs[1].speedup_vs_reference > 1.0

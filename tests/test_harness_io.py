@@ -63,8 +63,9 @@ def test_csv_round_trip():
 
 def test_markdown_grid():
     md = emit_report(_recs(), "markdown")
-    assert "### Iterative methods, f64" in md and "| Matrix dimension | cg | gmres |" in md
-    assert "### Direct methods, f32" in md
+    assert "### f64: speedup vs b200" in md and "| Matrix dimension | cg | gmres |" in md
+    assert "| 256 | 1.00x (10 ms) | - |" in md
+    assert "### f32: speedup vs b200" in md and "| 256 | - |" in md  # the NaN (failed) point
 
 
 def test_report_errors():
