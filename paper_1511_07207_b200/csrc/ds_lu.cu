@@ -1194,10 +1194,7 @@ static bool panel_fits_resident(ds_ctx* ctx, void* kfn, int nthr, size_t smem, s
   auto it = cache.find(key);
   if (it == cache.end()) {
     (void)f64;
-    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
+    (void)smem_cap;
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, nthr, smem) != cudaSuccess) {
       cudaGetLastError();
@@ -1270,21 +1267,21 @@ int panel_launch(ds_ctx* ctx, T* W, int64_t n, int64_t ld, int64_t kb, int64_t b
     void* kfn_pre = warp_k     ? (void*)lu_panel_warp_kernel<T>
                     : tpr == 4 ? (void*)lu_panel_smem_kernel<T, 4>
                                : (void*)lu_panel_smem_kernel<T, 2>;
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[sizeof(T) == 8 ? 1 : 0]) {
+      DS_CUDA(cudaFuncSetAttribute(lu_panel_smem_kernel<T, 2>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
+      DS_CUDA(cudaFuncSetAttribute(lu_panel_smem_kernel<T, 4>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
+      // <= 256 rows x 64 columns of retired values (131.6 KB) beside ~26 KB of static buffers
+      DS_CUDA(cudaFuncSetAttribute(lu_panel_warp_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)std::min<size_t>(smem_cap, 160 * 1024)));
+      attr_set[sizeof(T) == 8 ? 1 : 0] = true;
+    }
     if (smem <= smem_cap && per * tpr <= kPanelRegThreads &&
         panel_fits_resident(ctx, kfn_pre, nthr_pre, smem, smem_cap, g, sizeof(T) == 8)) {
       a.per = (int)per;
       a.ldt = ldt;
-      static bool attr_set[2] = {false, false};
-      if (!attr_set[sizeof(T) == 8 ? 1 : 0]) {
-        DS_CUDA(cudaFuncSetAttribute(lu_panel_smem_kernel<T, 2>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
-        DS_CUDA(cudaFuncSetAttribute(lu_panel_smem_kernel<T, 4>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap));
-        // <= 256 rows x 64 columns of retired values (131.6 KB) beside ~26 KB of static buffers
-        DS_CUDA(cudaFuncSetAttribute(lu_panel_warp_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)std::min<size_t>(smem_cap, 160 * 1024)));
-        attr_set[sizeof(T) == 8 ? 1 : 0] = true;
-      }
       const int nthr = warp_k ? (int)(32 + ceil_div(per, 32) * 32)
                              : (int)std::max<int64_t>(ceil_div(per * tpr, 32) * 32, ceil_div(g, 32) * 32);
       void* kfn = warp_k     ? (void*)lu_panel_warp_kernel<T>
