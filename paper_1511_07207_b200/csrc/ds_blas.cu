@@ -101,8 +101,31 @@ __global__ void __launch_bounds__(kGemvThreads)
   T* xs = reinterpret_cast<T*>(smem_raw);
   const int64_t c0 = (int64_t)blockIdx.y * chunk;
   const int64_t cn = min(chunk, n - c0);
-  for (int64_t j = threadIdx.x; j < cn; j += blockDim.x) xs[j] = x[c0 + j];
-  __syncthreads();
+  // the x chunk is staged by the bulk-copy engine (cp.async.bulk, the 1-D TMA path) into
+  // shared memory, completing on an mbarrier; unaligned / ragged chunks use plain loads
+  const unsigned xbytes = (unsigned)(cn * (int64_t)sizeof(T));
+  if (((reinterpret_cast<uintptr_t>(x + c0) | xbytes) & 15u) == 0 && xbytes > 0) {
+    __shared__ __align__(8) uint64_t xbar;
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(&xbar);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(xbytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+              (unsigned)__cvta_generic_to_shared(xs)),
+          "l"(x + c0), "r"(xbytes), "r"(bar)
+          : "memory");
+    }
+    __syncthreads();  // the barrier is initialised before anyone polls it
+    asm volatile(
+        "{\n .reg .pred P1;\n XW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n @!P1 bra XW_%=;\n}\n" ::"r"(
+            bar)
+        : "memory");
+  } else {
+    for (int64_t j = threadIdx.x; j < cn; j += blockDim.x) xs[j] = x[c0 + j];
+    __syncthreads();
+  }
   using V = typename VecT<T, VEC>::type;
   const int64_t r0 = (int64_t)blockIdx.x * (kGemvThreads * VEC) + (int64_t)threadIdx.x * VEC;
   if (r0 >= m) return;
