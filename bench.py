@@ -299,13 +299,9 @@ def run_b200(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     sharded = ws > 1 or args.force_sharded
-    if sharded:
+    if ws > 1:
         import torch.distributed as dist
         if not dist.is_initialized():
-            # --force-sharded without torchrun: a world of one on 127.0.0.1
-            for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("LOCAL_RANK", "0"),
-                         ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29531")):
-                os.environ.setdefault(k, v)
             dist.init_process_group("nccl", device_id=dev)
     from paper_1511_07207_b200 import SolverConfig, cg_solve, get_backend, pinned_empty
     from paper_1511_07207_b200.device import DeviceArray
@@ -322,7 +318,7 @@ def run_b200(args):
 
     if sharded:
         try:
-            return bench_sharded_cg(args, torch, dev, be)
+            return bench_sharded_cg(args, torch, dev, local)
         finally:
             import torch.distributed as dist
             if dist.is_initialized():
@@ -678,100 +674,137 @@ def bench_lu(args, torch, stream, be, n, lu_fit, hbm_peak):
 
 
 # ---------------------------------------------------------------------------- N > 1 (torchrun)
-def bench_sharded_cg(args, torch, dev, be):
-    """`bench.py --gpus N` under torchrun: C4 CG row-sharded over N GPUs (strong scaling).
-    Same JSON contract as the 1-GPU line: device-resident `value` (max over ranks of the
-    CUDA-event time), `e2e` (each rank uploads its row block of A, b, x0 from pinned host
-    memory and downloads its x shard every step), the per-rank GEMV `roofline`, clocks."""
+def bench_sharded_cg(args, torch, dev, local):
+    """C4 CG row-sharded through the public API: `get_backend("b200", distributed=True)` under
+    torchrun (one process per GPU, exchange regions mapped through CUDA IPC), or
+    `get_backend("b200", devices=[0])` for `--force-sharded` at N=1.  The whole iteration
+    loop runs in the library (ds_cg_sharded: the all-gathers of p and of the reduction
+    records are fused into the producing kernels over peer memory).  Same JSON contract as
+    the 1-GPU line: device-resident `value` (max over ranks of the CUDA-event time), `e2e`
+    (each rank uploads its row block of A, b, x0 from pinned host memory and gathers the
+    whole x every step), the per-rank GEMV `roofline`, clocks."""
     import json
     import torch.distributed as dist
 
-    from paper_1511_07207_b200.core import SolverConfig
-    from paper_1511_07207_b200.distributed import CudaShardOps, TorchComm, cg_solve_sharded, row_partition
+    from paper_1511_07207_b200 import SolverConfig, cg_solve, get_backend, pinned_empty
+    from paper_1511_07207_b200.device import DeviceArray, _padded_ld
     from paper_1511_07207_b200.harness import generate_problem_device
+    from paper_1511_07207_b200.sharded import ShardedMatrix, ShardedVector
 
-    comm = TorchComm()
-    ops = CudaShardOps(be.ctx)
-    ops.bind_current_stream()
-    stream = torch.cuda.current_stream()
+    multi = dist.is_initialized()
+    be = get_backend("b200", distributed=True, device=local) if multi else get_backend("b200", devices=[local])
+    G, q = be.nshards, be.local_ranks[0]
+    sctx = be.shard_contexts[0]
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
+    sctx.set_stream(stream.cuda_stream)  # the shard's library work on this stream: the events see it
     n, iters = args.n, args.iters
-    G, q = comm.size, comm.rank
-    n_loc, N = row_partition(n, G)
-    r0, r1 = q * n_loc, min(n, (q + 1) * n_loc)
+    ss = be.shardset(n, np.float64)
+    r0, r1 = ss.rows(q)
+    n_loc = ss.n_loc
     # every rank generates the full C4 matrix (the reference spd recipe, same bytes as the
-    # 1-GPU arm) and keeps its row block: A is symmetric, so rows r0:r1 are columns r0:r1
-    dA, db, _ = generate_problem_device("spd", n, 0, "f64", be)
+    # 1-GPU arm) and keeps its row block
+    gen = get_backend("b200", device=local)
+    dA, db, _ = generate_problem_device("spd", n, 0, "f64", gen)
+    gen.ctx.synchronize()
+    blk = DeviceArray(sctx, (n_loc, n), np.float64, ld=_padded_ld(n_loc))
+    bpart = DeviceArray(sctx, (n_loc,), np.float64)
+    x0part = DeviceArray(sctx, (n_loc,), np.float64)
     tA, tb = torch.as_tensor(dA, device=dev), torch.as_tensor(db, device=dev)
-    A_blk = torch.zeros((n, n_loc), dtype=torch.float64, device=dev)
-    b = torch.zeros(n_loc, dtype=torch.float64, device=dev)
+    tblk, tbp = torch.as_tensor(blk, device=dev), torch.as_tensor(bpart, device=dev)
+    tblk.zero_()
+    tbp.zero_()
+    torch.as_tensor(x0part, device=dev).zero_()
     if r1 > r0:
-        A_blk[:, : r1 - r0].copy_(tA[:, r0:r1])
-        b[: r1 - r0].copy_(tb[r0:r1])
+        tblk[: r1 - r0].copy_(tA[r0:r1, :])
+        tbp[: r1 - r0].copy_(tb[r0:r1])
     torch.cuda.synchronize()
-    del tA, tb, dA, db
-    x0 = torch.zeros(n_loc, dtype=torch.float64, device=dev)
+    del tA, tb, tblk, tbp, dA, db
+    A_sh, b_sh, x0_sh = ShardedMatrix(ss, [blk]), ShardedVector(ss, [bpart]), ShardedVector(ss, [x0part])
     cfg = SolverConfig(tolerance=1e-300, max_iterations=iters)
+
+    def max_over_ranks(v):
+        if not multi:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if multi:
+            dist.barrier()
+
     for _ in range(args.warmup):
-        cg_solve_sharded(A_blk, b, x0, n, cfg, comm, ops)
+        cg_solve(A_sh, b_sh, x0_sh, cfg, be)
     torch.cuda.synchronize()
-    comm.barrier()
+    barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    l0 = be.ctx.launches()
-    with ClockSampler(torch.cuda.current_device()) as clk:
+    l0 = sctx.launches()
+    with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            x, rep = cg_solve_sharded(A_blk, b, x0, n, cfg, comm, ops)
+            x, rep = cg_solve(A_sh, b_sh, x0_sh, cfg, be)
         e1.record(stream)
         torch.cuda.synchronize()
-    comm.barrier()
-    launches = be.ctx.launches() - l0
-    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
+    barrier()
+    assert rep.iterations == iters
+    launches = sctx.launches() - l0
+    ms = max_over_ranks(e0.elapsed_time(e1))
 
-    # per-rank GEMV roofline: the local n x n_loc block streamed once (8 (n n_loc + n + n_loc) B)
-    full = torch.zeros(N, dtype=torch.float64, device=dev)
-    y = torch.empty(n_loc, dtype=torch.float64, device=dev)
+    # per-rank GEMV roofline: the local n_loc x n block streamed once (8 (n n_loc + n + n_loc) B)
+    from ctypes import c_void_p
+
+    from paper_1511_07207_b200 import _lib
+    xin = DeviceArray(sctx, (n,), np.float64)
+    torch.as_tensor(xin, device=dev).fill_(1.0)
+    y = DeviceArray(sctx, (n_loc,), np.float64)
+
+    def gemv():
+        _lib.check(sctx.lib.ds_gemv(sctx.handle, _lib.DS_F64, n_loc, n, c_void_p(blk.ptr), blk.ld,
+                                    c_void_p(xin.ptr), c_void_p(y.ptr)))
+
     for _ in range(3):
-        ops.gemv(A_blk, n_loc, n_loc, n, full, y)
+        gemv()
     torch.cuda.synchronize()
     g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     g0.record(stream)
     for _ in range(20):
-        ops.gemv(A_blk, n_loc, n_loc, n, full, y)
+        gemv()
     g1.record(stream)
     torch.cuda.synchronize()
-    gemv_ms = torch.tensor([g0.elapsed_time(g1) / 20], dtype=torch.float64, device=dev)
-    dist.all_reduce(gemv_ms, op=dist.ReduceOp.MAX)
-    gemv_ms = float(gemv_ms.item())
+    gemv_ms = max_over_ranks(g0.elapsed_time(g1) / 20)
     hbm_peak, peak_src = _peaks()
     gbytes = 8.0 * (n * n_loc + n + n_loc)
     achieved = gbytes / (gemv_ms / 1e3) / 1e9
 
-    # end to end: pinned host shards -> device -> solve -> x shard back, every step
-    A_h = torch.empty((n, n_loc), dtype=torch.float64, pin_memory=True)
-    A_h.copy_(A_blk)
-    b_h = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
-    b_h.copy_(b)
-    x0_h = torch.zeros(n_loc, dtype=torch.float64, pin_memory=True)
-    x_h = torch.empty(n_loc, dtype=torch.float64, pin_memory=True)
+    # end to end: pinned host row block, b and x0 shards -> device -> solve -> whole x back
+    A_h = pinned_empty((n_loc, n), np.float64, order="F")
+    blk.to_host(out=A_h)
+    b_h = pinned_empty((n_loc,), np.float64)
+    bpart.to_host(out=b_h)
+    x0_h = pinned_empty((n_loc,), np.float64)
+    x0_h[:] = 0.0
     torch.cuda.synchronize()
-    comm.barrier()
+    barrier()
+    t0 = time.perf_counter()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     for _ in range(args.steps):
-        A_blk.copy_(A_h, non_blocking=True)
-        b.copy_(b_h, non_blocking=True)
-        x0.copy_(x0_h, non_blocking=True)
-        x, rep = cg_solve_sharded(A_blk, b, x0, n, cfg, comm, ops)
-        x_h.copy_(x, non_blocking=True)
+        blk.upload(A_h)
+        bpart.upload(b_h)
+        x0part.upload(x0_h)
+        xs, rep = cg_solve(A_sh, b_sh, x0_sh, cfg, be)
+        x_full = xs.to_host()
     f1.record(stream)
     torch.cuda.synchronize()
-    comm.barrier()
-    e2e_ms = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
-    dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_ms = float(e2e_ms.item())
-    lu = bench_block_cyclic_lu(args, torch, dev, comm, ops) if not getattr(args, "only_cg", False) else None
+    e2e_ms = max_over_ranks(max(f0.elapsed_time(f1), 1e3 * (time.perf_counter() - t0)))
+    barrier()
+    lu = None
+    if multi and not getattr(args, "only_cg", False):
+        from paper_1511_07207_b200.distributed import CudaShardOps, TorchComm
+        ops = CudaShardOps(gen.ctx)
+        ops.bind_current_stream()
+        lu = bench_block_cyclic_lu(args, torch, dev, TorchComm(), ops)
     if q == 0:
         value = iters * args.steps / (ms / 1e3)
         unit = f"CG iters/s (n={n} fp64)"
@@ -781,16 +814,17 @@ def bench_sharded_cg(args, torch, dev, be):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: the reference's seeded spd recipe (harness.py:88-91) generated on the device "
                     "(ds_generate), each rank keeping its row block",
-            "config": c4_config(n, iters, G),
+            "config": dict(c4_config(n, iters, G), api="get_backend('b200', %s)" % (
+                "distributed=True" if multi else f"devices=[{local}]")),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(achieved / hbm_peak, 4), "traffic": None,
-                         "kernel": "per-rank ds_gemv on the n x n_loc block (max over ranks)",
+                         "kernel": "per-rank ds_gemv on the n_loc x n row block (max over ranks)",
                          "algorithmic_bytes_per_launch": gbytes, "avg_launch_ms": round(gemv_ms, 4),
                          "peak_source": peak_src},
             "cpu_baseline": None,
             "e2e": {"value": iters * args.steps / (e2e_ms / 1e3), "unit": unit,
-                    "h2d_bytes_per_step": int(G * (A_h.numel() + 2 * n_loc) * 8),
-                    "d2h_bytes_per_step": int(G * n_loc * 8), "ms_per_step": e2e_ms / args.steps},
+                    "h2d_bytes_per_step": int(G * (A_h.nbytes + b_h.nbytes + x0_h.nbytes)),
+                    "d2h_bytes_per_step": int(G * x_full.nbytes), "ms_per_step": e2e_ms / args.steps},
             "gpu_launches": launches, "clocks": clk.summary(),
             "components": {"lu_block_cyclic": lu} if lu else {},
             "timing": "max over ranks of CUDA-event time"}), flush=True)

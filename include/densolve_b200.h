@@ -210,6 +210,44 @@ int ds_cg_shard_iterations(ds_ctx* ctx, ds_comm* comm, int dtype, int64_t n_loc,
                            void* d_Ap, double* d_state, double* d_hist, double* d_pap, double* d_pap_all,
                            double* d_parts, double* d_rparts, double tol, int64_t cap, int64_t k0, int64_t k1);
 
+/* ---- multi-GPU: row-sharded CG over peer memory - */
+/* Replaces krylov.cg_solve (krylov.py:36-72) for a system whose rows are split
+ * over G shards (one per GPU; `get_backend("b200", devices=[...])` or one process
+ * per GPU).  Shard q owns rows [q*n_loc, (q+1)*n_loc), n_loc = ceil(n/G): an
+ * n_loc x n column-major block of A (zero rows past n) and n_loc entries of b,
+ * x0, x.  The all-gather of p and of the per-shard reduction records is fused
+ * into the kernels that produce them (stores into every peer's exchange region
+ * over NVLink P2P, or CUDA IPC between processes; release/acquire flags), so no
+ * collective library and no host synchronisation sit inside an iteration.
+ * Every shard combines the records in shard order: all shards hold the same
+ * iteration count and history.
+ *
+ * A shard set holds `nlocal` of the G shards in this process (G for one process
+ * driving several GPUs, 1 for one process per GPU).  Connect it with
+ * ds_shardset_connect_local (all shards local) or, across processes, export each
+ * process's DS_SHARD_HANDLE_BYTES handle, gather all G in rank order (e.g. with
+ * torch.distributed) and call ds_shardset_connect_ipc.  xbuf_bytes sizes the
+ * staging buffer of the symmetry gate (n_loc * n_loc * elem when G > 1). */
+#define DS_MAX_SHARDS 16
+#define DS_SHARD_HANDLE_BYTES 64
+typedef struct ds_shardset ds_shardset;
+int ds_shardset_create(int nlocal, ds_ctx* const* ctxs, const int* ranks, int nshards, int dtype, int64_t n,
+                       int64_t xbuf_bytes, ds_shardset** out);
+int ds_shardset_info(const ds_shardset* ss, int64_t* n_loc, int64_t* N);
+int ds_shardset_connect_local(ds_shardset* ss);
+int ds_shardset_ipc_handle(ds_shardset* ss, unsigned char* h_out);
+int ds_shardset_connect_ipc(ds_shardset* ss, const unsigned char* h_all);
+int ds_shardset_destroy(ds_shardset* ss);
+/* All-gather of a row-sharded vector: d_loc[i] (n_loc entries of local shard i) ->
+ * h_out (all n entries) in every process. */
+int ds_shardset_gather(ds_shardset* ss, int dtype, const void* const* d_loc, void* h_out);
+/* d_A[i], d_b[i], d_x0[i], d_x[i]: device operands of local shard i (same order as
+ * ds_shardset_create's ctxs).  h_hist (history, replicated) is filled from local
+ * shard 0; the report is local shard 0's (identical on every shard). */
+int ds_cg_sharded(ds_shardset* ss, int dtype, void* const* d_A, int64_t lda, const void* const* d_b,
+                  const void* const* d_x0, void* const* d_x, double tol, int64_t max_it, int check_sym,
+                  double* h_hist, int64_t hist_cap, ds_solve_info* info);
+
 /* ---- input path: Matrix Market ingestion (host side) ------------------ */
 /* Replaces harness.read_matrix_market (harness.py:138-220).  Parses `path`
  * into the caller's column-major double buffer `h_out` (rows x cols, ld =

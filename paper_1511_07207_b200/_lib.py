@@ -106,6 +106,16 @@ _SIGNATURES = {
     "ds_cg_shard_iterations": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int64, c_void_p, c_int64, c_void_p,
                                        c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                        c_void_p, c_void_p, c_void_p, c_double, c_int64, c_int64, c_int64]),
+    # row-sharded CG over peer memory (ds_shard.cu)
+    "ds_shardset_create": (c_int, [c_int, c_void_p, c_void_p, c_int, c_int, c_int64, c_int64, POINTER(c_void_p)]),
+    "ds_shardset_info": (c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64)]),
+    "ds_shardset_connect_local": (c_int, [c_void_p]),
+    "ds_shardset_ipc_handle": (c_int, [c_void_p, c_void_p]),
+    "ds_shardset_connect_ipc": (c_int, [c_void_p, c_void_p]),
+    "ds_shardset_destroy": (c_int, [c_void_p]),
+    "ds_shardset_gather": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
+    "ds_cg_sharded": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_double, c_int64,
+                              c_int, c_void_p, c_int64, POINTER(SolveInfo)]),
     "ds_mm_read": (c_int, [c_char_p, c_void_p, c_int64, POINTER(c_int64), POINTER(c_int64), POINTER(c_int64)]),
     "ds_mm_last_error": (c_char_p, []),
     "ds_cholesky_factor": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_int64, c_int64, POINTER(c_int64)]),

@@ -274,8 +274,15 @@ BACKEND_NAMES = ("b200",)
 
 def get_backend(name: str = "b200", **kwargs) -> Backend:
     """Construct a backend by name (backends.py:258-264).  Only ``"b200"`` exists:
-    the reference's CPU backends are not part of this package (no CPU fallback)."""
+    the reference's CPU backends are not part of this package (no CPU fallback).
+    ``devices=[...]`` (one process, several GPUs) or ``distributed=True`` (one process
+    per GPU under torch.distributed) return the sharded backend (sharded.py)."""
     if name == "b200":
+        if kwargs.get("devices") is not None or kwargs.get("distributed"):
+            from .sharded import ShardedB200Backend
+            return ShardedB200Backend(**kwargs)
+        kwargs.pop("devices", None)
+        kwargs.pop("distributed", None)
         return B200Backend(**kwargs)
     raise ValueError(f"unknown backend {name!r}; expected one of {BACKEND_NAMES}")
 

@@ -1203,6 +1203,22 @@ template int trsm_upper_launch<double>(ds_ctx*, int64_t, int64_t, const double*,
 template int trsm_upper_launch<float>(ds_ctx*, int64_t, int64_t, const float*, int64_t,
                                       const float*, int64_t, float*, int64_t);
 
+// Load (lazy module loading) every kernel the row-sharded solver launches from this
+// file, before any shard starts spinning on an exchange: a first launch that loads its
+// module waits for the device, i.e. for the peers' exchange kernels on a shared GPU.
+int preload_sharded_kernels_blas() {
+  cudaFuncAttributes a;
+  const void* fns[] = {
+      (const void*)ds_colstream_mv_kernel<double, 2, 8>, (const void*)ds_colstream_mv_kernel<double, 1, 8>,
+      (const void*)ds_colstream_mv_kernel<float, 4, 8>,  (const void*)ds_colstream_mv_kernel<float, 1, 8>,
+      (const void*)ds_colstream_reduce_kernel<double, EPI_DOT>, (const void*)ds_colstream_reduce_kernel<float, EPI_DOT>,
+      (const void*)ds_colstream_reduce_kernel<double, EPI_RESID>,
+      (const void*)ds_colstream_reduce_kernel<float, EPI_RESID>,
+      (const void*)symcheck_kernel<double>, (const void*)symcheck_kernel<float>, (const void*)finish_max2_kernel};
+  for (const void* f : fns) DS_CUDA(cudaFuncGetAttributes(&a, f));
+  return DS_OK;
+}
+
 }  // namespace ds
 
 // ============================================================================

@@ -374,6 +374,14 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
 template <typename T>
 int laswp_range(ds_ctx* ctx, T* W, int64_t ld, int64_t ncols, int64_t k0, int64_t k1, const int64_t* d_piv);
 
+int preload_sharded_kernels_dist() {  // see preload_sharded_kernels_blas
+  cudaFuncAttributes a;
+  const void* fns[] = {(const void*)absdiff_t_kernel<double>, (const void*)absdiff_t_kernel<float>,
+                       (const void*)max2_finish_kernel};
+  for (const void* f : fns) DS_CUDA(cudaFuncGetAttributes(&a, f));
+  return DS_OK;
+}
+
 }  // namespace ds
 
 using namespace ds;

@@ -125,4 +125,8 @@ template <typename T>
 int trsv_upper_trans_launch(ds_ctx* ctx, int64_t n, const T* M, int64_t ld, const T* rhs, T* out,
                             char* scratch);
 
+// ---- lazy-loading guard of the row-sharded solver (ds_shard.cu) ----------------
+int preload_sharded_kernels_blas();
+int preload_sharded_kernels_dist();
+
 }  // namespace ds

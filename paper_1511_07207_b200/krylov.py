@@ -29,6 +29,7 @@ from . import _lib
 from .backends import as_b200
 from .core import (NotSpdError, SolveReport, SolverConfig, check_system)
 from .device import DeviceArray, is_device, to_device
+from .sharded import ShardedB200Backend, cg_solve_sharded
 
 
 def _tally_cg(be, n: int, iterations: int):
@@ -50,6 +51,11 @@ def cg_solve(A, b, x0, cfg: SolverConfig, backend=None):
     t0 = time.perf_counter()
     be = as_b200(backend)
     n = check_system(A, b, x0)
+    if isinstance(be, ShardedB200Backend):  # rows over several GPUs (sharded.py)
+        x, report, info = cg_solve_sharded(A, b, x0, cfg, be)
+        _tally_cg(be, n, info.iterations)
+        report.wall_time = time.perf_counter() - t0
+        return x, report
     ctx = be.ctx
     dA, db, dx0 = to_device(A, ctx), to_device(b, ctx), to_device(x0, ctx)
     dx = DeviceArray(ctx, (n,), dA.dtype)
@@ -178,6 +184,11 @@ def bicgstab_solve(A, b, x0, cfg: SolverConfig, backend=None):
     t0 = time.perf_counter()
     be = as_b200(backend)
     n = check_system(A, b, x0)
+    if isinstance(be, ShardedB200Backend):  # rows over several GPUs (sharded.py)
+        x, report, info = cg_solve_sharded(A, b, x0, cfg, be)
+        _tally_cg(be, n, info.iterations)
+        report.wall_time = time.perf_counter() - t0
+        return x, report
     ctx = be.ctx
     dA, db, dx0 = to_device(A, ctx), to_device(b, ctx), to_device(x0, ctx)
     dx = DeviceArray(ctx, (n,), dA.dtype)

@@ -4,6 +4,12 @@ import sys
 import numpy as np
 import pytest
 
+# Several row shards share the one GPU of the test box (tests/test_gpu_sharded.py): every
+# shard stream needs its own hardware work queue, or a shard's exchange wait queued in
+# front of a peer's signal on a shared queue would never be released.  Set before CUDA
+# initialises in this process (the default is 8 queues).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

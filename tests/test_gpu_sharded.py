@@ -1,0 +1,147 @@
+"""Row-sharded CG behind the reference API (get_backend("b200", devices=[...]) and
+get_backend("b200", distributed=True)) against the CPU oracle (krylov.py:36-72).
+
+The test box has one GPU, so several shards share it: devices=[0, 0] runs two shards
+with their own streams and exchange regions on GPU 0 (the P2P stores are then local
+stores, the flag protocol and the all-gather fusion are exercised unchanged), and the
+distributed test runs two processes on GPU 0 that map each other's exchange regions
+through CUDA IPC."""
+import os
+import sys
+import traceback
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+
+from oracle import densolve_oracle as O  # noqa: E402
+
+
+def _spd(n, seed):
+    A, b, _ = O.generate_problem("spd", n, seed)
+    return A, b
+
+
+@pytest.mark.parametrize("devices,n", [([0], 300), ([0, 0], 300), ([0, 0, 0], 301), ([0, 0, 0, 0], 257)])
+def test_sharded_cg_matches_oracle(devices, n):
+    from paper_1511_07207_b200 import SolverConfig, cg_solve, get_backend
+
+    A, b = _spd(n, 7)
+    be = get_backend("b200", devices=devices)
+    x, rep = cg_solve(A, b, np.zeros_like(b), SolverConfig(tolerance=1e-10), be)
+    xo, ro = O.cg(A, b, np.zeros_like(b), 1e-10)
+    assert rep.converged
+    assert abs(rep.iterations - ro["iterations"]) <= 1
+    k = min(len(rep.residual_history), len(ro["history"]))
+    np.testing.assert_allclose(rep.residual_history[:k], ro["history"][:k], rtol=1e-6)
+    assert np.linalg.norm(x - xo, np.inf) <= 1e-9 * np.linalg.norm(xo, np.inf)
+    # the reference's counter law (one gemv per iteration + setup)
+    assert be.counters.gemv_calls == rep.iterations + 1
+
+
+def test_sharded_cg_equals_across_shard_counts():
+    """The shard-ordered record combination is deterministic: repeated solves are bitwise
+    equal, and every shard count converges to the same solution."""
+    from paper_1511_07207_b200 import SolverConfig, cg_solve, get_backend
+
+    A, b = _spd(512, 3)
+    cfg = SolverConfig(tolerance=1e-12)
+    be2 = get_backend("b200", devices=[0, 0])
+    x1, r1 = cg_solve(A, b, np.zeros_like(b), cfg, be2)
+    x2, r2 = cg_solve(A, b, np.zeros_like(b), cfg, be2)
+    assert np.array_equal(x1, x2) and r1.residual_history == r2.residual_history
+    x0_, r0_ = cg_solve(A, b, np.zeros_like(b), cfg, get_backend("b200"))
+    assert abs(r1.iterations - r0_.iterations) <= 1
+    assert np.linalg.norm(x1 - x0_, np.inf) <= 1e-10 * np.linalg.norm(x0_, np.inf)
+
+
+def test_sharded_cg_fp32_and_c_order():
+    from paper_1511_07207_b200 import SolverConfig, cg_solve, get_backend
+
+    A, b = _spd(200, 5)
+    A32, b32 = np.ascontiguousarray(A.astype(np.float32)), b.astype(np.float32)
+    x, rep = cg_solve(A32, b32, np.zeros_like(b32), SolverConfig(tolerance=1e-5), get_backend("b200", devices=[0, 0]))
+    xo, ro = O.cg(np.asfortranarray(A32), b32, np.zeros_like(b32), 1e-5)
+    assert x.dtype == np.float32 and rep.converged
+    assert abs(rep.iterations - ro["iterations"]) <= 1
+    assert np.linalg.norm(x - xo, np.inf) <= 1e-3 * np.linalg.norm(xo, np.inf)
+
+
+def test_sharded_cg_nonzero_x0_and_device_resident():
+    from paper_1511_07207_b200 import SolverConfig, ShardedVector, cg_solve, get_backend
+
+    A, b = _spd(333, 11)
+    x0 = np.random.default_rng(1).standard_normal(333)
+    be = get_backend("b200", devices=[0, 0, 0])
+    dA, db, dx0 = be.stage_in(A, b, x0)
+    x, rep = cg_solve(dA, db, dx0, SolverConfig(tolerance=1e-10), be)
+    assert isinstance(x, ShardedVector)
+    xh = be.stage_out(x)
+    xo, ro = O.cg(A, b, x0, 1e-10)
+    assert abs(rep.iterations - ro["iterations"]) <= 1
+    assert np.linalg.norm(xh - xo, np.inf) <= 1e-9 * np.linalg.norm(xo, np.inf)
+
+
+def test_sharded_cg_errors():
+    from paper_1511_07207_b200 import (DegenerateRhsError, NotSpdError, SolverConfig, cg_solve, get_backend)
+
+    be = get_backend("b200", devices=[0, 0])
+    A, b = _spd(128, 2)
+    B = A.copy(order="F")
+    B[3, 100] += 1e-3  # not symmetric: caught by the sharded gate (off-diagonal block pair)
+    with pytest.raises(NotSpdError):
+        cg_solve(B, b, np.zeros_like(b), SolverConfig(tolerance=1e-8), be)
+    with pytest.raises(NotSpdError):  # symmetric, negative definite: p'Ap <= 0
+        cg_solve(np.asfortranarray(-A), b, np.zeros_like(b), SolverConfig(tolerance=1e-8), be)
+    with pytest.raises(DegenerateRhsError):
+        cg_solve(A, np.zeros_like(b), np.zeros_like(b), SolverConfig(tolerance=1e-8), be)
+    # the shard set is still usable after the errors
+    x, rep = cg_solve(A, b, np.zeros_like(b), SolverConfig(tolerance=1e-8), be)
+    assert rep.converged
+
+
+def _dist_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    try:
+        import torch.distributed as dist
+
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), LOCAL_RANK="0")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_1511_07207_b200 import SolverConfig, cg_solve, get_backend
+
+        A, b = _spd(301, 9)  # same host arrays on every rank (the reference call)
+        be = get_backend("b200", distributed=True, device=0)
+        x, rep = cg_solve(A, b, np.zeros_like(b), SolverConfig(tolerance=1e-10), be)
+        q.put((rank, x, rep.iterations, rep.residual_history))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:
+        q.put((rank, traceback.format_exc(), None, None))
+
+
+def test_distributed_cg_two_processes_ipc():
+    import torch.multiprocessing as mp
+
+    from test_distributed_gloo import _free_port
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(60)
+    for r, x, it, h in res:
+        assert it is not None, x
+    A, b = _spd(301, 9)
+    xo, ro = O.cg(A, b, np.zeros_like(b), 1e-10)
+    (_, xa, ia, ha), (_, xb, ib, hb) = sorted(res, key=lambda t: t[0])
+    assert ia == ib and ha == hb and np.array_equal(xa, xb)  # replicated decisions
+    assert abs(ia - ro["iterations"]) <= 1
+    assert np.linalg.norm(xa - xo, np.inf) <= 1e-9 * np.linalg.norm(xo, np.inf)
