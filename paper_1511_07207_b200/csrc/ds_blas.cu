@@ -5,6 +5,7 @@
 // iteration is built on (K1 in SURVEY.md §2b); GEMM is the FP64 DMMA
 // (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4) trailing-update kernel of the
 // blocked LU (K13); TRSM/GER are the panel-side helpers (K12, K10).
+#include <cuda.h>  // CUtensorMap (types only; the encoder is resolved at run time)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -902,6 +903,211 @@ __global__ void __launch_bounds__(gemm64::THREADS, 2)
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-fed variant (the default for 16-byte aligned operands with even leading
+// dimensions): the A and B slabs are moved by the tensor-memory accelerator
+// (cp.async.bulk.tensor, 128-byte swizzle) into a 4-stage ring; one elected thread
+// issues the copies and arms the stage's full mbarrier with the byte count, the 8
+// compute warps release a stage through its empty mbarrier.  No per-thread address
+// math or LDGSTS in the main loop, and out-of-range rows/columns/k are zero-filled
+// by the TMA unit (no ragged-tile code).  Same CTA/warp tiling and the same DMMA
+// sequence per output element as gemm64_kernel, so results are bitwise equal.
+//   A stage: 8 boxes of 16 (m) x 16 (k), box b at b*2 KB, row k = 128 B, 16-byte chunk
+//            index (m/2) ^ (k & 7)          (SWIZZLE_128B, stage base 1024-B aligned)
+//   B stage: 64 rows (n) of 16 (k) doubles, chunk index (k/2) ^ (n & 7)
+// ---------------------------------------------------------------------------
+namespace gemm64 {
+constexpr int A_TMA_BYTES = BM * BK * 8;  // 16 KB
+constexpr int B_TMA_BYTES = BN * BK * 8;  // 8 KB
+constexpr int STAGE_TMA_BYTES = A_TMA_BYTES + B_TMA_BYTES;
+constexpr size_t SMEM_TMA = (size_t)STAGES * STAGE_TMA_BYTES + 1024;  // + alignment slack
+}  // namespace gemm64
+
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          (unsigned)__cvta_generic_to_shared(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+template <int MODE /*0: general, 1: out = C - AB*/>
+__global__ void __launch_bounds__(gemm64::THREADS, 2)
+    gemm64_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t m,
+                      int64_t n, int64_t k, double alpha, double beta, const double* C, int64_t ldc, double* out,
+                      int64_t ldo, int tri) {
+  using namespace gemm64;
+  if (tri && (int64_t)(blockIdx.x + 1) * BM <= (int64_t)blockIdx.y * BN) return;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+  const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+  const int g = lane >> 2, t = lane & 3;
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
+  const int64_t ktiles = ceil_div(k, BK);
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init_cta(&full_bar[s], 1);
+      mbar_init_cta(&empty_bar[s], THREADS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t kt) {  // one thread: arm full[s] and copy slab kt
+    const int s = (int)(kt % STAGES);
+    unsigned char* st = sm + (size_t)s * STAGE_TMA_BYTES;
+    mbar_arrive_expect_tx(&full_bar[s], STAGE_TMA_BYTES);
+    const int kc = (int)(kt * BK);
+#pragma unroll
+    for (int b = 0; b < BM / 16; ++b) tma_load_2d(st + b * 2048, &tmA, (int)(m0 + 16 * b), kc, &full_bar[s]);
+    tma_load_2d(st + A_TMA_BYTES, &tmB, kc, (int)n0, &full_bar[s]);
+  };
+  if (threadIdx.x == 0)
+    for (int s = 0; s < STAGES - 1; ++s)
+      if (s < ktiles) issue(s);
+
+  double acc[MI][4][2];
+  if (MODE == 1) {  // accumulators start from C (the LU update out = C - A B, A negated)
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      const int64_t r = m0 + wm * WR + i * 8 + g;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t c = n0 + wn * 32 + j * 8 + 2 * t + e;
+          acc[i][j][e] = (r < m && c < n) ? C[r + c * ldc] : 0.0;
+        }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  }
+  // per-lane swizzled fragment offsets (bytes within a stage), see the layout above
+  const unsigned a_lane = (unsigned)(wm * 2) * 2048u + (unsigned)t * 128u + ((unsigned)((g >> 1) ^ t) << 4) +
+                          ((unsigned)(g & 1) << 3);
+  unsigned b_lane[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    b_lane[q] = (unsigned)A_TMA_BYTES + (unsigned)(wn * 32 + g) * 128u +
+                ((unsigned)(((t >> 1) ^ g) ^ (2 * q)) << 4) + ((unsigned)(t & 1) << 3);
+
+  for (int64_t kt = 0; kt < ktiles; ++kt) {
+    if (warp == 0) {
+      if (lane == 0) {
+        const int64_t pf = kt + STAGES - 1;  // refill the stage every warp released at kt - 1
+        if (pf < ktiles) {
+          if (kt >= 1) mbar_wait_cta(&empty_bar[pf % STAGES], (unsigned)(((kt - 1) / STAGES) & 1));
+          issue(pf);
+        }
+      }
+      __syncwarp();
+    }
+    const int s = (int)(kt % STAGES);
+    mbar_wait_cta(&full_bar[s], (unsigned)((kt / STAGES) & 1));
+    const unsigned char* st = sm + (size_t)s * STAGE_TMA_BYTES;
+#pragma unroll
+    for (int q = 0; q < BK / 4; ++q) {
+      double a[MI], b[4];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        const unsigned off = a_lane + (unsigned)(i >> 1) * 2048u + (unsigned)q * 512u +
+                             ((unsigned)(((i & 1) << 2) ^ ((q & 1) << 2)) << 4);
+        const double v = *reinterpret_cast<const double*>(st + off);
+        a[i] = MODE == 1 ? -v : v;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = *reinterpret_cast<const double*>(st + b_lane[q] + (unsigned)j * 1024u);
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cta(&empty_bar[s]);
+  }
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    const int64_t r = m0 + wm * WR + i * 8 + g;
+    if (r >= m) continue;
+    double cv[4][2];
+    if (MODE == 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t c = n0 + wn * 32 + j * 8 + 2 * t + e;
+          cv[j][e] = (c < n && beta != 0.0) ? C[r + c * ldc] : 0.0;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t c = n0 + wn * 32 + j * 8 + 2 * t + e;
+        if (c >= n) continue;
+        double o;
+        if (MODE == 1) {
+          o = acc[i][j][e];
+        } else {
+          const double cb = beta == 0.0 ? 0.0 : __dmul_rn(beta, cv[j][e]);
+          o = __dadd_rn(cb, __dmul_rn(alpha, acc[i][j][e]));
+        }
+        out[r + c * ldo] = o;
+      }
+    }
+  }
+}
+
+// Host side: the driver's tensor-map encoder, resolved once through the runtime (no
+// libcuda link).  A 2-D map of a column-major matrix: dim 0 = rows (contiguous), dim 1 =
+// columns, box {16, box_cols}, 128-byte swizzle, out-of-range elements zero-filled.
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn tensor_map_encoder() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+static bool encode_colmajor_map(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld,
+                                unsigned box_rows, unsigned box_cols) {
+  EncodeTiledFn enc = tensor_map_encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  const cuuint32_t box[2] = {box_rows, box_cols};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+static bool gemm_tma_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("DENSOLVE_GEMM_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // FP32 GEMM (FFMA, fp32 accumulation like sgemm): 64x64 tile, 256 threads, 4x4 per thread.
 template <int MODE>
 __global__ void __launch_bounds__(256)
@@ -977,6 +1183,28 @@ static int gemm_impl(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha,
   const bool vec = (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
                    (reinterpret_cast<uintptr_t>(B) % 16 == 0) && (lda % 2 == 0) && (ldb % 2 == 0);
   const bool sub = (alpha == -1.0 && beta == 1.0);
+  if (vec && k > 0 && gemm_tma_enabled() && m < (1ll << 31) && n < (1ll << 31) && k < (1ll << 31)) {
+    CUtensorMap ta, tb;
+    if (encode_colmajor_map(&ta, A, m, k, lda, 16, BK) && encode_colmajor_map(&tb, B, k, n, ldb, BK, BN)) {
+      static bool tma_attr = false;
+      if (!tma_attr) {
+        DS_CUDA(cudaFuncSetAttribute(gemm64_tma_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)SMEM_TMA));
+        DS_CUDA(cudaFuncSetAttribute(gemm64_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)SMEM_TMA));
+        tma_attr = true;
+      }
+      if (sub)
+        gemm64_tma_kernel<1><<<grid, THREADS, SMEM_TMA, ctx->stream>>>(ta, tb, m, n, k, alpha, beta, C, ldc, out,
+                                                                       ldo, tri);
+      else
+        gemm64_tma_kernel<0><<<grid, THREADS, SMEM_TMA, ctx->stream>>>(ta, tb, m, n, k, alpha, beta, C, ldc, out,
+                                                                       ldo, tri);
+      count_launch(ctx);
+      DS_CHECK_LAUNCH();
+      return DS_OK;
+    }
+  }
   if (k == 0) {
     // out = beta*C (alpha*0 added)
     if (vec && sub)
