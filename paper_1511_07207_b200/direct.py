@@ -29,6 +29,7 @@ from .backends import as_b200
 from .core import (CholeskyFactor, DimensionError, LuFactors, NotSpdError, SingularMatrixError,
                    check_precision, check_square)
 from .device import DeviceArray, is_device, to_device
+from .sharded import ShardedB200Backend, lu_factor_block_cyclic_api
 
 
 def _tally_lu(be, n: int, b: int, zero_cols: np.ndarray, blocked: bool):
@@ -56,6 +57,13 @@ def _factor(A, b: int, backend, blocked: bool) -> LuFactors:
     be = as_b200(backend)
     n = check_square(A)
     check_precision(A)
+    if isinstance(be, ShardedB200Backend) and not is_device(A):
+        # columns dealt to the shards in NB-wide blocks (1-D block-cyclic, sharded.py)
+        packed, piv, singular = lu_factor_block_cyclic_api(A, max(b, 1), be)
+        zero = np.zeros(max(n, 1), dtype=np.int8)
+        zero[:n] = np.diagonal(packed) == 0
+        _tally_lu(be, n, max(b, 1), zero, blocked)
+        return LuFactors(packed=packed, pivots=piv.astype(np.intp), singular=singular)
     ctx = be.ctx
     src = to_device(A, ctx)
     W = src.copy() if is_device(A) else src  # never mutate the caller's A (direct.py:61)

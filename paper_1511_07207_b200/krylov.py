@@ -29,7 +29,7 @@ from . import _lib
 from .backends import as_b200
 from .core import (NotSpdError, SolveReport, SolverConfig, check_system)
 from .device import DeviceArray, is_device, to_device
-from .sharded import ShardedB200Backend, cg_solve_sharded
+from .sharded import ShardedB200Backend, cg_solve_sharded, gmres_solve_rows
 
 
 def _tally_cg(be, n: int, iterations: int):
@@ -107,6 +107,14 @@ def gmres_solve(A, b, x0, cfg: SolverConfig, backend=None, workspace_sink: list 
     t0 = time.perf_counter()
     be = as_b200(backend)
     n = check_system(A, b, x0)
+    if isinstance(be, ShardedB200Backend):  # rows over several GPUs (sharded.py)
+        if workspace_sink is not None:
+            raise ValueError("workspace_sink is not supported by the sharded backend (V lives in row shards)")
+        be.tally("nrm2", 2 * n)
+        x, report = gmres_solve_rows(A, b, x0, cfg, be)
+        _tally_gmres(be, n, report, len(report.restart_cycles or []) + 1)
+        report.wall_time = time.perf_counter() - t0
+        return x, report
     ctx = be.ctx
     m = int(cfg.restart_m)
     dA, db, dx0 = to_device(A, ctx), to_device(b, ctx), to_device(x0, ctx)

@@ -145,3 +145,36 @@ def test_distributed_cg_two_processes_ipc():
     assert ia == ib and ha == hb and np.array_equal(xa, xb)  # replicated decisions
     assert abs(ia - ro["iterations"]) <= 1
     assert np.linalg.norm(xa - xo, np.inf) <= 1e-9 * np.linalg.norm(xo, np.inf)
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0]])
+def test_sharded_gmres_matches_oracle(devices):
+    """krylov.gmres_solve with A split by rows (distributed.gmres_solve_sharded per shard,
+    one thread per shard, ThreadComm collectives)."""
+    from paper_1511_07207_b200 import SolverConfig, get_backend, gmres_solve
+
+    A, b, _ = O.generate_problem("general_nonsymmetric", 301, 4)
+    be = get_backend("b200", devices=devices)
+    x, rep = gmres_solve(A, b, np.zeros_like(b), SolverConfig(tolerance=1e-10, restart_m=20), be)
+    xo, ro = O.gmres(A, b, np.zeros_like(b), 1e-10, 20)
+    assert rep.converged
+    assert abs(rep.iterations - ro["iterations"]) <= 1
+    assert np.linalg.norm(x - xo, np.inf) <= 1e-8 * np.linalg.norm(xo, np.inf)
+
+
+@pytest.mark.parametrize("devices,n,b", [([0], 300, 64), ([0, 0], 600, 64), ([0, 0, 0], 777, 32)])
+def test_sharded_lu_matches_oracle(devices, n, b):
+    """direct.lu_factor_blocked with the columns dealt block-cyclically to the shards:
+    the pivot sequence equals the oracle's, the factors agree within the blocked-vs-
+    unblocked bound, lu_solve solves."""
+    from paper_1511_07207_b200 import get_backend, lu_factor_blocked, lu_solve
+
+    A = np.asfortranarray(np.random.default_rng(n).uniform(-1, 1, (n, n)))
+    be = get_backend("b200", devices=devices)
+    f = lu_factor_blocked(A, b, be)
+    W, piv, _ = O.lu_factor_blocked(A, b)
+    assert np.array_equal(np.asarray(f.pivots), piv)
+    assert np.abs(f.packed - W).max() <= 100 * n * np.finfo(np.float64).eps * np.abs(A).max()
+    rhs = np.ones(n)
+    x = lu_solve(f, rhs)
+    assert np.linalg.norm(A @ x - rhs) <= 1e-10 * np.linalg.norm(A, 1) * np.linalg.norm(x)
