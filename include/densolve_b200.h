@@ -190,26 +190,6 @@ int ds_upload_async(ds_ctx* ctx, int dtype, const void* h_src, int64_t rows, int
 int ds_wait_event(ds_ctx* ctx, void* event);
 int ds_event_destroy(void* event);
 
-/* ---- multi-GPU: NCCL inside the library (row-sharded Krylov) - */
-/* A communicator over the ranks of a row-sharded solve.  Rank 0 creates the
- * id with ds_comm_unique_id, the caller distributes the DS_COMM_ID_BYTES bytes
- * (e.g. torch.distributed.broadcast), every rank calls ds_comm_create.  NCCL is
- * dlopen'ed at run time (libnccl.so.2). */
-#define DS_COMM_ID_BYTES 128
-typedef struct ds_comm ds_comm;
-int ds_comm_unique_id(unsigned char* h_out);
-int ds_comm_create(ds_ctx* ctx, int nranks, int rank, const unsigned char* h_id, ds_comm** out);
-int ds_comm_destroy(ds_comm* comm);
-/* Iterations [k0, k1) of the row-sharded CG (krylov.py:54-67) on this rank:
- * per iteration ncclAllGather(p) -> local GEMV -> p'Ap record -> ncclAllGather ->
- * rank-ordered alpha, x/r update -> ncclAllGather of (r'r, scale, ssq) -> beta,
- * p update, history, stop word (d_state, DS shard layout of ds_cg_shard_*).
- * Enqueued on the context stream, no host synchronisation. */
-int ds_cg_shard_iterations(ds_ctx* ctx, ds_comm* comm, int dtype, int64_t n_loc, int64_t n,
-                           const void* d_A_blk, int64_t lda, void* d_full, void* d_x, void* d_r, void* d_p,
-                           void* d_Ap, double* d_state, double* d_hist, double* d_pap, double* d_pap_all,
-                           double* d_parts, double* d_rparts, double tol, int64_t cap, int64_t k0, int64_t k1);
-
 /* ---- multi-GPU: row-sharded CG over peer memory - */
 /* Replaces krylov.cg_solve (krylov.py:36-72) for a system whose rows are split
  * over G shards (one per GPU; `get_backend("b200", devices=[...])` or one process

@@ -100,12 +100,6 @@ _SIGNATURES = {
                                 POINTER(c_void_p)]),
     "ds_wait_event": (c_int, [c_void_p, c_void_p]),
     "ds_event_destroy": (c_int, [c_void_p]),
-    "ds_comm_unique_id": (c_int, [c_void_p]),
-    "ds_comm_create": (c_int, [c_void_p, c_int, c_int, c_void_p, POINTER(c_void_p)]),
-    "ds_comm_destroy": (c_int, [c_void_p]),
-    "ds_cg_shard_iterations": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int64, c_void_p, c_int64, c_void_p,
-                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                       c_void_p, c_void_p, c_void_p, c_double, c_int64, c_int64, c_int64]),
     # row-sharded CG over peer memory (ds_shard.cu)
     "ds_shardset_create": (c_int, [c_int, c_void_p, c_void_p, c_int, c_int, c_int64, c_int64, POINTER(c_void_p)]),
     "ds_shardset_info": (c_int, [c_void_p, POINTER(c_int64), POINTER(c_int64)]),

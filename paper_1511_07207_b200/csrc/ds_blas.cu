@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ds_common.cuh"
 #include "ds_kernels.cuh"
@@ -84,6 +85,11 @@ GemvPlan gemv_plan(ds_ctx* ctx, int64_t m, int64_t n, size_t elem) {
   chunk = std::max<int64_t>(chunk, 64);
   chunk = std::min<int64_t>(chunk, 2048);
   chunk = ceil_div(chunk, 8) * 8;
+  static const int64_t forced = [] {
+    const char* e = getenv("DENSOLVE_GEMV_CHUNK");  // tuning experiments only
+    return e ? (int64_t)atoll(e) : (int64_t)0;
+  }();
+  if (forced >= 8) chunk = ceil_div(forced, 8) * 8;
   p.chunk = chunk;
   p.nchunks = ceil_div(std::max<int64_t>(n, 1), chunk);
   p.part_bytes = (size_t)p.nchunks * (size_t)std::max<int64_t>(m, 1) * sizeof(double);

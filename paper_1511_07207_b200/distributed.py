@@ -110,28 +110,6 @@ class TorchComm:
     def barrier(self):
         self.dist.barrier(group=self.group)
 
-    def native(self, ctx, device):
-        """The library's own NCCL communicator over this group (ds_comm_create), created
-        once: rank 0's ncclUniqueId is broadcast through torch.distributed."""
-        import ctypes
-
-        import torch
-
-        if getattr(self, "_native", None) is None:
-            idt = torch.zeros(128, dtype=torch.uint8, device=device)
-            if self.rank == 0:
-                buf = (ctypes.c_ubyte * 128)()
-                _lib.check(ctx.lib.ds_comm_unique_id(ctypes.cast(buf, c_void_p)))
-                idt.copy_(torch.tensor(list(bytes(buf)), dtype=torch.uint8))
-            self.dist.broadcast(idt, 0, group=self.group)
-            raw = bytes(idt.cpu().tolist())
-            h = c_void_p()
-            buf = (ctypes.c_ubyte * 128).from_buffer_copy(raw)
-            _lib.check(ctx.lib.ds_comm_create(ctx.handle, self.size, self.rank, ctypes.cast(buf, c_void_p),
-                                              ctypes.byref(h)))
-            self._native = h
-        return self._native
-
 
 # ---------------------------------------------------------------------------
 # per-rank compute on the device (product implementation)
@@ -183,13 +161,6 @@ class CudaShardOps:
     def cg_init(self, bparts, rparts, nranks, state, hist, tol, cap):
         _lib.check(self.lib.ds_cg_shard_init(self.h, _p(bparts), _p(rparts), nranks, _p(state), _p(hist),
                                              float(tol), int(cap)))
-
-    def cg_iterations(self, comm, A, n_loc, n, full, x, r, p, Ap, state, hist, pap, pap_all, parts, rparts,
-                      tol, cap, k0, k1):
-        _lib.check(self.lib.ds_cg_shard_iterations(
-            self.h, comm, self.code(x), n_loc, n, _p(A), n_loc, _p(full), _p(x), _p(r), _p(p), _p(Ap),
-            _p(state), _p(hist), _p(pap), _p(pap_all), _p(parts), _p(rparts), float(tol), int(cap), int(k0),
-            int(k1)))
 
     def cg_update(self, nranks, pap_all, state, k, x, r, p, Ap, out3):
         _lib.check(self.lib.ds_cg_shard_update(self.h, self.code(x), x.numel(), nranks, _p(pap_all), _p(state),
@@ -339,26 +310,12 @@ def cg_solve_sharded(A_blk, b_loc, x0_loc, n: int, cfg: SolverConfig, comm, ops,
     if st[1] == 0.0:
         raise DegenerateRhsError("||b|| = 0")
     p = r.clone()
-    # DENSOLVE_NATIVE_NCCL=1: the chunk's iterations are enqueued by the library itself with
-    # its own NCCL communicator (ds_cg_shard_iterations, no per-iteration Python).  Off by
-    # default: at N=1 it measured slower (640 vs 720 it/s, raw NCCL kernels vs torch's 1-rank
-    # shortcut) and N>1 is unmeasured this round.  The per-call loop below also serves the
-    # CPU / gloo test double.
-    import os as _os
-    native = None
-    if (_os.environ.get("DENSOLVE_NATIVE_NCCL") == "1" and isinstance(ops, CudaShardOps)
-            and isinstance(comm, TorchComm) and dev.type == "cuda" and comm.dist.get_backend(comm.group) == "nccl"):
-        native = comm.native(ops.ctx, dev)
     k, chunk = 0, 2
     while True:
         st = state.cpu().numpy()
         if st[3] <= k or k >= cap or st[2] != 0:
             break
         kend = min(cap, k + chunk)
-        if native is not None:
-            ops.cg_iterations(native, A_blk, n_loc, n, full, x, r, p, Ap, state, hist, pap, pap_all, parts,
-                              rparts, cfg.tolerance, cap, k, kend)
-            k = kend
         while k < kend:
             comm.allgather(full, p)
             ops.gemv(A_blk, n_loc, n_loc, n, full, Ap)
