@@ -1041,6 +1041,10 @@ __global__ void __launch_bounds__(gemm64::THREADS, 2)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
+    // Release the stage to the TMA unit: this thread's generic-proxy reads of it are ordered
+    // before the async-proxy writes that refill it (without the proxy fence the refill raced
+    // with fragment loads still in flight under concurrent kernels: rare, wrong products)
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive_cta(&empty_bar[s]);
   }
@@ -1112,6 +1116,105 @@ static bool gemm_tma_enabled() {
     return !(e && e[0] == '0');
   }();
   return on;
+}
+
+// FP32 GEMM, large tiles (the fp32 LU / Cholesky trailing update): CTA tile 128 x 128,
+// k-slab 8, 256 threads of 8 x 8 outputs (two 4 x 4 quadrants per dimension, so the
+// fragment reads are two float4 per operand per k), the next slab prefetched into
+// registers while the current one is consumed from a double-buffered shared-memory
+// stage (one CTA barrier per slab).  B's slab is transposed on its way into shared
+// memory ([k][n]).  Every output accumulates fmaf(a_k, b_k, acc) for k = 0, 1, ...
+// from 0 exactly like gemm32_kernel, so the two are bitwise equal.
+namespace gemm32 {
+constexpr int BM = 128, BN = 128, BK = 8, THREADS = 256, PAD = 4;
+}
+template <int MODE, bool VEC>
+__global__ void __launch_bounds__(gemm32::THREADS, 2)
+    gemm32_big_kernel(int64_t m, int64_t n, int64_t k, float alpha, const float* __restrict__ A, int64_t lda,
+                      const float* __restrict__ B, int64_t ldb, float beta, const float* C, int64_t ldc, float* out,
+                      int64_t ldo, int tri) {
+  using namespace gemm32;
+  if (tri && (int64_t)(blockIdx.x + 1) * BM <= (int64_t)blockIdx.y * BN) return;
+  __shared__ __align__(16) float As[2][BK][BM + PAD];
+  __shared__ __align__(16) float Bs[2][BK][BN + PAD];
+  const int t = threadIdx.x;
+  const int tx = t & 15, ty = t >> 4;
+  const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+  // loader roles: A: k row t/32, m = 4 (t%32) .. +3;  B: column n = t/2, k = 4 (t%2) .. +3
+  const int la_k = t >> 5, la_m = (t & 31) * 4;
+  const int lb_n = t >> 1, lb_k = (t & 1) * 4;
+  float ra[4], rb[4];
+  auto load = [&](int64_t k0) {
+    const int64_t gk = k0 + la_k, gm = m0 + la_m;
+    if (VEC && gk < k && gm + 3 < m) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(A + gk * lda + gm));
+      ra[0] = v.x; ra[1] = v.y; ra[2] = v.z; ra[3] = v.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) ra[e] = (gk < k && gm + e < m) ? A[gk * lda + gm + e] : 0.f;
+    }
+    const int64_t gn = n0 + lb_n, gk2 = k0 + lb_k;
+    if (VEC && gn < n && gk2 + 3 < k) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(B + gn * ldb + gk2));
+      rb[0] = v.x; rb[1] = v.y; rb[2] = v.z; rb[3] = v.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) rb[e] = (gn < n && gk2 + e < k) ? B[gn * ldb + gk2 + e] : 0.f;
+    }
+  };
+  auto store = [&](int buf) {
+    *reinterpret_cast<float4*>(&As[buf][la_k][la_m]) = make_float4(ra[0], ra[1], ra[2], ra[3]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) Bs[buf][lb_k + e][lb_n] = rb[e];
+  };
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  const int64_t ktiles = ceil_div(k, BK);
+  if (ktiles > 0) {
+    load(0);
+    store(0);
+  }
+  __syncthreads();
+  for (int64_t kt = 0; kt < ktiles; ++kt) {
+    const int buf = (int)(kt & 1);
+    if (kt + 1 < ktiles) load((kt + 1) * BK);  // in flight during the FMAs below
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 + tx * 4]);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    if (kt + 1 < ktiles) store(buf ^ 1);  // the other buffer: its readers passed the last barrier
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t r = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    if (r >= m) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t c = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+      if (c >= n) continue;
+      float o;
+      if (MODE == 1) {
+        o = __fsub_rn(C[r + c * ldc], acc[i][j]);
+      } else {
+        const float cb = beta == 0.f ? 0.f : __fmul_rn(beta, C[r + c * ldc]);
+        o = __fadd_rn(cb, __fmul_rn(alpha, acc[i][j]));
+      }
+      out[r + c * ldo] = o;
+    }
+  }
 }
 
 // FP32 GEMM (FFMA, fp32 accumulation like sgemm): 64x64 tile, 256 threads, 4x4 per thread.
@@ -1243,8 +1346,31 @@ static int gemm_impl(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha,
                      int64_t lda, const float* B, int64_t ldb, double beta, const float* C,
                      int64_t ldc, float* out, int64_t ldo, int tri) {
   if (m == 0 || n == 0) return DS_OK;
+  const bool sub = alpha == -1.0 && beta == 1.0;
+  static const bool small_only = [] {
+    const char* e = getenv("DENSOLVE_GEMM32_SMALL");  // A/B switch: the 64 x 64 kernel everywhere
+    return e && e[0] == '1';
+  }();
+  if (!small_only && m >= 128 && n >= 128 && k >= 128) {  // K = 64 panels: more CTAs win (21.7 vs 12.4 TF)
+    using namespace gemm32;
+    dim3 grid((unsigned)ceil_div(m, BM), (unsigned)ceil_div(n, BN));
+    const bool vec = (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (reinterpret_cast<uintptr_t>(B) % 16 == 0) &&
+                     (lda % 4 == 0) && (ldb % 4 == 0);
+    const float fa = (float)alpha, fb = (float)beta;
+    if (sub && vec)
+      gemm32_big_kernel<1, true><<<grid, THREADS, 0, ctx->stream>>>(m, n, k, fa, A, lda, B, ldb, fb, C, ldc, out, ldo, tri);
+    else if (sub)
+      gemm32_big_kernel<1, false><<<grid, THREADS, 0, ctx->stream>>>(m, n, k, fa, A, lda, B, ldb, fb, C, ldc, out, ldo, tri);
+    else if (vec)
+      gemm32_big_kernel<0, true><<<grid, THREADS, 0, ctx->stream>>>(m, n, k, fa, A, lda, B, ldb, fb, C, ldc, out, ldo, tri);
+    else
+      gemm32_big_kernel<0, false><<<grid, THREADS, 0, ctx->stream>>>(m, n, k, fa, A, lda, B, ldb, fb, C, ldc, out, ldo, tri);
+    count_launch(ctx);
+    DS_CHECK_LAUNCH();
+    return DS_OK;
+  }
   dim3 grid((unsigned)ceil_div(m, 64), (unsigned)ceil_div(n, 64));
-  if (alpha == -1.0 && beta == 1.0)
+  if (sub)
     gemm32_kernel<1><<<grid, 256, 0, ctx->stream>>>(m, n, k, (float)alpha, A, lda, B, ldb,
                                                     (float)beta, C, ldc, out, ldo, tri);
   else

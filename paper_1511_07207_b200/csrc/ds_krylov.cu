@@ -689,7 +689,7 @@ constexpr int kOrthThreads = 512;
 constexpr unsigned kOrthMaxCluster = 16;  // the launch uses 16 or 8
 
 template <typename T>
-__global__ void __launch_bounds__(kOrthThreads, 1)
+__global__ void __launch_bounds__(kOrthThreads, 2)
     arnoldi_orth_cluster_kernel(int64_t n, T* V, int64_t ldv, int k, int passes, T* H, T* Hraw, int64_t ldh, T* g,
                                 T* cs, T* sn, double* est_out, GmDev* st, double tol, int64_t total_before,
                                 int64_t cap, Gate gate, const double* __restrict__ gpart, int64_t nchunks,
@@ -731,12 +731,13 @@ __global__ void __launch_bounds__(kOrthThreads, 1)
     }
     const double* pr = gpart + r0 + r;
     double s = 0.0;
-    for (int64_t c0 = 0; c0 < nchunks; c0 += 32) {
-      double v[32];
+    constexpr int PB = 16;  // partial loads in flight (the 64-register budget of 2 CTAs/SM)
+    for (int64_t c0 = 0; c0 < nchunks; c0 += PB) {
+      double v[PB];
 #pragma unroll
-      for (int u = 0; u < 32; ++u) v[u] = c0 + u < nchunks ? pr[(c0 + u) * n] : 0.0;
+      for (int u = 0; u < PB; ++u) v[u] = c0 + u < nchunks ? pr[(c0 + u) * n] : 0.0;
 #pragma unroll
-      for (int u = 0; u < 32; ++u)
+      for (int u = 0; u < PB; ++u)
         if (c0 + u < nchunks) s += v[u];
     }
     wv[r] = (double)(T)s;
@@ -788,12 +789,13 @@ __global__ void __launch_bounds__(kOrthThreads, 1)
     for (int r = tid; r < nr; r += blockDim.x) {
       T wi = (T)wv[r];
       const T* vr = V + r0 + r;
-      for (int j0 = 0; j0 < kc; j0 += 32) {  // up to 32 basis loads in flight, then the ordered axpys
-        T vv[32];
+      constexpr int VB = sizeof(T) == 8 ? 16 : 32;  // basis loads in flight, then the ordered axpys
+      for (int j0 = 0; j0 < kc; j0 += VB) {
+        T vv[VB];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) vv[u] = j0 + u < kc ? vr[(int64_t)(j0 + u) * ldv] : T(0);
+        for (int u = 0; u < VB; ++u) vv[u] = j0 + u < kc ? vr[(int64_t)(j0 + u) * ldv] : T(0);
 #pragma unroll
-        for (int u = 0; u < 32; ++u)
+        for (int u = 0; u < VB; ++u)
           if (j0 + u < kc) wi = add_rn(wi, mul_rn((T)(-hs[j0 + u]), vv[u]));
       }
       wv[r] = (double)wi;

@@ -1,6 +1,7 @@
-"""Bitwise equality of the TMA-fed and the cp.async DMMA GEMM on ragged shapes:
+"""Bitwise equality of GEMM kernel variants on ragged shapes:
 DENSOLVE_GEMM_TMA=0 python tools/gemm_check.py out0.npz; python tools/gemm_check.py out1.npz;
-python tools/gemm_check.py --compare out0.npz out1.npz"""
+python tools/gemm_check.py --compare out0.npz out1.npz.  A third argument f32 checks the fp32
+path (DENSOLVE_GEMM32_SMALL=1 selects the 64 x 64 kernel)."""
 import os
 import sys
 from ctypes import c_void_p
@@ -21,23 +22,26 @@ if sys.argv[1] == "--compare":
 from paper_1511_07207_b200 import _lib, get_backend  # noqa: E402
 from paper_1511_07207_b200.device import DeviceArray  # noqa: E402
 
+dt = np.float32 if len(sys.argv) > 2 and sys.argv[2] == "f32" else np.float64
+code = _lib.DS_F32 if dt == np.float32 else _lib.DS_F64
+tol = 1e-4 if dt == np.float32 else 1e-13
 be = get_backend("b200")
 ctx = be.ctx
 rng = np.random.default_rng(5)
 out = {}
 for (m, n, k) in SHAPES:
     for mode, (alpha, beta) in (("sub", (-1.0, 1.0)), ("gen", (0.75, -1.25))):
-        A = np.asfortranarray(rng.standard_normal((m, k)))
-        B = np.asfortranarray(rng.standard_normal((k, n)))
-        C = np.asfortranarray(rng.standard_normal((m, n)))
+        A = np.asfortranarray(rng.standard_normal((m, k)).astype(dt))
+        B = np.asfortranarray(rng.standard_normal((k, n)).astype(dt))
+        C = np.asfortranarray(rng.standard_normal((m, n)).astype(dt))
         dA, dB, dC = DeviceArray.from_host(A, ctx), DeviceArray.from_host(B, ctx), DeviceArray.from_host(C, ctx)
-        dO = DeviceArray(ctx, (m, n), np.float64)
-        _lib.check(ctx.lib.ds_gemm(ctx.handle, _lib.DS_F64, m, n, k, alpha, c_void_p(dA.ptr), dA.ld, c_void_p(dB.ptr),
+        dO = DeviceArray(ctx, (m, n), dt)
+        _lib.check(ctx.lib.ds_gemm(ctx.handle, code, m, n, k, alpha, c_void_p(dA.ptr), dA.ld, c_void_p(dB.ptr),
                                    dB.ld, beta, c_void_p(dC.ptr), dC.ld, c_void_p(dO.ptr), dO.ld))
         o = dO.to_host()
-        ref = beta * C + alpha * (A @ B)
-        err = np.abs(o - ref).max() / max(1.0, np.abs(ref).max())
-        assert err < 1e-13, (m, n, k, mode, err)
+        ref = beta * C.astype(np.float64) + alpha * (A.astype(np.float64) @ B.astype(np.float64))
+        err = np.abs(o - ref).max() / max(1.0, np.abs(ref).max()) / max(1.0, np.sqrt(k))
+        assert err < tol, (m, n, k, mode, err)
         out[f"{m}x{n}x{k}_{mode}"] = o
 np.savez(sys.argv[1], **out)
-print("saved", len(out), "results; all within 1e-13 of numpy")
+print("saved", len(out), "results; all within", tol, "(x sqrt k) of numpy fp64")

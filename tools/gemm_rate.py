@@ -13,14 +13,17 @@ ctx = be.ctx
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 ctx.set_stream(stream.cuda_stream)
+dt, code = torch.float64, _lib.DS_F64
+if os.environ.get("GEMM_RATE_F32") == "1":
+    dt, code = torch.float32, _lib.DS_F32
 n = int(sys.argv[1])
 for K in [int(v) for v in sys.argv[2:]]:
-    A = torch.rand((n, K), dtype=torch.float64, device="cuda")
-    B = torch.rand((K, n), dtype=torch.float64, device="cuda")
-    C = torch.rand((n, n), dtype=torch.float64, device="cuda")
+    A = torch.rand((n, K), dtype=dt, device="cuda")
+    B = torch.rand((K, n), dtype=dt, device="cuda")
+    C = torch.rand((n, n), dtype=dt, device="cuda")
 
     def gemm():
-        _lib.check(ctx.lib.ds_gemm(ctx.handle, _lib.DS_F64, n, n, K, -1.0, c_void_p(A.data_ptr()), n,
+        _lib.check(ctx.lib.ds_gemm(ctx.handle, code, n, n, K, -1.0, c_void_p(A.data_ptr()), n,
                                    c_void_p(B.data_ptr()), K, 1.0, c_void_p(C.data_ptr()), n,
                                    c_void_p(C.data_ptr()), n))
     gemm()
@@ -32,5 +35,5 @@ for K in [int(v) for v in sys.argv[2:]]:
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 5
-    print(f"GEMM {n}x{n}x{K}: {ms:.3f} ms  {2 * n * n * K / ms / 1e9:.2f} TFLOP/s", flush=True)
+    print(f"GEMM {dt} {n}x{n}x{K}: {ms:.3f} ms  {2 * n * n * K / ms / 1e9:.2f} TFLOP/s", flush=True)
     del A, B, C
