@@ -229,3 +229,38 @@ def test_stage_in_async_pipelined_solves(backend):
     for (A, b, _), x in zip(probs, outs):
         xs, _ = cg_solve(A, b, np.zeros_like(b), SolverConfig(tolerance=1e-10), backend)
         np.testing.assert_array_equal(x, xs)
+
+
+def test_gemm_concurrent_streams_bitwise():
+    """Two DMMA GEMMs running at the same time on two library contexts (two streams) give
+    the bits of the same GEMMs run one after the other (TMA stage-reuse ordering)."""
+    from ctypes import c_void_p
+
+    from paper_1511_07207_b200 import _lib
+    from paper_1511_07207_b200.device import DeviceArray
+
+    c1, c2 = _lib.Context(0), _lib.Context(0)
+    n, K = 4096, 512
+    rng = np.random.default_rng(11)
+    ops = []
+    for ctx in (c1, c2):
+        A = DeviceArray.from_host(np.asfortranarray(rng.random((n, K))), ctx)
+        B = DeviceArray.from_host(np.asfortranarray(rng.random((K, n))), ctx)
+        C = DeviceArray.from_host(np.asfortranarray(rng.random((n, n))), ctx)
+        ops.append((ctx, A, B, C))
+
+    def gemm(ctx, A, B, C, out):
+        _lib.check(ctx.lib.ds_gemm(ctx.handle, _lib.DS_F64, n, n, K, -1.0, c_void_p(A.ptr), A.ld, c_void_p(B.ptr),
+                                   B.ld, 1.0, c_void_p(C.ptr), C.ld, c_void_p(out.ptr), out.ld))
+
+    refs = []
+    for ctx, A, B, C in ops:
+        out = DeviceArray(ctx, (n, n), np.float64)
+        gemm(ctx, A, B, C, out)
+        refs.append(out.to_host())
+    outs = [DeviceArray(ctx, (n, n), np.float64) for ctx, *_ in ops]
+    for _ in range(40):
+        for (ctx, A, B, C), out in zip(ops, outs):
+            gemm(ctx, A, B, C, out)
+        for (ctx, *_), out, ref in zip(ops, outs, refs):
+            assert np.array_equal(out.to_host(), ref)
