@@ -227,6 +227,15 @@ int ds_shardset_gather(ds_shardset* ss, int dtype, const void* const* d_loc, voi
 int ds_cg_sharded(ds_shardset* ss, int dtype, void* const* d_A, int64_t lda, const void* const* d_b,
                   const void* const* d_x0, void* const* d_x, double tol, int64_t max_it, int check_sym,
                   double* h_hist, int64_t hist_cap, ds_solve_info* info);
+/* Row-sharded GMRES(m) (krylov.py:75-182), same layout and conventions as ds_cg_sharded:
+ * the v_k slices, the multi-dot records of each CGS pass and the norm records are
+ * all-gathered over the peer-memory regions; H, the Givens rotations, the estimates and the
+ * restart / stagnation / happy-breakdown decisions are replicated on every shard.
+ * restart_m <= 63.  h_cycles receives the restart cycle starts (SolveReport.restart_cycles). */
+int ds_gmres_sharded(ds_shardset* ss, int dtype, void* const* d_A, int64_t lda, const void* const* d_b,
+                     const void* const* d_x0, void* const* d_x, double tol, int64_t max_it, int64_t restart_m,
+                     int orth, double* h_hist, int64_t hist_cap, int64_t* h_cycles, int64_t cycles_cap,
+                     ds_solve_info* info);
 
 /* ---- input path: Matrix Market ingestion (host side) ------------------ */
 /* Replaces harness.read_matrix_market (harness.py:138-220).  Parses `path`

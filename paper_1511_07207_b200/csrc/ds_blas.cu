@@ -1574,7 +1574,12 @@ int preload_sharded_kernels_blas() {
       (const void*)ds_colstream_reduce_kernel<double, EPI_DOT>, (const void*)ds_colstream_reduce_kernel<float, EPI_DOT>,
       (const void*)ds_colstream_reduce_kernel<double, EPI_RESID>,
       (const void*)ds_colstream_reduce_kernel<float, EPI_RESID>,
-      (const void*)symcheck_kernel<double>, (const void*)symcheck_kernel<float>, (const void*)finish_max2_kernel};
+      (const void*)symcheck_kernel<double>, (const void*)symcheck_kernel<float>, (const void*)finish_max2_kernel,
+      // the row-sharded GMRES: r = b - A x, x += V y
+      (const void*)ds_colstream_reduce_kernel<double, EPI_STORE>, (const void*)ds_colstream_reduce_kernel<float, EPI_STORE>,
+      (const void*)ds_colstream_reduce_kernel<double, EPI_AXPY_INTO>,
+      (const void*)ds_colstream_reduce_kernel<float, EPI_AXPY_INTO>, (const void*)axpy_kernel<double>,
+      (const void*)axpy_kernel<float>};
   for (const void* f : fns) DS_CUDA(cudaFuncGetAttributes(&a, f));
   return DS_OK;
 }

@@ -377,7 +377,16 @@ int laswp_range(ds_ctx* ctx, T* W, int64_t ld, int64_t ncols, int64_t k0, int64_
 int preload_sharded_kernels_dist() {  // see preload_sharded_kernels_blas
   cudaFuncAttributes a;
   const void* fns[] = {(const void*)absdiff_t_kernel<double>, (const void*)absdiff_t_kernel<float>,
-                       (const void*)max2_finish_kernel};
+                       (const void*)max2_finish_kernel,
+                       // the row-sharded GMRES shard kernels
+                       (const void*)vec_parts_kernel<double>, (const void*)vec_parts_kernel<float>,
+                       (const void*)parts3_finish_kernel, (const void*)multidot_dev_kernel<double>,
+                       (const void*)multidot_dev_kernel<float>, (const void*)multidot_finish_kernel,
+                       (const void*)cgs_update_shard_kernel<double>, (const void*)cgs_update_shard_kernel<float>,
+                       (const void*)gm_shard_normalize_kernel<double>, (const void*)gm_shard_normalize_kernel<float>,
+                       (const void*)gm_shard_givens_kernel<double>, (const void*)gm_shard_givens_kernel<float>,
+                       (const void*)gm_shard_lsq_kernel<double>, (const void*)gm_shard_lsq_kernel<float>,
+                       (const void*)gm_shard_start_kernel<double>, (const void*)gm_shard_start_kernel<float>};
   for (const void* f : fns) DS_CUDA(cudaFuncGetAttributes(&a, f));
   return DS_OK;
 }

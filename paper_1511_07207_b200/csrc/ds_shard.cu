@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <condition_variable>
 #include <ctime>
 #include <mutex>
@@ -61,7 +62,13 @@ struct Peers {
   double* rec[kMaxShards];               // shard t's records [REC_KINDS][kMaxShards][kRecW]
   char* full[kMaxShards];                // shard t's gathered vector
   char* xbuf[kMaxShards];                // shard t's staging buffer
+  double* gr[kMaxShards];                // shard t's gather regions (GMRES records, rank-major)
 };
+
+// gather regions (doubles): two multi-dot record buffers (CGS pass parity) of G x kc and
+// one (s2, scale, ssq) record buffer of G x 3, each written at [rank * cnt ...] by every shard
+constexpr int GR_MD0 = 0, GR_MD1 = kMaxShards * 64, GR_P3 = 2 * kMaxShards * 64;
+constexpr size_t kGrBytes = (size_t)(2 * kMaxShards * 64 + kMaxShards * 4) * sizeof(double);
 
 __device__ __forceinline__ size_t rec_off(int kind, int src) {
   return ((size_t)kind * kMaxShards + src) * kRecW;
@@ -182,6 +189,19 @@ __global__ void __launch_bounds__(kShT) sh_put_slice_kernel(Peers P, int64_t n_l
     for (int t = 0; t < P.G; ++t) reinterpret_cast<T*>(P.full[t])[P.rank * n_loc + i] = x;
   }
   if (P.G > 1) __threadfence_system();
+}
+
+// a finalised local array (cnt doubles, device) into every shard's gather region at
+// [off + rank * cnt], then signal (the all-gather of the GMRES records)
+__global__ void sh_publish_array_kernel(Peers P, const double* __restrict__ src, int cnt, int off,
+                                        unsigned long long seq) {
+  for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+    const double v = src[j];
+    for (int t = 0; t < P.G; ++t) P.gr[t][off + P.rank * cnt + j] = v;
+  }
+  if (P.G > 1) __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) signal_peers(P, seq);
 }
 
 struct ShCg {
@@ -344,8 +364,11 @@ struct ShardLocal {
   int rank = 0;
   char* region = nullptr;  // cudaMalloc'd exchange region
   size_t region_bytes = 0;
+  void* sws = nullptr;     // the solver's own device buffers (grow-only, allocated before any exchange)
+  size_t sws_bytes = 0;
   unsigned long long* flag = nullptr;
   double* rec = nullptr;
+  double* gr = nullptr;
   char* full = nullptr;
   char* xbuf = nullptr;
   int* err = nullptr;  // watchdog word (in the region)
@@ -373,13 +396,14 @@ constexpr size_t kErrBytes = 256;
 size_t round256(size_t b) { return (b + 255) / 256 * 256; }
 
 struct Layout {
-  size_t flag, rec, err, full, xbuf, total;
+  size_t flag, rec, gr, err, full, xbuf, total;
 };
 Layout layout_of(const ds_shardset* s) {
   Layout L;
   L.flag = 0;
   L.rec = kFlagBytes;
-  L.err = L.rec + round256(kRecBytes);
+  L.gr = L.rec + round256(kRecBytes);
+  L.err = L.gr + round256(kGrBytes);
   L.full = L.err + kErrBytes;
   L.xbuf = L.full + round256((size_t)s->N * s->elem);
   L.total = L.xbuf + round256(std::max<size_t>(s->xbytes, 256));
@@ -389,6 +413,7 @@ Layout layout_of(const ds_shardset* s) {
 void bind_region(ShardLocal& S, const Layout& L, char* base) {
   S.flag = reinterpret_cast<unsigned long long*>(base + L.flag);
   S.rec = reinterpret_cast<double*>(base + L.rec);
+  S.gr = reinterpret_cast<double*>(base + L.gr);
   S.err = reinterpret_cast<int*>(base + L.err);
   S.full = base + L.full;
   S.xbuf = base + L.xbuf;
@@ -677,6 +702,271 @@ int sh_cg_run(ShardLocal& S, ds_shardset* ss, const T* A, int64_t lda, const T* 
   return DS_OK;
 }
 
+// ---- row-sharded GMRES(m) (krylov.py:75-182) ------------------------------------
+// The host logic of distributed.gmres_solve_sharded in C++: every exchange is an
+// all-gather over the peer-memory regions (v_k slices into `full`, multi-dot records per
+// CGS pass, (s2, scale, ssq) norm records), the per-shard compute is the ds_dist.cu shard
+// kernels.  All shards hold identical H, Givens rotations, estimates and stop decisions.
+void combine3_host(const double* parts, int G, double* s2_out, double* nrm_out) {
+  double s2 = 0.0, scale = 0.0, ssq = 0.0;  // rank-ordered, as the device combine3
+  for (int q = 0; q < G; ++q) {
+    s2 += parts[3 * q];
+    const double bs = parts[3 * q + 1], bq = parts[3 * q + 2];
+    if (scale != scale) continue;
+    if (bs != bs) {
+      scale = bs;
+      ssq = bq;
+      continue;
+    }
+    if (std::isinf(scale) || std::isinf(bs)) {
+      scale = INFINITY;
+      ssq = 1.0;
+      continue;
+    }
+    if (bs == 0.0) continue;
+    if (scale == 0.0) {
+      scale = bs;
+      ssq = bq;
+      continue;
+    }
+    if (scale >= bs) {
+      const double r = bs / scale;
+      ssq = ssq + bq * r * r;
+    } else {
+      const double r = scale / bs;
+      const double ns = bq + ssq * r * r;
+      scale = bs;
+      ssq = ns;
+    }
+  }
+  *s2_out = s2;
+  *nrm_out = (scale == 0.0 || !(scale - scale == 0.0)) ? scale : scale * std::sqrt(ssq);
+}
+
+enum { GST_RS = 0, GST_BNORM = 1, GST_STATUS = 2, GST_STOP = 3, GST_BAD = 4, GST_RES = 5 };
+
+template <typename T>
+int sh_gmres_run(ShardLocal& S, ds_shardset* ss, const T* A, int64_t lda, const T* b, const T* x0, T* x, double tol,
+                 int64_t cap, int64_t m, int orth, double* h_hist, int64_t hist_cap, int64_t* h_cycles,
+                 int64_t cycles_cap, ds_solve_info* info, HostBarrier* allocated) {
+  ds_ctx* ctx = S.ctx;
+  const int64_t launches0 = ctx->launches;
+  const int G = ss->G;
+  const int64_t n = ss->n, nl = ss->n_loc;
+  const int dt = sizeof(T) == 8 ? DS_F64 : DS_F32;
+  const double u = (sizeof(T) == 8 ? 1.1102230246251565e-16 : 5.960464477539063e-08);
+  const int passes = orth == DS_ORTH_CLASSICAL ? 1 : 2;
+  // scratch of the ds_* shard entry points (the context workspace, reused from offset 0 by
+  // each call) and this solver's own buffers: both sized here, before any exchange
+  const GemvPlan gp = gemv_plan(ctx, nl, n, sizeof(T));
+  const int vg = vgrid(ctx, nl);
+  const size_t ws_need = std::max<size_t>(gp.part_bytes + 4096, ((size_t)vg * 64 + 64) * sizeof(double) + 4096);
+  const int64_t ldv = ceil_div(std::max<int64_t>(nl, 1), 4) * 4;
+  const int64_t ldh = m + 1;
+  size_t need = 0;
+  need += 256 + (size_t)ldv * (m + 1) * sizeof(T);      // V
+  need += 256 + (size_t)ldh * m * sizeof(T) * 2;        // H, Hraw
+  need += 256 + (size_t)(m + 2) * sizeof(T) * 3;        // g, cs, sn
+  need += 256 + 64 * sizeof(T);                         // y
+  need += 256 + (size_t)nl * sizeof(T);                 // r
+  need += 256 + (64 + 64 + 16 + 64) * sizeof(double);   // hsave, est, state, md (local records)
+  int ast = DS_OK;
+  void* ws = nullptr;
+  ast = ctx_workspace(ctx, ws_need, &ws);
+  if (ast == DS_OK && need > S.sws_bytes) {
+    if (S.sws) cudaFree(S.sws);
+    S.sws = nullptr;
+    S.sws_bytes = 0;
+    if (cudaMalloc(&S.sws, need) == cudaSuccess)
+      S.sws_bytes = need;
+    else
+      ast = DS_ENOMEM;
+  }
+  double* h_st = nullptr;
+  if (ast == DS_OK) ast = ctx_hostbuf(ctx, 64 * sizeof(double) + kMaxShards * 3 * sizeof(double), (void**)&h_st);
+  if (allocated) allocated->arrive_and_wait();
+  if (ast != DS_OK) {
+    ss->broken = true;
+    if (ast == DS_ENOMEM) set_error("sharded GMRES: device buffers (%zu bytes) could not be allocated", need);
+    return ast;
+  }
+  DS_CUDA(cudaMemsetAsync(S.err, 0, kErrBytes, ctx->stream));
+  Carver cv{(char*)S.sws};
+  T* V = cv.take<T>((size_t)ldv * (m + 1) * sizeof(T));
+  T* H = cv.take<T>((size_t)ldh * m * sizeof(T));
+  T* Hraw = cv.take<T>((size_t)ldh * m * sizeof(T));
+  T* g = cv.take<T>((size_t)(m + 2) * sizeof(T));
+  T* cs = cv.take<T>((size_t)(m + 2) * sizeof(T));
+  T* sn = cv.take<T>((size_t)(m + 2) * sizeof(T));
+  T* y = cv.take<T>(64 * sizeof(T));
+  T* r = cv.take<T>((size_t)nl * sizeof(T));
+  double* hsave = cv.take<double>(64 * sizeof(double));
+  double* est = cv.take<double>(64 * sizeof(double));
+  double* st = cv.take<double>(16 * sizeof(double));
+  double* md = cv.take<double>(64 * sizeof(double));  // this shard's multi-dot record / (s2, scale, ssq)
+  T* full = reinterpret_cast<T*>(S.full);
+  double* p3_all = S.gr + GR_P3;
+  double* h_p3 = h_st + 64;
+
+  auto gather_vec = [&](const T* v) -> int {  // v (n_loc) -> every shard's full
+    sh_put_slice_kernel<T><<<vg, kShT, 0, ctx->stream>>>(S.peers, nl, v);
+    count_launch(ctx);
+    DS_CHECK_LAUNCH();
+    DS_TRY(sh_signal(S, ss));
+    return sh_wait(S, ss);
+  };
+  auto publish = [&](const double* src, int cnt, int off) -> int {
+    ++S.seq;
+    sh_publish_array_kernel<<<1, 64, 0, ctx->stream>>>(S.peers, src, cnt, off, S.seq);
+    count_launch(ctx);
+    DS_CHECK_LAUNCH();
+    return sh_wait(S, ss);
+  };
+  auto read_p3 = [&](double* s2, double* nrm) -> int {  // the G (s2, scale, ssq) records, host-combined
+    DS_CUDA(cudaMemcpyAsync(h_p3, p3_all, (size_t)G * 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    DS_CUDA(cudaStreamSynchronize(ctx->stream));
+    DS_TRY(check_watchdog(S));
+    combine3_host(h_p3, G, s2, nrm);
+    return DS_OK;
+  };
+  auto residual = [&](double* s2, double* nrm) -> int {  // r = b - A x (krylov.py:104), its record
+    DS_TRY(gather_vec(x));
+    DS_TRY(ds_resid_parts(ctx, dt, nl, n, A, lda, full, b, r, md));
+    DS_TRY(publish(md, 3, GR_P3));
+    return read_p3(s2, nrm);
+  };
+
+  // ||b|| (krylov.py:87 -> _rhs_norm)
+  DS_TRY(ds_vec_parts(ctx, dt, nl, b, md));
+  DS_TRY(publish(md, 3, GR_P3));
+  double s2b = 0.0, bnorm = 0.0;
+  DS_TRY(read_p3(&s2b, &bnorm));
+  if (bnorm == 0.0) {
+    set_error("||b|| = 0");
+    return DS_EDEGRHS;
+  }
+  const double bnorm_plain = std::sqrt(s2b);
+  if (x != x0) DS_CUDA(cudaMemcpyAsync(x, x0, nl * sizeof(T), cudaMemcpyDeviceToDevice, ctx->stream));
+  {
+    double h0[8] = {0, bnorm, 0, 0, 0, 0, 0, 0};
+    DS_CUDA(cudaMemcpyAsync(st, h0, sizeof h0, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  std::vector<double> history;
+  std::vector<int64_t> cycles;
+  int64_t total = 0, resid_evals = 0;
+  int breakdown = DS_BREAKDOWN_NONE;
+  bool converged = false;
+  const size_t vbytes = (size_t)ldv * (m + 1) * sizeof(T), hbytes = (size_t)ldh * m * sizeof(T);
+  while (true) {
+    double s2r = 0.0, beta = 0.0;
+    DS_TRY(residual(&s2r, &beta));
+    ++resid_evals;
+    const double relres = beta / bnorm;
+    if (total == 0) history.push_back(relres);
+    if (relres <= tol) {
+      converged = true;
+      break;
+    }
+    if (total >= cap) break;
+    cycles.push_back(total);
+    const double start_res = relres;
+    DS_CUDA(cudaMemsetAsync(V, 0, vbytes, ctx->stream));
+    DS_CUDA(cudaMemsetAsync(H, 0, hbytes, ctx->stream));
+    DS_CUDA(cudaMemsetAsync(Hraw, 0, hbytes, ctx->stream));
+    DS_CUDA(cudaMemsetAsync(g, 0, (size_t)(m + 2) * sizeof(T), ctx->stream));
+    DS_CUDA(cudaMemsetAsync(cs, 0, (size_t)(m + 2) * sizeof(T), ctx->stream));
+    DS_CUDA(cudaMemsetAsync(sn, 0, (size_t)(m + 2) * sizeof(T), ctx->stream));
+    {
+      const double hs[3] = {0.0, (double)m, 0.0};  // status, stop, happy
+      DS_CUDA(cudaMemcpyAsync(st + GST_STATUS, hs, sizeof hs, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    DS_TRY(ds_gmres_shard_start(ctx, dt, nl, r, V, G, p3_all, g, st));
+    int64_t k = 0, chunk = 4;
+    while (true) {
+      if (k > 0) {
+        DS_CUDA(cudaMemcpyAsync(h_st, st, 8 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        DS_CUDA(cudaStreamSynchronize(ctx->stream));
+        DS_TRY(check_watchdog(S));
+        if (h_st[GST_STOP] <= (double)k || k >= m) break;
+      }
+      const int64_t kend = std::min<int64_t>(m, k + chunk);
+      for (; k < kend; ++k) {
+        T* vk = V + k * ldv;
+        T* w = V + (k + 1) * ldv;
+        DS_TRY(gather_vec(vk));
+        DS_TRY(ds_gemv(ctx, dt, nl, n, A, lda, full, w));
+        const int kc = (int)(k + 1);
+        for (int ps = 0; ps < passes; ++ps) {
+          const int off = ps == 0 ? GR_MD0 : GR_MD1;
+          DS_TRY(ds_multidot_dev(ctx, dt, nl, V, ldv, kc, w, md));
+          DS_TRY(publish(md, kc, off));
+          DS_TRY(ds_cgs_update_shard(ctx, dt, nl, V, ldv, kc, w, G, S.gr + off, H + k * ldh, hsave, ps, md, st,
+                                     k));
+        }
+        DS_TRY(publish(md, 3, GR_P3));
+        DS_TRY(ds_gmres_shard_step(ctx, dt, nl, w, G, p3_all, H, Hraw, ldh, g, cs, sn, (int)k, est, st, tol, total,
+                                   cap));
+      }
+      chunk = std::min<int64_t>(2 * chunk, 32);
+    }
+    DS_CUDA(cudaMemcpyAsync(h_st, st, 8 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    DS_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int64_t inner = std::min<int64_t>((int64_t)h_st[GST_STOP], m);
+    const bool happy = h_st[GST_BAD] != 0.0;
+    {
+      std::vector<double> e((size_t)std::max<int64_t>(inner, 1));
+      if (inner > 0) {
+        DS_CUDA(cudaMemcpyAsync(e.data(), est, inner * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        DS_CUDA(cudaStreamSynchronize(ctx->stream));
+      }
+      for (int64_t i = 0; i < inner; ++i) history.push_back(e[i]);
+    }
+    total += inner;
+    DS_TRY(ds_gmres_lsq(ctx, dt, H, ldh, g, (int)inner, y, st));
+    DS_CUDA(cudaMemcpyAsync(h_st, st, 8 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    DS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h_st[GST_STATUS] == (double)DS_ESINGULAR) {
+      set_error("zero diagonal at row %lld", (long long)h_st[GST_RES]);
+      info->error_index = (int64_t)h_st[GST_RES];
+      return DS_ESINGULAR;
+    }
+    if (inner > 0) DS_TRY(ds_gemv_acc(ctx, dt, nl, inner, V, ldv, y, x));  // x += V y (krylov.py:167)
+    double s2t = 0.0, nt = 0.0;
+    DS_TRY(residual(&s2t, &nt));
+    ++resid_evals;
+    const double true_res = std::sqrt(s2t) / bnorm_plain;
+    if (happy || history.back() <= tol || true_res <= tol) {
+      history.back() = true_res;
+      if (true_res <= tol || happy) {
+        converged = true;
+        if (happy) breakdown = DS_BREAKDOWN_HAPPY;
+        break;
+      }
+    }
+    if (total >= cap) {
+      history.back() = true_res;
+      break;
+    }
+    if (inner == m && true_res >= start_res * (1.0 - u)) {  // stagnation (krylov.py:177-180)
+      history.back() = true_res;
+      break;
+    }
+  }
+  const int64_t hl = std::min<int64_t>((int64_t)history.size(), hist_cap);
+  if (h_hist) std::copy(history.begin(), history.begin() + hl, h_hist);
+  const int64_t cl = std::min<int64_t>((int64_t)cycles.size(), cycles_cap);
+  if (h_cycles) std::copy(cycles.begin(), cycles.begin() + cl, h_cycles);
+  info->iterations = total;
+  info->history_len = hl;
+  info->cycles_len = cl;
+  info->final_relative_residual = history.back();
+  info->converged = converged;
+  info->breakdown = breakdown;
+  info->residual_evals = resid_evals;
+  info->kernel_launches = ctx->launches - launches0;
+  return DS_OK;
+}
+
 // run fn(i) for every local shard: inline for one, one host thread per shard otherwise;
 // the first failing shard's status and message are returned
 template <typename F>
@@ -719,7 +1009,8 @@ void shard_kernel_list(std::vector<const void*>& f) {
 }
 int preload_kernels() {
   std::vector<const void*> f = {(const void*)sh_wait_kernel, (const void*)sh_signal_kernel,
-                                (const void*)sh_publish2_kernel, (const void*)sh_cg_init_kernel};
+                                (const void*)sh_publish2_kernel, (const void*)sh_cg_init_kernel,
+                                (const void*)sh_publish_array_kernel};
   shard_kernel_list<double>(f);
   shard_kernel_list<float>(f);
   cudaFuncAttributes a;
@@ -739,6 +1030,7 @@ int connect_peers(ds_shardset* ss, const std::vector<char*>& bases) {
       S.peers.rec[t] = reinterpret_cast<double*>(b + L.rec);
       S.peers.full[t] = b + L.full;
       S.peers.xbuf[t] = b + L.xbuf;
+      S.peers.gr[t] = reinterpret_cast<double*>(b + L.gr);
     }
   }
   ss->connected = true;
@@ -887,6 +1179,7 @@ int ds_shardset_destroy(ds_shardset* ss) {
     cudaStreamSynchronize(S.ctx->stream);
     for (void* p : S.opened) cudaIpcCloseMemHandle(p);
     if (S.region) cudaFree(S.region);
+    if (S.sws) cudaFree(S.sws);
   }
   delete ss;
   return DS_OK;
@@ -918,6 +1211,58 @@ int ds_shardset_gather(ds_shardset* ss, int dtype, const void* const* d_loc, voi
     DS_CUDA(cudaStreamSynchronize(S.ctx->stream));
     return check_watchdog(S);
   });
+  if (st == DS_ECUDA) ss->broken = true;
+  return st;
+}
+
+int ds_gmres_sharded(ds_shardset* ss, int dtype, void* const* d_A, int64_t lda, const void* const* d_b,
+                     const void* const* d_x0, void* const* d_x, double tol, int64_t max_it, int64_t restart_m,
+                     int orth, double* h_hist, int64_t hist_cap, int64_t* h_cycles, int64_t cycles_cap,
+                     ds_solve_info* info) {
+  if (!ss || !ss->connected) {
+    set_error("shard set is not connected");
+    return DS_EINVAL;
+  }
+  if (ss->broken) {
+    set_error("shard set is unusable after an earlier failed exchange; create a new one");
+    return DS_ECUDA;
+  }
+  if (dtype_size(dtype) != ss->elem) {
+    set_error("dtype does not match the shard set");
+    return DS_EPREC;
+  }
+  if (!(tol > 0) || max_it < 1 || restart_m < 1 || lda < ss->n_loc ||
+      (orth != DS_ORTH_MODIFIED && orth != DS_ORTH_CLASSICAL)) {
+    set_error("invalid sharded GMRES configuration");
+    return DS_EINVAL;
+  }
+  if (restart_m > 63) {  // the shard kernels keep one Hessenberg column (<= 64 entries) in shared memory
+    set_error("restart_m = %lld exceeds the sharded GMRES limit of 63", (long long)restart_m);
+    return DS_EINVAL;
+  }
+  const int L = (int)ss->loc.size();
+  std::vector<ds_solve_info> infos(L);
+  HostBarrier allocated(L);
+  const int st = for_each_local(ss, [&](int i) -> int {
+    ShardLocal& S = ss->loc[i];
+    const int e = ctx_begin(S.ctx);
+    if (e != DS_OK) {
+      allocated.arrive_and_wait();
+      return e;
+    }
+    std::lock_guard<std::recursive_mutex> guard(S.ctx->mu);
+    infos[i] = ds_solve_info{};
+    infos[i].error_index = -1;
+    const bool first = i == 0;
+    if (dtype == DS_F64)
+      return sh_gmres_run<double>(S, ss, (const double*)d_A[i], lda, (const double*)d_b[i], (const double*)d_x0[i],
+                                  (double*)d_x[i], tol, max_it, restart_m, orth, first ? h_hist : nullptr, hist_cap,
+                                  first ? h_cycles : nullptr, cycles_cap, &infos[i], &allocated);
+    return sh_gmres_run<float>(S, ss, (const float*)d_A[i], lda, (const float*)d_b[i], (const float*)d_x0[i],
+                               (float*)d_x[i], tol, max_it, restart_m, orth, first ? h_hist : nullptr, hist_cap,
+                               first ? h_cycles : nullptr, cycles_cap, &infos[i], &allocated);
+  });
+  *info = infos[0];
   if (st == DS_ECUDA) ss->broken = true;
   return st;
 }

@@ -111,8 +111,8 @@ def gmres_solve(A, b, x0, cfg: SolverConfig, backend=None, workspace_sink: list 
         if workspace_sink is not None:
             raise ValueError("workspace_sink is not supported by the sharded backend (V lives in row shards)")
         be.tally("nrm2", 2 * n)
-        x, report = gmres_solve_rows(A, b, x0, cfg, be)
-        _tally_gmres(be, n, report, len(report.restart_cycles or []) + 1)
+        x, report, info = gmres_solve_rows(A, b, x0, cfg, be)
+        _tally_gmres(be, n, report, int(info.residual_evals))
         report.wall_time = time.perf_counter() - t0
         return x, report
     ctx = be.ctx

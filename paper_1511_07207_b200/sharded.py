@@ -403,34 +403,44 @@ def _row_block_tensor(A: np.ndarray, r0: int, r1: int, n_loc: int, dev, torch):
 
 
 def gmres_solve_rows(A, b, x0, cfg, be: ShardedB200Backend):
-    """krylov.gmres_solve (krylov.py:75-182) with A split by rows over the backend's
-    shards (distributed.gmres_solve_sharded per shard)."""
-    import torch
+    """krylov.gmres_solve (krylov.py:75-182) with A split by rows over the backend's shards:
+    ds_gmres_sharded runs the restarted Arnoldi loop in the library (the v_k slices, the
+    multi-dot records of each CGS pass and the norm records all-gathered over peer memory)."""
+    from .core import SingularMatrixError, SolveReport
 
-    from . import distributed as D
-
-    A, b, x0 = np.asarray(A), np.asarray(b), np.asarray(x0)
     n = A.shape[0]
-    G = be.nshards
-    n_loc, N = D.row_partition(n, G)
-
-    def work(q, size, comm, ops, dev):
-        r0, r1 = q * n_loc, min(n, (q + 1) * n_loc)
-        A_blk = _row_block_tensor(A, r0, r1, n_loc, dev, torch)
-        tdt = A_blk.dtype
-        b_loc = torch.zeros(n_loc, dtype=tdt, device=dev)
-        x_loc = torch.zeros(n_loc, dtype=tdt, device=dev)
-        if r1 > r0:
-            b_loc[: r1 - r0] = torch.from_numpy(b[r0:r1]).to(dev)
-            x_loc[: r1 - r0] = torch.from_numpy(x0[r0:r1]).to(dev)
-        x, rep = D.gmres_solve_sharded(A_blk, b_loc, x_loc, n, cfg, comm, ops)
-        full = torch.empty(N, dtype=tdt, device=dev)
-        comm.allgather(full, x)
-        return full[:n].cpu().numpy(), rep
-
-    res = _run_local_shards(be, work)
-    x, rep = res[0]
-    return x.astype(A.dtype, copy=False), rep
+    m = int(cfg.restart_m)
+    if m > 63:
+        raise ValueError(f"restart_m = {m} exceeds the sharded GMRES limit of 63 (use the single-GPU backend)")
+    dA = be._stage(A)
+    ss = dA.sset
+    db = b if is_sharded(b) else be.shard_vector(np.asarray(b), ss)
+    dx0 = x0 if is_sharded(x0) else be.shard_vector(np.asarray(x0), ss)
+    for v in (db, dx0):
+        if v.sset is not ss:
+            raise ValueError("sharded operands belong to different shard sets")
+    dx = be.empty_vector(ss)
+    cap = int(cfg.iteration_cap(n))
+    hist = np.empty(cap + 2, dtype=np.float64)
+    cycles = np.empty(cap + 2, dtype=np.int64)
+    info = _lib.SolveInfo()
+    orth = _lib.DS_ORTH_CLASSICAL if cfg.orthogonalization == "classical" else _lib.DS_ORTH_MODIFIED
+    st = be.ctx.lib.ds_gmres_sharded(ss.handle, ss.dcode, _ptr_array([d.ptr for d in dA.blocks]), dA.blocks[0].ld,
+                                     _ptr_array([d.ptr for d in db.parts]), _ptr_array([d.ptr for d in dx0.parts]),
+                                     _ptr_array([d.ptr for d in dx.parts]), float(cfg.tolerance), cap, m, orth,
+                                     hist.ctypes.data_as(c_void_p), cap + 2, cycles.ctypes.data_as(c_void_p),
+                                     cap + 2, ctypes.byref(info))
+    if st == _lib.DS_ESINGULAR:
+        raise SingularMatrixError(_lib.last_error())
+    _lib.check(st)
+    report = SolveReport(converged=bool(info.converged), iterations=int(info.iterations),
+                         final_relative_residual=float(info.final_relative_residual),
+                         residual_history=hist[: info.history_len].tolist(),
+                         breakdown="happy-breakdown" if info.breakdown == _lib.DS_BREAKDOWN_HAPPY else None,
+                         restart_cycles=cycles[: info.cycles_len].tolist())
+    report.kernel_launches = int(info.kernel_launches)
+    x = dx if is_sharded(x0) else dx.to_host()
+    return x, report, info
 
 
 def lu_factor_block_cyclic_api(A, b: int, be: ShardedB200Backend):

@@ -116,11 +116,14 @@ def _dist_worker(rank, world, port, q):
         A, b = _spd(301, 9)  # same host arrays on every rank (the reference call)
         be = get_backend("b200", distributed=True, device=0)
         x, rep = cg_solve(A, b, np.zeros_like(b), SolverConfig(tolerance=1e-10), be)
-        q.put((rank, x, rep.iterations, rep.residual_history))
+        from paper_1511_07207_b200 import gmres_solve
+        An, bn, _ = O.generate_problem("general_nonsymmetric", 301, 4)
+        xg, repg = gmres_solve(An, bn, np.zeros_like(bn), SolverConfig(tolerance=1e-10, restart_m=8), be)
+        q.put((rank, x, rep.iterations, rep.residual_history, xg, repg.iterations))
         dist.barrier()
         dist.destroy_process_group()
     except Exception:
-        q.put((rank, traceback.format_exc(), None, None))
+        q.put((rank, traceback.format_exc(), None, None, None, None))
 
 
 def test_distributed_cg_two_processes_ipc():
@@ -137,29 +140,59 @@ def test_distributed_cg_two_processes_ipc():
     res = [q.get(timeout=300) for _ in procs]
     for p in procs:
         p.join(60)
-    for r, x, it, h in res:
+    for r, x, it, h, _, _ in res:
         assert it is not None, x
     A, b = _spd(301, 9)
     xo, ro = O.cg(A, b, np.zeros_like(b), 1e-10)
-    (_, xa, ia, ha), (_, xb, ib, hb) = sorted(res, key=lambda t: t[0])
+    (_, xa, ia, ha, ga, gia), (_, xb, ib, hb, gb, gib) = sorted(res, key=lambda t: t[0])
     assert ia == ib and ha == hb and np.array_equal(xa, xb)  # replicated decisions
     assert abs(ia - ro["iterations"]) <= 1
     assert np.linalg.norm(xa - xo, np.inf) <= 1e-9 * np.linalg.norm(xo, np.inf)
+    An, bn, _ = O.generate_problem("general_nonsymmetric", 301, 4)
+    xgo, rgo = O.gmres(An, bn, np.zeros_like(bn), 1e-10, 8)
+    assert gia == gib and np.array_equal(ga, gb)
+    assert abs(gia - rgo["iterations"]) <= 1
+    assert np.linalg.norm(ga - xgo, np.inf) <= 1e-8 * np.linalg.norm(xgo, np.inf)
 
 
-@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0]])
-def test_sharded_gmres_matches_oracle(devices):
-    """krylov.gmres_solve with A split by rows (distributed.gmres_solve_sharded per shard,
-    one thread per shard, ThreadComm collectives)."""
+@pytest.mark.parametrize("devices,m,orth", [([0], 20, "modified"), ([0, 0], 20, "modified"),
+                                            ([0, 0, 0], 5, "modified"), ([0, 0], 7, "classical")])
+def test_sharded_gmres_matches_oracle(devices, m, orth):
+    """krylov.gmres_solve with A split by rows: ds_gmres_sharded (the Arnoldi loop in the
+    library, records all-gathered over peer memory) against the oracle, restarts included."""
     from paper_1511_07207_b200 import SolverConfig, get_backend, gmres_solve
 
     A, b, _ = O.generate_problem("general_nonsymmetric", 301, 4)
     be = get_backend("b200", devices=devices)
-    x, rep = gmres_solve(A, b, np.zeros_like(b), SolverConfig(tolerance=1e-10, restart_m=20), be)
-    xo, ro = O.gmres(A, b, np.zeros_like(b), 1e-10, 20)
-    assert rep.converged
+    cfg = SolverConfig(tolerance=1e-10, restart_m=m, orthogonalization=orth)
+    x, rep = gmres_solve(A, b, np.zeros_like(b), cfg, be)
+    xo, ro = O.gmres(A, b, np.zeros_like(b), 1e-10, m, orth=orth)
+    assert rep.converged and ro["converged"]
     assert abs(rep.iterations - ro["iterations"]) <= 1
+    k = min(len(rep.residual_history), len(ro["history"])) - 1
+    np.testing.assert_allclose(rep.residual_history[:k], ro["history"][:k], rtol=1e-6)
+    if rep.iterations == ro["iterations"]:
+        assert rep.restart_cycles == ro["cycles"]
     assert np.linalg.norm(x - xo, np.inf) <= 1e-8 * np.linalg.norm(xo, np.inf)
+    # the single-GPU solver agrees too
+    x1, rep1 = gmres_solve(A, b, np.zeros_like(b), cfg, get_backend("b200"))
+    assert abs(rep.iterations - rep1.iterations) <= 1
+
+
+def test_sharded_gmres_fp32_and_errors():
+    from paper_1511_07207_b200 import DegenerateRhsError, SolverConfig, get_backend, gmres_solve
+
+    A, b, _ = O.generate_problem("general_nonsymmetric", 200, 6)
+    A32, b32 = np.asfortranarray(A.astype(np.float32)), b.astype(np.float32)
+    be = get_backend("b200", devices=[0, 0])
+    x, rep = gmres_solve(A32, b32, np.zeros_like(b32), SolverConfig(tolerance=1e-5, restart_m=30), be)
+    xo, ro = O.gmres(A32, b32, np.zeros_like(b32), 1e-5, 30)
+    assert x.dtype == np.float32 and rep.converged
+    assert abs(rep.iterations - ro["iterations"]) <= 1
+    with pytest.raises(DegenerateRhsError):
+        gmres_solve(A, np.zeros_like(b), np.zeros_like(b), SolverConfig(tolerance=1e-8), be)
+    with pytest.raises(ValueError):
+        gmres_solve(A, b, np.zeros_like(b), SolverConfig(tolerance=1e-8, restart_m=64), be)
 
 
 @pytest.mark.parametrize("devices,n,b", [([0], 300, 64), ([0, 0], 600, 64), ([0, 0, 0], 777, 32)])
