@@ -769,7 +769,7 @@ int sh_gmres_run(ShardLocal& S, ds_shardset* ss, const T* A, int64_t lda, const 
   need += 256 + (size_t)(m + 2) * sizeof(T) * 3;        // g, cs, sn
   need += 256 + 64 * sizeof(T);                         // y
   need += 256 + (size_t)nl * sizeof(T);                 // r
-  need += 256 + (64 + 64 + 16 + 64) * sizeof(double);   // hsave, est, state, md (local records)
+  need += 256 + (64 + 64 + 16 + 64) * sizeof(double);   // hsave, est, state (16: ST_* + int64 stop mirror), md
   int ast = DS_OK;
   void* ws = nullptr;
   ast = ctx_workspace(ctx, ws_need, &ws);
@@ -879,9 +879,14 @@ int sh_gmres_run(ShardLocal& S, ds_shardset* ss, const T* A, int64_t lda, const 
     {
       const double hs[3] = {0.0, (double)m, 0.0};  // status, stop, happy
       DS_CUDA(cudaMemcpyAsync(st + GST_STATUS, hs, sizeof hs, cudaMemcpyHostToDevice, ctx->stream));
+      const int64_t stop64 = m;  // the GEMVs' Gate word (int64 mirror of the stop, slot 8)
+      DS_CUDA(cudaMemcpyAsync(st + 8, &stop64, sizeof stop64, cudaMemcpyHostToDevice, ctx->stream));
     }
     DS_TRY(ds_gmres_shard_start(ctx, dt, nl, r, V, G, p3_all, g, st));
-    int64_t k = 0, chunk = 4;
+    // all m steps enqueued at once behind the replicated stop word: after a stop the
+    // GEMVs are gated (Gate on the int64 mirror), the rest are tiny; one sync per cycle
+    int64_t k = 0, chunk = m;
+    const int64_t* stop64 = reinterpret_cast<const int64_t*>(st + 8);
     while (true) {
       if (k > 0) {
         DS_CUDA(cudaMemcpyAsync(h_st, st, 8 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -894,7 +899,8 @@ int sh_gmres_run(ShardLocal& S, ds_shardset* ss, const T* A, int64_t lda, const 
         T* vk = V + k * ldv;
         T* w = V + (k + 1) * ldv;
         DS_TRY(gather_vec(vk));
-        DS_TRY(ds_gemv(ctx, dt, nl, n, A, lda, full, w));
+        DS_TRY(gemv_launch<T>(ctx, gp, A, lda, full, w, static_cast<double*>(ws), EPI_STORE, nullptr, nullptr,
+                              nullptr, Gate{stop64, k}));
         const int kc = (int)(k + 1);
         for (int ps = 0; ps < passes; ++ps) {
           const int off = ps == 0 ? GR_MD0 : GR_MD1;
@@ -1235,6 +1241,13 @@ int ds_gmres_sharded(ds_shardset* ss, int dtype, void* const* d_A, int64_t lda, 
       (orth != DS_ORTH_MODIFIED && orth != DS_ORTH_CLASSICAL)) {
     set_error("invalid sharded GMRES configuration");
     return DS_EINVAL;
+  }
+  if (ss->G == 1) {
+    // one shard holds every row: there is nothing to exchange, and the single-GPU solver's
+    // fused step (GEMV + one-cluster orthogonalisation chained by PDL) is the same
+    // arithmetic with fewer launches than the shard kernels
+    return ds_gmres(ss->loc[0].ctx, dtype, ss->n, d_A[0], lda, d_b[0], d_x0[0], d_x[0], tol, max_it, restart_m,
+                    orth, h_hist, hist_cap, h_cycles, cycles_cap, nullptr, nullptr, info);
   }
   if (restart_m > 63) {  // the shard kernels keep one Hessenberg column (<= 64 entries) in shared memory
     set_error("restart_m = %lld exceeds the sharded GMRES limit of 63", (long long)restart_m);

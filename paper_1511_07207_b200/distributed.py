@@ -336,7 +336,7 @@ def cg_solve_sharded(A_blk, b_loc, x0_loc, n: int, cfg: SolverConfig, comm, ops,
     return x, rep
 
 
-_STATE = 8
+_STATE = 16  # the shard kernels keep an int64 mirror of the stop word at slot 8
 
 
 # ---------------------------------------------------------------------------

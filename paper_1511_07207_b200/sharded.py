@@ -410,7 +410,7 @@ def gmres_solve_rows(A, b, x0, cfg, be: ShardedB200Backend):
 
     n = A.shape[0]
     m = int(cfg.restart_m)
-    if m > 63:
+    if m > 63 and be.nshards > 1:
         raise ValueError(f"restart_m = {m} exceeds the sharded GMRES limit of 63 (use the single-GPU backend)")
     dA = be._stage(A)
     ss = dA.sset

@@ -40,8 +40,12 @@ def test_cg_matches_reference_golden(backend, golden, name):
     h_ref = golden[f"cg_{name}_hist"]
     k = min(len(h_ref), len(rep.residual_history))
     rt = 1e-6 if prec == "f64" else 1e-2
-    if name != "fixed":  # the fixed-iteration run walks into round-off where histories diverge
+    if name != "fixed":
         np.testing.assert_allclose(rep.residual_history[:k], h_ref[:k], rtol=rt)
+    else:  # the fixed-iteration run walks into round-off: compared while above 1e-12
+        kk = int(np.argmax(np.asarray(h_ref[:k]) < 1e-12)) or k
+        assert kk >= 10
+        np.testing.assert_allclose(rep.residual_history[:kk], h_ref[:kk], rtol=1e-5)
     xr = golden[f"cg_{name}_x"]
     xt = 1e-9 if prec == "f64" else 1e-3
     assert np.linalg.norm(x - xr, np.inf) <= xt * np.linalg.norm(xr, np.inf)
@@ -142,8 +146,13 @@ def test_gmres_matches_reference_golden(backend, golden, name):
         assert rep.restart_cycles == [int(c) for c in golden[f"gm_{name}_cycles"]]
     h_ref = golden[f"gm_{name}_hist"]
     k = min(len(h_ref), len(rep.residual_history))
-    if prec == "f64" and float(tol) > 1e-11:
-        np.testing.assert_allclose(rep.residual_history[: k - 1], h_ref[: k - 1], rtol=1e-5)
+    if prec == "f64":
+        # Arnoldi LS estimates while above 1e-11 (below, both walk into round-off), and the
+        # final (true) residual of converged runs within 1e-3
+        kk = int(np.argmax(np.asarray(h_ref[: k - 1]) < 1e-11)) or (k - 1)
+        np.testing.assert_allclose(rep.residual_history[:kk], h_ref[:kk], rtol=1e-5)
+        if rep.converged and rep.iterations == it_ref and h_ref[-1] > 1e-13:
+            np.testing.assert_allclose(rep.residual_history[-1], h_ref[-1], rtol=1e-3)
     xr = golden[f"gm_{name}_x"]
     xt = 1e-8 if prec == "f64" else 1e-3
     if rep.converged:

@@ -193,6 +193,10 @@ def test_sharded_gmres_fp32_and_errors():
         gmres_solve(A, np.zeros_like(b), np.zeros_like(b), SolverConfig(tolerance=1e-8), be)
     with pytest.raises(ValueError):
         gmres_solve(A, b, np.zeros_like(b), SolverConfig(tolerance=1e-8, restart_m=64), be)
+    # one shard: the fused single-GPU step, no restart limit
+    x1, r1 = gmres_solve(A, b, np.zeros_like(b), SolverConfig(tolerance=1e-8, restart_m=80),
+                         get_backend("b200", devices=[0]))
+    assert r1.converged
 
 
 @pytest.mark.parametrize("devices,n,b", [([0], 300, 64), ([0, 0], 600, 64), ([0, 0, 0], 777, 32)])
