@@ -25,7 +25,7 @@ from ctypes import c_int32, c_int64, c_void_p
 import numpy as np
 
 from . import _lib
-from .backends import as_b200
+from .backends import B200Backend, as_b200
 from .core import (CholeskyFactor, DimensionError, LuFactors, NotSpdError, SingularMatrixError,
                    check_precision, check_square)
 from .device import DeviceArray, is_device, to_device
@@ -57,12 +57,17 @@ def _factor(A, b: int, backend, blocked: bool) -> LuFactors:
     be = as_b200(backend)
     n = check_square(A)
     check_precision(A)
+    counting = be  # the caller's backend receives the counter tallies
+    if isinstance(be, ShardedB200Backend) and be.nshards == 1:
+        # one shard owns every column block: the single-GPU factorization (look-ahead panel
+        # stream, TMA-fed trailing GEMM) on that shard's device
+        be = B200Backend(device=be.devices[0])
     if isinstance(be, ShardedB200Backend) and not is_device(A):
         # columns dealt to the shards in NB-wide blocks (1-D block-cyclic, sharded.py)
         packed, piv, singular = lu_factor_block_cyclic_api(A, max(b, 1), be)
         zero = np.zeros(max(n, 1), dtype=np.int8)
         zero[:n] = np.diagonal(packed) == 0
-        _tally_lu(be, n, max(b, 1), zero, blocked)
+        _tally_lu(counting, n, max(b, 1), zero, blocked)
         return LuFactors(packed=packed, pivots=piv.astype(np.intp), singular=singular)
     ctx = be.ctx
     src = to_device(A, ctx)
@@ -73,7 +78,7 @@ def _factor(A, b: int, backend, blocked: bool) -> LuFactors:
     _lib.check(ctx.lib.ds_lu_factor(ctx.handle, W.dcode, n, c_void_p(W.ptr), W.ld, max(b, 1),
                                     piv.ctypes.data_as(c_void_p), zero.ctypes.data_as(c_void_p),
                                     ctypes.byref(sing)))
-    _tally_lu(be, n, max(b, 1), zero, blocked)
+    _tally_lu(counting, n, max(b, 1), zero, blocked)
     packed = W if is_device(A) else W.to_host()
     return LuFactors(packed=packed, pivots=piv, singular=bool(sing.value), device=W)
 
