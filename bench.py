@@ -446,7 +446,7 @@ def run_b200(args):
         from paper_1511_07207_b200 import bicgstab_solve, cholesky_factor
         components["bicgstab"] = bench_bicgstab(args, torch, stream, be, dA, db, dx0, n, bicgstab_solve,
                                                 SolverConfig, hbm_peak, A_h, b_h)
-        components["cholesky"] = bench_cholesky(args, torch, stream, be, dA, n, cholesky_factor)
+        components["cholesky"] = bench_cholesky(args, torch, stream, be, dA, n, cholesky_factor, A_h)
     del dA, A_h
     torch.cuda.empty_cache()
     if not args.only_cg:
@@ -594,15 +594,50 @@ def bench_bicgstab(args, torch, stream, be, dA, db, dx0, n, bicgstab_solve, Solv
     return out
 
 
-def bench_cholesky(args, torch, stream, be, dA, n, cholesky_factor):
-    """Cholesky of the C4 SPD matrix, b=64, device-resident."""
+def bench_cholesky(args, torch, stream, be, dA, n, cholesky_factor, A_h=None):
+    """Cholesky of the C4 SPD matrix, b=64, device-resident.  CPU
+    baseline: the reference cholesky_factor (b=64, 'blocked') at n = 2048 / 4096 on the spd
+    recipe fitted to t = a n^3 (labelled extrapolated), plus scipy's LAPACK dpotrf at full n
+    on the same bytes as a labelled comparator."""
     runs = [_timed(torch, stream, lambda: cholesky_factor(dA, 64, be), 1)[0] for _ in range(3)]
     ms = min(runs)  # 1 warm-up (inside _timed) + best of 3, harness.py:281-294
     tf = n ** 3 / 3.0 / (ms / 1e3) / 1e12
-    return {"workload": f"blocked Cholesky b=64, dense SPD n={n} fp64 (C4 matrix), device-resident; best of 3",
-            "value": round(tf * 1e3, 1), "unit": "GFLOP/s", "ms": round(ms, 2),
-            "ms_runs": [round(r, 2) for r in runs],
-            "fp64_peak_tflops": FP64_PEAK_TFLOPS, "frac_of_fp64_peak": round(tf / FP64_PEAK_TFLOPS, 4)}
+    out = {"workload": f"blocked Cholesky b=64, dense SPD n={n} fp64 (C4 matrix), device-resident; best of 3",
+           "value": round(tf * 1e3, 1), "unit": "GFLOP/s", "ms": round(ms, 2),
+           "ms_runs": [round(r, 2) for r in runs],
+           "fp64_peak_tflops": FP64_PEAK_TFLOPS, "frac_of_fp64_peak": round(tf / FP64_PEAK_TFLOPS, 4)}
+    if args.no_cpu_baseline:
+        return out
+    try:
+        from paper_1511_07207_b200.harness import ProblemSpec, generate_problem
+        densolve = ref_densolve()
+        rbe = densolve.get_backend("blocked")
+        pts = []
+        for m in (2048, 4096):
+            S, _, _ = generate_problem(ProblemSpec(kind="spd", n=m, seed=0))
+            t0 = time.perf_counter()
+            densolve.cholesky_factor(S, 64, rbe)
+            pts.append((m, time.perf_counter() - t0))
+        a = sum(t * m ** 3 for m, t in pts) / sum(m ** 6 for m, _ in pts)
+        te = a * n ** 3
+        cpu = {"value": round(n ** 3 / 3.0 / te / 1e9, 3), "unit": "GFLOP/s", "cores": host_info()["cores"],
+               "kind": "reference",
+               "sample": f"EXTRAPOLATED: densolve.cholesky_factor (baseline/_ref, b=64, 'blocked') timed at "
+                         f"n=2048/4096, t = a n^3 -> {te:.0f} s at n={n}",
+               "points": [{"n": m, "s": round(t, 3), "GFLOP/s": round(m ** 3 / 3 / t / 1e9, 3)} for m, t in pts]}
+        if A_h is not None:
+            import scipy.linalg
+            t0 = time.perf_counter()
+            scipy.linalg.cholesky(A_h, lower=True, overwrite_a=False, check_finite=False)
+            tl = time.perf_counter() - t0
+            cpu["lapack_comparator"] = {"value": round(n ** 3 / 3.0 / tl / 1e9, 1), "unit": "GFLOP/s",
+                                        "s": round(tl, 2),
+                                        "what": "scipy.linalg.cholesky (LAPACK dpotrf, OpenBLAS) at full n on the "
+                                                "same bytes; NOT the reference"}
+        out["cpu_baseline"] = cpu
+    except Exception as e:  # the reference install is optional on the box
+        out["cpu_baseline"] = {"unavailable": str(e)[:200]}
+    return out
 
 
 def reference_lu_fit():

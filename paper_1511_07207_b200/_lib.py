@@ -13,6 +13,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+import weakref
 from ctypes import (POINTER, c_char_p, c_double, c_int, c_int8, c_int32, c_int64, c_size_t, c_uint64,
                     c_void_p)
 
@@ -223,7 +224,9 @@ def dtype_code(dtype) -> int:
 class Context:
     """One CUDA device context (stream + scratch) of the library."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, owned: bool = False):
+        """owned=True: a private context (e.g. one per shard of a sharded backend) that is
+        destroyed with this object; the per-device defaults of context() live for the process."""
         self.lib = load_library()
         n = c_int(0)
         self.lib.ds_device_count(ctypes.byref(n))
@@ -234,6 +237,8 @@ class Context:
         check(self.lib.ds_ctx_create(device, ctypes.byref(h)))
         self.handle = h
         self.device = device
+        if owned:  # device arrays keep their context alive (DeviceArray finalizer), so this runs last
+            weakref.finalize(self, self.lib.ds_ctx_destroy, h)
 
     def launches(self) -> int:
         v = c_int64(0)

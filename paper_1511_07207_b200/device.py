@@ -23,7 +23,8 @@ from . import _lib, core
 LD_ALIGN = 4
 
 
-def _release_device(lib, handle, ptr, inflight):
+def _release_device(lib, handle, ptr, inflight, ctx=None):
+    # ctx: held by the finalizer so the context outlives every buffer allocated on it
     """Finalizer of a DeviceArray: the context stream first waits for a still pending
     asynchronous upload into the buffer (copy stream), then frees it stream-ordered."""
     if inflight[0] is not None:
@@ -61,7 +62,7 @@ class DeviceArray:
         # [event, host array] of an in-flight asynchronous upload (upload_async); shared with
         # the finalizer so a handle dropped before its copy finished is freed only after it
         self._inflight = [None, None]
-        self._fin = weakref.finalize(self, _release_device, ctx.lib, ctx.handle, self.ptr, self._inflight)
+        self._fin = weakref.finalize(self, _release_device, ctx.lib, ctx.handle, self.ptr, self._inflight, ctx)
 
     # -- numpy-like metadata used by the validators -------------------------------------
     @property

@@ -20,6 +20,7 @@ returns a :class:`ShardedMatrix`, ``backend.stage_in(b)`` a :class:`ShardedVecto
 from __future__ import annotations
 
 import ctypes
+import weakref
 from ctypes import c_int, c_int64, c_void_p
 
 import numpy as np
@@ -32,6 +33,11 @@ from .device import DeviceArray, _padded_ld
 
 def _ptr_array(ptrs):
     return (c_void_p * len(ptrs))(*[c_void_p(p) for p in ptrs])
+
+
+def _destroy_shardset(lib, handle, ctxs):
+    # ctxs: held until here so the shard contexts outlive the exchange regions
+    lib.ds_shardset_destroy(handle)
 
 
 class ShardSet:
@@ -53,6 +59,8 @@ class ShardSet:
         _lib.check(self.lib.ds_shardset_create(len(self.ctxs), arr, ranks, self.G, self.dcode, self.n, xbytes,
                                                ctypes.byref(h)))
         self.handle = h
+        # destroyed before its contexts: the finalizer holds them
+        self._fin = weakref.finalize(self, _destroy_shardset, self.lib, h, tuple(self.ctxs))
         a, b = c_int64(0), c_int64(0)
         _lib.check(self.lib.ds_shardset_info(h, ctypes.byref(a), ctypes.byref(b)))
         self.n_loc, self.N = a.value, b.value
@@ -82,15 +90,8 @@ class ShardSet:
         return out
 
     def close(self):
-        if self.handle:
-            self.lib.ds_shardset_destroy(self.handle)
-            self.handle = None
-
-    def __del__(self):
-        try:
-            self.close()
-        except Exception:
-            pass
+        self._fin()
+        self.handle = None
 
 
 class ShardedMatrix:
@@ -167,7 +168,7 @@ class ShardedB200Backend(B200Backend):
     def shard_contexts(self) -> list[_lib.Context]:
         # private contexts (own streams and workspaces), so shards sharing a GPU run concurrently
         if self._shard_ctxs is None:
-            self._shard_ctxs = [_lib.Context(d) for d in self.devices]
+            self._shard_ctxs = [_lib.Context(d, owned=True) for d in self.devices]
         return self._shard_ctxs
 
     def shardset(self, n: int, dtype) -> ShardSet:
