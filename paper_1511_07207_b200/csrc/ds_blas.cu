@@ -178,6 +178,140 @@ __global__ void __launch_bounds__(kGemvThreads)
     if (r0 + e < m) out[e] = acc[e];
 }
 
+// Wide-CTA stage 1 for small matrices (the GMRES C2 step, n <= 8192): about one CTA per SM,
+// CS column groups of 256 threads per CTA (CS x 32 KB of loads in flight per SM instead of
+// short-lived CTAs of one group), the group partials summed in a fixed order through shared
+// memory: one partial per row per CTA, so the orthogonalisation cluster that sums the
+// partials reads ~4x fewer of them.
+int wide_groups() {  // column groups per CTA of the wide GEMV (DENSOLVE_GEMV_WIDE=2|4, default 4)
+  static const int g = [] {
+    const char* e = getenv("DENSOLVE_GEMV_WIDE");
+    return e && atoi(e) == 2 ? 2 : 4;
+  }();
+  return g;
+}
+GemvPlan gemv_wide_plan(ds_ctx* ctx, int64_t m, int64_t n, size_t elem) {
+  const int kWideGroups = wide_groups();
+  GemvPlan p;
+  p.m = m;
+  p.n = n;
+  const int vec = elem == 8 ? 2 : 4;
+  p.rows_per_cta = kGemvThreads * vec;
+  p.rowtiles = ceil_div(std::max<int64_t>(m, 1), p.rows_per_cta);
+  const int64_t nch = std::max<int64_t>(1, (int64_t)ctx->num_sms / p.rowtiles);
+  p.chunk = ceil_div(ceil_div(std::max<int64_t>(n, 1), nch), 8 * kWideGroups) * 8 * kWideGroups;
+  p.nchunks = ceil_div(std::max<int64_t>(n, 1), p.chunk);
+  p.part_bytes = (size_t)p.nchunks * (size_t)std::max<int64_t>(m, 1) * sizeof(double);
+  return p;
+}
+
+template <typename T, int VEC, int UNR, int CS>
+__global__ void __launch_bounds__(kGemvThreads * CS)
+    ds_colstream_mv_wide_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t n, const T* __restrict__ x,
+                                int64_t chunk, double* __restrict__ part, Gate gate) {
+  pdl_wait();  // x and the stop word come from the previous kernel
+  if (gated(gate)) return;
+  pdl_launch_dependents();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* xs = reinterpret_cast<T*>(smem_raw);
+  double* red = reinterpret_cast<double*>(smem_raw + ((size_t)chunk * sizeof(T) + 15) / 16 * 16);
+  const int tl = threadIdx.x % kGemvThreads, grp = threadIdx.x / kGemvThreads;
+  const int64_t c0 = (int64_t)blockIdx.y * chunk;
+  const int64_t cn = min(chunk, n - c0);
+  for (int64_t j = threadIdx.x; j < cn; j += blockDim.x) xs[j] = x[c0 + j];
+  __syncthreads();
+  const int64_t gsz = ceil_div(cn, (int64_t)CS);
+  const int64_t g0 = min(cn, grp * gsz), g1 = min(cn, g0 + gsz);
+  using V = typename VecT<T, VEC>::type;
+  const int64_t r0 = (int64_t)blockIdx.x * (kGemvThreads * VEC) + (int64_t)tl * VEC;
+  double acc[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) acc[e] = 0.0;
+  if (r0 < m) {
+    const T* a = A + c0 * lda + r0;
+    if (r0 + VEC <= m) {
+      int64_t j = g0;
+      for (; j + UNR <= g1; j += UNR) {
+        V v[UNR];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) v[u] = ldg_stream(reinterpret_cast<const V*>(a + (j + u) * lda));
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          T t[VEC];
+          vec_to_array<T, VEC>(v[u], t);
+          const double xv = (double)xs[j + u];
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc[e] = fma((double)t[e], xv, acc[e]);
+        }
+      }
+      for (; j < g1; ++j) {
+        V v = ldg_stream(reinterpret_cast<const V*>(a + j * lda));
+        T t[VEC];
+        vec_to_array<T, VEC>(v, t);
+        const double xv = (double)xs[j];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[e] = fma((double)t[e], xv, acc[e]);
+      }
+    } else {
+      for (int64_t j = g0; j < g1; ++j) {
+        const double xv = (double)xs[j];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e)
+          if (r0 + e < m) acc[e] = fma((double)__ldg(a + j * lda + e), xv, acc[e]);
+      }
+    }
+  }
+  if (grp > 0) {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) red[(size_t)(grp - 1) * kGemvThreads * VEC + tl * VEC + e] = acc[e];
+  }
+  __syncthreads();
+  if (grp == 0 && r0 < m) {
+    double* out = part + (int64_t)blockIdx.y * m + r0;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      double sum = acc[e];
+      for (int g = 1; g < CS; ++g) sum += red[(size_t)(g - 1) * kGemvThreads * VEC + tl * VEC + e];  // group order
+      if (r0 + e < m) out[e] = sum;
+    }
+  }
+}
+
+template <typename T>
+int gemv_partial_wide_pdl_launch(ds_ctx* ctx, const GemvPlan& p, const T* A, int64_t lda, const T* x, double* part,
+                                 Gate stop) {
+  constexpr int VEC = sizeof(T) == 8 ? 2 : 4;
+  const bool aligned = (reinterpret_cast<uintptr_t>(A) % 16 == 0) && (lda % VEC == 0);
+  if (p.m == 0 || p.n == 0 || !aligned) {
+    set_error("wide GEMV needs a non-empty, 16-byte aligned matrix");
+    return DS_EINVAL;
+  }
+  const int kWideGroups = wide_groups();
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)p.rowtiles, (unsigned)p.nchunks);
+  lc.blockDim = dim3(kGemvThreads * kWideGroups);
+  lc.dynamicSmemBytes = ((size_t)p.chunk * sizeof(T) + 15) / 16 * 16 +
+                        (size_t)(kWideGroups - 1) * kGemvThreads * VEC * sizeof(double);
+  lc.stream = ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  const int64_t m = p.m, n = p.n, chunk = p.chunk;
+  if (kWideGroups == 2)
+    DS_CUDA(cudaLaunchKernelEx(&lc, ds_colstream_mv_wide_kernel<T, VEC, 8, 2>, A, lda, m, n, x, chunk, part, stop));
+  else
+    DS_CUDA(cudaLaunchKernelEx(&lc, ds_colstream_mv_wide_kernel<T, VEC, 8, 4>, A, lda, m, n, x, chunk, part, stop));
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+template int gemv_partial_wide_pdl_launch<double>(ds_ctx*, const GemvPlan&, const double*, int64_t, const double*,
+                                                  double*, Gate);
+template int gemv_partial_wide_pdl_launch<float>(ds_ctx*, const GemvPlan&, const float*, int64_t, const float*,
+                                                 double*, Gate);
+
 constexpr int kRedThreads = 256;
 
 template <typename T, int EPI>

@@ -57,6 +57,12 @@ GemvPlan gemv_plan(ds_ctx* ctx, int64_t m, int64_t n, size_t elem);
 template <typename T>
 int gemv_partial_pdl_launch(ds_ctx* ctx, const GemvPlan& p, const T* A, int64_t lda, const T* x, double* part,
                             Gate stop);
+// Wide-CTA stage 1 for small matrices (~one CTA per SM, 4 column groups per CTA, one
+// partial per row per CTA), launched with the PDL attribute (the GMRES cluster path).
+GemvPlan gemv_wide_plan(ds_ctx* ctx, int64_t m, int64_t n, size_t elem);
+template <typename T>
+int gemv_partial_wide_pdl_launch(ds_ctx* ctx, const GemvPlan& p, const T* A, int64_t lda, const T* x, double* part,
+                                 Gate stop);
 // Launch stage 1 + 2.  `part` must have plan.part_bytes; `red` (for EPI_DOT /
 // EPI_RESID) receives per-block reduction partials (see reduce_blocks()).
 template <typename T>

@@ -1051,6 +1051,16 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
       }
     }
   }
+  // small n (C2): the wide-CTA GEMV (~one CTA per SM, one partial per row per CTA) feeds the
+  // cluster, which then sums ~18 instead of ~64 partials per row; DENSOLVE_GEMV_WIDE=0 disables
+  static const bool wide_env = [] {
+    const char* e = getenv("DENSOLVE_GEMV_WIDE");
+    return !(e && e[0] == '0');
+  }();
+  constexpr int kVecW = sizeof(T) == 8 ? 2 : 4;
+  const GemvPlan wp = gemv_wide_plan(ctx, n, n, sizeof(T));
+  const bool wide = wide_env && orth_cl > 0 && orth_fold && n <= 8192 && wp.part_bytes <= gp.part_bytes &&
+                    reinterpret_cast<uintptr_t>(A) % 16 == 0 && lda % kVecW == 0;
   const int arn_rch = (int)std::min<int64_t>(4, ceil_div(arn_per, 32)) == 3 ? 4
                                                                            : (int)std::min<int64_t>(4, ceil_div(arn_per, 32));
   size_t need = gp.part_bytes + (size_t)ldv * (m + 1) * sizeof(T) + (size_t)n * sizeof(T) +
@@ -1189,6 +1199,8 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
         if (orth_cl > 0) {  // streamed GEMV on every SM + one-cluster orthogonalisation
           if (!orth_fold)  // large n: the reduce kernel on every SM writes w
             DS_TRY(gemv_launch<T>(ctx, gp, A, lda, vk, w, part, EPI_STORE, nullptr, nullptr, nullptr, gt));
+          else if (pdl_on && wide)
+            DS_TRY(gemv_partial_wide_pdl_launch<T>(ctx, wp, A, lda, vk, part, gt));
           else if (pdl_on)
             DS_TRY(gemv_partial_pdl_launch<T>(ctx, gp, A, lda, vk, part, gt));
           else
@@ -1210,7 +1222,8 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
           const int passes = orth == DS_ORTH_CLASSICAL ? 1 : 2;
           DS_CUDA(cudaLaunchKernelEx(&lc, arnoldi_orth_cluster_kernel<T>, n, V, ldv, (int)k, passes, H, Hraw, ldh, g,
                                      cs, sn, est, st, tol, total_it, cap, gt,
-                                     orth_fold ? (const double*)part : nullptr, (int64_t)gp.nchunks,
+                                     orth_fold ? (const double*)part : nullptr,
+                                     (int64_t)(pdl_on && wide ? wp.nchunks : gp.nchunks),
                                      orth_trace));
           count_launch(ctx);
           continue;
