@@ -25,9 +25,10 @@
 //   iteration k (p: finish(k) waits for r-records(k), which every shard publishes
 //   after its GEMV(k) has read full; records likewise).
 //
-// Per iteration and shard:  [wait p] GEMV(partials) reduce(+local p'Ap partials)
-//   publish(p'Ap) [wait] update(x, r, (r.r, ssq) partials) publish(r) [wait]
-//   finish(p -> own slice + every peer's slice) signal.
+// Per iteration and shard:  [wait p] GEMV(partials) reduce(+p'Ap record, published by the
+//   last CTA) [wait] update(x, r; the r record published by its last CTA) [wait]
+//   finish(p -> own slice + every peer's slice; the last CTA releases the exchange):
+//   seven launches, three of them one-warp waits.
 // At G = 1 the waits, signals and record kernels vanish (the update and finish kernels
 // read the local block partials directly): the fused single-GPU CG's four launches.
 //
@@ -232,48 +233,135 @@ __global__ void sh_cg_init_kernel(const double* rec, int G, ShCg* st, double* rs
   st->stop_it = (res > tol && 0 < cap) ? cap : 0;
 }
 
-// alpha = rs/pAp (pAp from the shard-ordered records); x += alpha p; r -= alpha Ap;
-// (r.r, scale, ssq) partials per block (krylov.py:55-61)
-template <typename T>
-__global__ void __launch_bounds__(kShT)
-    sh_cg_update_kernel(int64_t n, const double* __restrict__ rec, int G, const double* __restrict__ red_pap,
-                        int nblk_pap, ShCg* st, const double* __restrict__ rs_hist, T* __restrict__ x,
-                        T* __restrict__ r, const T* __restrict__ p, const T* __restrict__ Ap, double* __restrict__ red,
-                        Gate gate) {
-  if (gated(gate)) return;
-  __shared__ double sm[64];
-  double pAp = 0.0;
-  if (G == 1) {  // one shard: the GEMV's block partials directly (no record round trip)
-    pAp = reduce_sum_partials(red_pap, nblk_pap, sm);
-  } else {
-    for (int t = 0; t < G; ++t) pAp += rec[rec_off(REC_PAP, t)];
+// Last-CTA helper: every CTA has stored its block partial; the CTA that arrives last
+// (ticket) sees all of them (fence + atomic, the classic threadfence reduction).
+__device__ __forceinline__ bool last_cta(unsigned* ticket) {
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
   }
-  if (pAp <= 0.0) {  // krylov.py:57-58
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      st->status = DS_ENOTSPD;
-      st->bad_val = pAp;
-      st->stop_it = gate.k;
-    }
-    return;
-  }
-  const double alpha = rs_hist[gate.k] / pAp;
-  const T a = (T)alpha, na = (T)(-alpha);
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last;
+}
+
+// the (s2, scale, ssq) record of nblk block partials red[3 blk ..] in block order, stored into
+// every shard's slot [kind][rank], then signal (== sh_publish_kernel<1>, fused into its producer)
+__device__ __forceinline__ void publish_parts3(const Peers& P, const double* red, int nblk, int kind,
+                                               unsigned long long seq, double* sm) {
   double s2 = 0.0;
   Ssq q{0.0, 0.0};
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    x[i] = add_rn(x[i], mul_rn(a, p[i]));
-    const T ri = add_rn(r[i], mul_rn(na, Ap[i]));
-    r[i] = ri;
-    const double v = (double)ri;
-    s2 = fma(v, v, s2);
-    q = ssq_add(q, v);
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    s2 += red[3 * i];
+    q = ssq_merge(q, Ssq{red[3 * i + 1], red[3 * i + 2]});
   }
   s2 = block_sum(s2, sm);
   q = block_ssq(q, sm);
   if (threadIdx.x == 0) {
-    red[3 * blockIdx.x] = s2;
-    red[3 * blockIdx.x + 1] = q.scale;
-    red[3 * blockIdx.x + 2] = q.ssq;
+    for (int t = 0; t < P.G; ++t) {
+      double* r = P.rec[t] + rec_off(kind, P.rank);
+      r[0] = s2;
+      r[1] = q.scale;
+      r[2] = q.ssq;
+    }
+    signal_peers(P, seq);
+  }
+}
+
+// alpha = rs/pAp (pAp from the shard-ordered records); x += alpha p; r -= alpha Ap;
+// (r.r, scale, ssq) partials per block (krylov.py:55-61).  G > 1: the last CTA finalises this
+// shard's r record and publishes it to the peers (no separate record kernel).
+template <typename T>
+__global__ void __launch_bounds__(kShT)
+    sh_cg_update_kernel(int64_t n, Peers P, const double* __restrict__ rec, const double* __restrict__ red_pap,
+                        int nblk_pap, ShCg* st, const double* __restrict__ rs_hist, T* __restrict__ x,
+                        T* __restrict__ r, const T* __restrict__ p, const T* __restrict__ Ap, double* __restrict__ red,
+                        Gate gate, unsigned* ticket, unsigned long long seq) {
+  const int G = P.G;
+  const bool skip = gated(gate);
+  if (skip && G == 1) return;
+  __shared__ double sm[64];
+  double pAp = 0.0;
+  if (!skip) {
+    if (G == 1) {  // one shard: the GEMV's block partials directly (no record round trip)
+      pAp = reduce_sum_partials(red_pap, nblk_pap, sm);
+    } else {
+      for (int t = 0; t < G; ++t) pAp += rec[rec_off(REC_PAP, t)];
+    }
+  }
+  const bool notspd = !skip && pAp <= 0.0;
+  if (notspd && blockIdx.x == 0 && threadIdx.x == 0) {  // krylov.py:57-58
+    st->status = DS_ENOTSPD;
+    st->bad_val = pAp;
+    st->stop_it = gate.k;
+  }
+  if (!skip && !notspd) {
+    const double alpha = rs_hist[gate.k] / pAp;
+    const T a = (T)alpha, na = (T)(-alpha);
+    double s2 = 0.0;
+    Ssq q{0.0, 0.0};
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+      x[i] = add_rn(x[i], mul_rn(a, p[i]));
+      const T ri = add_rn(r[i], mul_rn(na, Ap[i]));
+      r[i] = ri;
+      const double v = (double)ri;
+      s2 = fma(v, v, s2);
+      q = ssq_add(q, v);
+    }
+    s2 = block_sum(s2, sm);
+    q = block_ssq(q, sm);
+    if (threadIdx.x == 0) {
+      red[3 * blockIdx.x] = s2;
+      red[3 * blockIdx.x + 1] = q.scale;
+      red[3 * blockIdx.x + 2] = q.ssq;
+    }
+  }
+  if (G > 1 && last_cta(ticket)) {  // (stale partials after a stop: the consumers are gated)
+    publish_parts3(P, red, gridDim.x, REC_R, seq, sm);
+    if (threadIdx.x == 0) *ticket = 0;
+  }
+}
+
+// GEMV stage 2 of the sharded CG (G > 1): Ap = sum of the chunk partials (chunk order),
+// the block partials of p'Ap, and the last CTA publishes this shard's p'Ap record
+template <typename T>
+__global__ void __launch_bounds__(kShT)
+    sh_cg_reduce_pap_kernel(Peers P, const double* __restrict__ part, int64_t m, int64_t nchunks, T* Ap,
+                            const T* __restrict__ p, double* __restrict__ red, Gate gate, unsigned* ticket,
+                            unsigned long long seq) {
+  __shared__ double sm[64];
+  if (!gated(gate)) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double d = 0.0;
+    if (i < m) {
+      double s = 0.0;
+      int64_t c = 0;
+      for (; c + 8 <= nchunks; c += 8) {  // the chunk order of ds_colstream_reduce_kernel
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = part[(c + u) * m + i];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+      }
+      for (; c < nchunks; ++c) s += part[c * m + i];
+      const T yi = (T)s;
+      Ap[i] = yi;
+      d = (double)p[i] * (double)yi;
+    }
+    d = block_sum(d, sm);
+    if (threadIdx.x == 0) red[blockIdx.x] = d;
+  }
+  if (last_cta(ticket)) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) s += red[b];
+    s = block_sum(s, sm);
+    if (threadIdx.x == 0) {
+      for (int t = 0; t < P.G; ++t) P.rec[t][rec_off(REC_PAP, P.rank)] = s;
+      signal_peers(P, seq);
+      *ticket = 0;
+    }
   }
 }
 
@@ -283,8 +371,15 @@ template <typename T>
 __global__ void __launch_bounds__(kShT)
     sh_cg_finish_kernel(int64_t n_loc, Peers P, const double* __restrict__ rec, const double* __restrict__ red,
                         int nblk, const T* __restrict__ r, double* rs_hist, double* hist, ShCg* st, double tol,
-                        int64_t cap, Gate gate) {
-  if (gated(gate)) return;
+                        int64_t cap, Gate gate, unsigned* ticket, unsigned long long seq) {
+  if (gated(gate)) {
+    // G > 1: still release this exchange (the peers wait for it; nothing was written)
+    if (P.G > 1 && last_cta(ticket) && threadIdx.x == 0) {
+      signal_peers(P, seq);
+      *ticket = 0;
+    }
+    return;
+  }
   double rs_new, nrm;
   if (P.G == 1) {  // one shard: the update's block partials directly
     __shared__ double sm[64];
@@ -316,6 +411,11 @@ __global__ void __launch_bounds__(kShT)
     rs_hist[k + 1] = rs_new;
     hist[k + 1] = res;
     if (!(res > tol) || k + 1 >= cap) st->stop_it = k + 1;
+  }
+  // G > 1: the p slices of every CTA are in the peers' regions: the last CTA releases them
+  if (P.G > 1 && last_cta(ticket) && threadIdx.x == 0) {
+    signal_peers(P, seq);
+    *ticket = 0;
   }
 }
 
@@ -586,7 +686,7 @@ int sh_cg_run(ShardLocal& S, ds_shardset* ss, const T* A, int64_t lda, const T* 
   need += (size_t)nl * sizeof(T) * 2 + 2 * 256;  // r, Ap
   need += ((size_t)std::max(rblocks, vg) * 3 + 64) * sizeof(double) * 2 + 2 * 256;
   need += (size_t)(cap + 2) * sizeof(double) * 2 + 2 * 256;
-  need += sizeof(ShCg) + 256;
+  need += sizeof(ShCg) + 256 + 256;
   // Every allocation of the call happens here, before the first exchange: an allocation
   // that synchronises the device (cudaFree of a smaller workspace, pinned host memory)
   // would otherwise wait on a peer shard's exchange kernel sharing this GPU.
@@ -618,6 +718,7 @@ int sh_cg_run(ShardLocal& S, ds_shardset* ss, const T* A, int64_t lda, const T* 
   double* rs_hist = cv.take<double>((size_t)(cap + 2) * sizeof(double));
   double* hist = cv.take<double>((size_t)(cap + 2) * sizeof(double));
   ShCg* st = cv.take<ShCg>(sizeof(ShCg));
+  unsigned* tickets = cv.take<unsigned>(64);  // last-CTA tickets of the fused record kernels
   T* full = reinterpret_cast<T*>(S.full);
   T* p = full + (int64_t)S.rank * nl;
 
@@ -641,6 +742,7 @@ int sh_cg_run(ShardLocal& S, ds_shardset* ss, const T* A, int64_t lda, const T* 
   count_launch(ctx);
   DS_TRY(sh_signal(S, ss));
   DS_CHECK_LAUNCH();
+  DS_CUDA(cudaMemsetAsync(tickets, 0, 64, ctx->stream));
   ShCg hst;
   DS_CUDA(cudaMemcpyAsync(&hst, st, sizeof(ShCg), cudaMemcpyDeviceToHost, ctx->stream));
   DS_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -662,16 +764,26 @@ int sh_cg_run(ShardLocal& S, ds_shardset* ss, const T* A, int64_t lda, const T* 
       const Gate g{&st->stop_it, k};
       DS_TRY(sh_wait(S, ss));  // every shard's slice of p is in full
       int rb2 = 0;
-      DS_TRY(gemv_launch<T>(ctx, gp, A, lda, full, Ap, part, EPI_DOT, p, red_a, &rb2, g));
-      if (G > 1) DS_TRY(sh_publish<0>(S, ss, red_a, rb2, REC_PAP));
-      sh_cg_update_kernel<T><<<vg, kShT, 0, ctx->stream>>>(nl, S.rec, G, red_a, rb2, st, rs_hist, x, r, p, Ap,
-                                                           red_b, g);
+      if (G == 1) {
+        DS_TRY(gemv_launch<T>(ctx, gp, A, lda, full, Ap, part, EPI_DOT, p, red_a, &rb2, g));
+      } else {  // stage 2 with the p'Ap record published by its last CTA
+        DS_TRY(gemv_launch<T>(ctx, gp, A, lda, full, Ap, part, EPI_PARTIAL, nullptr, nullptr, nullptr, g));
+        rb2 = (int)ceil_div(nl, 256);
+        ++S.seq;
+        sh_cg_reduce_pap_kernel<T><<<rb2, kShT, 0, ctx->stream>>>(S.peers, part, nl, gp.nchunks, Ap, p, red_a, g,
+                                                                  tickets, S.seq);
+        count_launch(ctx);
+        DS_TRY(sh_wait(S, ss));
+      }
+      if (G > 1) ++S.seq;
+      sh_cg_update_kernel<T><<<vg, kShT, 0, ctx->stream>>>(nl, S.peers, S.rec, red_a, rb2, st, rs_hist, x, r, p, Ap,
+                                                           red_b, g, tickets + 1, S.seq);
       count_launch(ctx);
-      if (G > 1) DS_TRY(sh_publish<1>(S, ss, red_b, vg, REC_R));
+      if (G > 1) DS_TRY(sh_wait(S, ss));
+      ++S.seq;  // the p exchange: released by the finish kernel's last CTA
       sh_cg_finish_kernel<T><<<vg, kShT, 0, ctx->stream>>>(nl, S.peers, S.rec, red_b, vg, r, rs_hist, hist, st,
-                                                           tol, cap, g);
+                                                           tol, cap, g, tickets + 2, S.seq);
       count_launch(ctx);
-      DS_TRY(sh_signal(S, ss));
     }
     DS_CHECK_LAUNCH();
     chunk = std::min<int64_t>(chunk * 2, 64);
@@ -1010,6 +1122,7 @@ void shard_kernel_list(std::vector<const void*>& f) {
   f.push_back((const void*)sh_put_slice_kernel<T>);
   f.push_back((const void*)sh_cg_update_kernel<T>);
   f.push_back((const void*)sh_cg_finish_kernel<T>);
+  f.push_back((const void*)sh_cg_reduce_pap_kernel<T>);
   f.push_back((const void*)sh_parts_kernel<T>);
   f.push_back((const void*)sh_copy_block_kernel<T>);
 }
