@@ -227,6 +227,14 @@ int ds_shardset_gather(ds_shardset* ss, int dtype, const void* const* d_loc, voi
 int ds_cg_sharded(ds_shardset* ss, int dtype, void* const* d_A, int64_t lda, const void* const* d_b,
                   const void* const* d_x0, void* const* d_x, double tol, int64_t max_it, int check_sym,
                   double* h_hist, int64_t hist_cap, ds_solve_info* info);
+/* 1-D block-cyclic LU with partial pivoting (direct.py:50-84) over the shard set: column
+ * blocks of width nb dealt round-robin (shard q owns blocks q, q+G, ..., stored contiguously
+ * in d_W[i], n rows, leading dimension ldw), b the reference's panel width.  Factors in
+ * place (each shard's blocks of the packed LU); h_piv (n, absolute rows, the reference's
+ * swap sequence) and *h_singular from local shard 0 (replicated).  The owner of each panel
+ * broadcasts it through the peers' staging buffers (2 slots of n*nb*elem + 9*nb bytes). */
+int ds_lu_block_cyclic(ds_shardset* ss, int dtype, void* const* d_W, int64_t ldw, int64_t nb, int64_t b,
+                       int64_t* h_piv, int32_t* h_singular);
 /* Row-sharded GMRES(m) (krylov.py:75-182), same layout and conventions as ds_cg_sharded:
  * the v_k slices, the multi-dot records of each CGS pass and the norm records are
  * all-gathered over the peer-memory regions; H, the Givens rotations, the estimates and the

@@ -109,6 +109,7 @@ _SIGNATURES = {
     "ds_shardset_connect_ipc": (c_int, [c_void_p, c_void_p]),
     "ds_shardset_destroy": (c_int, [c_void_p]),
     "ds_shardset_gather": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
+    "ds_lu_block_cyclic": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_int64, c_int64, c_void_p, POINTER(c_int32)]),
     "ds_gmres_sharded": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_double, c_int64,
                                  c_int64, c_int, c_void_p, c_int64, c_void_p, c_int64, POINTER(SolveInfo)]),
     "ds_cg_sharded": (c_int, [c_void_p, c_int, c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_double, c_int64,

@@ -1700,6 +1700,20 @@ template int trsm_upper_launch<float>(ds_ctx*, int64_t, int64_t, const float*, i
 // Load (lazy module loading) every kernel the row-sharded solver launches from this
 // file, before any shard starts spinning on an exchange: a first launch that loads its
 // module waits for the device, i.e. for the peers' exchange kernels on a shared GPU.
+int preload_dense_kernels_blas() {  // TRSM and GEMM of the block-cyclic LU shards
+  cudaFuncAttributes a;
+  const void* fns[] = {(const void*)trsm_lower_unit_cols64<double>, (const void*)trsm_lower_unit_cols64<float>,
+                       (const void*)trsm_lower_unit_tile<double>,   (const void*)trsm_lower_unit_tile<float>,
+                       (const void*)trsm_lower_unit_big<double>,    (const void*)trsm_lower_unit_big<float>,
+                       (const void*)gemm64_tma_kernel<0>,           (const void*)gemm64_tma_kernel<1>,
+                       (const void*)gemm64_kernel<true, 0>,         (const void*)gemm64_kernel<true, 1>,
+                       (const void*)gemm64_kernel<false, 0>,        (const void*)gemm64_kernel<false, 1>,
+                       (const void*)gemm32_kernel<0>,               (const void*)gemm32_kernel<1>,
+                       (const void*)gemm32_big_kernel<0, true>,     (const void*)gemm32_big_kernel<1, true>,
+                       (const void*)gemm32_big_kernel<0, false>,    (const void*)gemm32_big_kernel<1, false>};
+  for (const void* f : fns) DS_CUDA(cudaFuncGetAttributes(&a, f));
+  return DS_OK;
+}
 int preload_sharded_kernels_blas() {
   cudaFuncAttributes a;
   const void* fns[] = {

@@ -133,6 +133,12 @@ int trsv_upper_trans_launch(ds_ctx* ctx, int64_t n, const T* M, int64_t ld, cons
 
 // ---- lazy-loading guard of the row-sharded solver (ds_shard.cu) ----------------
 int preload_sharded_kernels_blas();
+int preload_dense_kernels_blas();
+int preload_lu_kernels();
+template <typename T>
+int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t b, int64_t* d_piv, int8_t* d_zero);
+template <typename T>
+int laswp_range(ds_ctx* ctx, T* W, int64_t ld, int64_t ncols, int64_t k0, int64_t k1, const int64_t* d_piv);
 int preload_sharded_kernels_dist();
 
 }  // namespace ds

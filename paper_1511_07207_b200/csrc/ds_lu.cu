@@ -1571,6 +1571,19 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
   }
   return DS_OK;
 }
+// Load (lazy module loading) every kernel the block-cyclic LU shards launch, before any shard
+// waits on a peer (see ds_shard.cu): a first launch that loads a module waits for the device.
+int preload_lu_kernels() {
+  cudaFuncAttributes a;
+  const void* fns[] = {(const void*)lu_panel_smem_kernel<double, 2>, (const void*)lu_panel_smem_kernel<double, 4>,
+                       (const void*)lu_panel_smem_kernel<float, 2>,  (const void*)lu_panel_smem_kernel<float, 4>,
+                       (const void*)lu_panel_warp_kernel<double>,     (const void*)lu_panel_warp_kernel<float>,
+                       (const void*)lu_panel_global_kernel<double>,   (const void*)lu_panel_global_kernel<float>,
+                       (const void*)laswp_plan_kernel,                (const void*)laswp_plan_serial_kernel,
+                       (const void*)laswp_gather_kernel<double>,      (const void*)laswp_gather_kernel<float>};
+  for (const void* f : fns) DS_CUDA(cudaFuncGetAttributes(&a, f));
+  return DS_OK;
+}
 template int lu_factor_impl<double>(ds_ctx*, int64_t, int64_t, double*, int64_t, int64_t, int64_t*, int8_t*);
 template int lu_factor_impl<float>(ds_ctx*, int64_t, int64_t, float*, int64_t, int64_t, int64_t*, int8_t*);
 

@@ -54,6 +54,7 @@ namespace ds {
 
 constexpr int kMaxShards = DS_MAX_SHARDS;
 enum { REC_B = 0, REC_PAP = 1, REC_R = 2, REC_GEN = 3, REC_KINDS = 4 };
+constexpr int FLAG_BCAST = 16, FLAG_DONE = 32;  // offsets of the block-cyclic LU flag sets
 constexpr int kRecW = 4;
 constexpr int kShT = 256;
 
@@ -203,6 +204,81 @@ __global__ void sh_publish_array_kernel(Peers P, const double* __restrict__ src,
   if (P.G > 1) __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) signal_peers(P, seq);
+}
+
+// ---- 1-D block-cyclic LU exchange kernels -------------------------------------------
+// the owner's factored panel (rows kb..n of its column block, width w), its pivots (absolute)
+// and zero-pivot flags into every peer's staging slot; then release the broadcast flag
+template <typename T>
+__global__ void __launch_bounds__(kShT)
+    sh_bcast_panel_kernel(Peers P, const T* __restrict__ panel, int64_t ldp, int64_t mp, int64_t w,
+                          const int64_t* __restrict__ piv, const int8_t* __restrict__ zero, size_t slot_off,
+                          size_t piv_off, size_t zero_off, unsigned long long flag_val, unsigned* ticket) {
+  const int64_t total = mp * w;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / mp, i = e - j * mp;
+    const T v = panel[i + j * ldp];
+    for (int t = 0; t < P.G; ++t)
+      if (t != P.rank) reinterpret_cast<T*>(P.xbuf[t] + slot_off)[e] = v;
+  }
+  if (blockIdx.x == 0)
+    for (int64_t j = threadIdx.x; j < w; j += blockDim.x)
+      for (int t = 0; t < P.G; ++t)
+        if (t != P.rank) {
+          reinterpret_cast<int64_t*>(P.xbuf[t] + piv_off)[j] = piv[j];
+          reinterpret_cast<int8_t*>(P.xbuf[t] + zero_off)[j] = zero[j];
+        }
+  __threadfence_system();
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence_system();
+    for (int t = 0; t < P.G; ++t)
+      if (t != P.rank) st_release_sys(P.flag[t] + FLAG_BCAST + P.rank, flag_val);
+    *ticket = 0;
+  }
+}
+
+// one flag word per peer at `off` (FLAG_DONE: every peer; single source: src >= 0)
+__global__ void sh_wait_set_kernel(const unsigned long long* flag, int off, int G, int rank, int src,
+                                   unsigned long long val, int* err, unsigned long long timeout_ns) {
+  const int t = threadIdx.x;
+  const bool mine = src >= 0 ? t == src : (t < G && t != rank);
+  if (mine) {
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_acquire_sys(flag + off + t) < val) {
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        atomicExch(err, 1);
+        break;
+      }
+      __nanosleep(32);
+    }
+  }
+}
+
+__global__ void sh_signal_set_kernel(Peers P, int off, unsigned long long val) {
+  if (threadIdx.x != 0 || P.G <= 1) return;
+  __threadfence_system();
+  for (int t = 0; t < P.G; ++t)
+    if (t != P.rank) st_release_sys(P.flag[t] + off + P.rank, val);
+}
+
+__global__ void sh_piv_offset_kernel(int64_t* piv, int64_t w, int64_t kb) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < w; j += (int64_t)gridDim.x * blockDim.x)
+    piv[j] += kb;
+}
+
+__global__ void sh_any_kernel(const int8_t* z, int64_t n, int* out) {
+  int a = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a |= z[i] != 0;
+  a = __syncthreads_or(a);
+  if (threadIdx.x == 0 && a) *out = 1;
 }
 
 struct ShCg {
@@ -475,6 +551,7 @@ struct ShardLocal {
   Peers peers{};
   std::vector<void*> opened;  // IPC-mapped peer regions (closed on destroy)
   unsigned long long seq = 0;
+  unsigned long long lu_epoch = 0;  // block-cyclic LU: flag values of earlier factorizations
 };
 
 struct ds_shardset {
@@ -489,7 +566,7 @@ struct ds_shardset {
 
 namespace {
 
-constexpr size_t kFlagBytes = 256;
+constexpr size_t kFlagBytes = 512;  // words 0..15: exchange sequence; 16..31: LU broadcasts; 32..47: LU done
 constexpr size_t kRecBytes = (size_t)REC_KINDS * kMaxShards * kRecW * sizeof(double);  // 2 KB
 constexpr size_t kErrBytes = 256;
 
@@ -1085,6 +1162,164 @@ int sh_gmres_run(ShardLocal& S, ds_shardset* ss, const T* A, int64_t lda, const 
   return DS_OK;
 }
 
+// ---- 1-D block-cyclic LU (direct.py:50-84) ------------------------------------------
+// Column blocks of width nb are dealt round-robin: shard q owns blocks q, q+G, ... stored
+// contiguously in W (n rows, ld ldw).  Step k: the owner of block k broadcasts its factored
+// panel (rows kb..n, its pivots and zero-pivot flags) into every peer's staging slot
+// (parity k&1) and releases the broadcast flag; every shard applies the panel's row swaps to
+// all its columns outside block k, the b-blocked TRSM of the U block row and the DMMA
+// trailing update to its blocks right of k, then signals that it is done with the slot.
+// Look-ahead: the owner of block k+1 updates that block first and factors it before its
+// other step-k updates.  Two flag sets decouple the broadcast (one source per step) from the
+// done signals (every shard), so the look-ahead owner can broadcast early.
+size_t lu_slot_bytes(int64_t n, int64_t nb, size_t elem) {
+  return round256((size_t)n * nb * elem) + round256((size_t)nb * 8) + round256((size_t)nb);
+}
+
+template <typename T>
+int sh_lu_run(ShardLocal& S, ds_shardset* ss, T* W, int64_t ldw, int64_t nb, int64_t b, int64_t* h_piv, int* h_sing,
+              HostBarrier* allocated) {
+  ds_ctx* ctx = S.ctx;
+  const int G = ss->G, q = S.rank;
+  const int64_t n = ss->n;
+  const int64_t nblocks = ceil_div(n, nb);
+  const size_t slot = lu_slot_bytes(n, nb, sizeof(T));
+  const int64_t nloc_blocks = nblocks > q ? ceil_div(nblocks - q, (int64_t)G) : 0;
+  auto lcol = [&](int64_t k) { return (k / G) * nb; };                 // local column of (own) block k
+  auto bw = [&](int64_t k) { return std::min<int64_t>(nb, n - k * nb); };
+  const int64_t ncols = nloc_blocks > 0 ? lcol(q + (nloc_blocks - 1) * G) + bw(q + (nloc_blocks - 1) * G) : 0;
+  // allocations (before any exchange, behind the host barrier of the local shards)
+  void* ws = nullptr;
+  int ast = ctx_workspace(ctx, (size_t)16 << 20, &ws);  // panel / laswp scratch of the shard kernels
+  const size_t need = round256((size_t)n * 8) + round256((size_t)n) + 512;
+  if (ast == DS_OK && need > S.sws_bytes) {
+    if (S.sws) cudaFree(S.sws);
+    S.sws = nullptr;
+    S.sws_bytes = 0;
+    if (cudaMalloc(&S.sws, need) == cudaSuccess)
+      S.sws_bytes = need;
+    else
+      ast = DS_ENOMEM;
+  }
+  if (allocated) allocated->arrive_and_wait();
+  if (ast != DS_OK) {
+    ss->broken = true;
+    return ast;
+  }
+  if (G > 1 && ss->xbytes < 2 * slot) {
+    set_error("shard set staging buffer too small for the block-cyclic LU panels");
+    return DS_EINVAL;
+  }
+  Carver cv{(char*)S.sws};
+  int64_t* piv = cv.take<int64_t>((size_t)n * 8);
+  int8_t* zero = cv.take<int8_t>((size_t)n);
+  unsigned* ticket = cv.take<unsigned>(64);
+  int* d_any = reinterpret_cast<int*>(ticket + 8);
+  DS_CUDA(cudaMemsetAsync(zero, 0, (size_t)n, ctx->stream));
+  DS_CUDA(cudaMemsetAsync(ticket, 0, 64, ctx->stream));
+  DS_CUDA(cudaMemsetAsync(S.err, 0, kErrBytes, ctx->stream));
+  const unsigned long long base = S.lu_epoch;
+  const unsigned long long tmo = watchdog_ns();
+
+  auto factor = [&](int64_t k) -> int {  // the owner's panel: rows kb..n of block k
+    const int64_t kb = k * nb, w = bw(k);
+    DS_TRY(lu_factor_impl<T>(ctx, n - kb, w, W + kb + lcol(k) * ldw, ldw, std::min<int64_t>(b, w), piv + kb,
+                             zero + kb));
+    sh_piv_offset_kernel<<<1, 256, 0, ctx->stream>>>(piv + kb, w, kb);
+    count_launch(ctx);
+    return DS_OK;
+  };
+  auto update = [&](int64_t k, const T* L, int64_t ldl, int64_t c0, int64_t c1) -> int {
+    if (c1 <= c0) return DS_OK;
+    const int64_t kb = k * nb, w = bw(k), cw = c1 - c0;
+    for (int64_t ib = 0; ib < w; ib += b) {  // U block row, b-blocked (direct.py:80-81)
+      const int64_t ibf = std::min<int64_t>(ib + b, w);
+      T* U = W + (kb + ib) + c0 * ldw;
+      DS_TRY(trsm_lower_unit_launch<T>(ctx, ibf - ib, cw, L + ib + ib * ldl, ldl, U, ldw, U, ldw));
+      if (ibf < w)
+        DS_TRY(gemm_launch<T>(ctx, w - ibf, cw, ibf - ib, -1.0, L + ibf + ib * ldl, ldl, U, ldw, 1.0,
+                              W + (kb + ibf) + c0 * ldw, ldw, W + (kb + ibf) + c0 * ldw, ldw));
+    }
+    if (kb + w < n)  // trailing update (direct.py:82-83)
+      DS_TRY(gemm_launch<T>(ctx, n - kb - w, cw, w, -1.0, L + w, ldl, W + kb + c0 * ldw, ldw, 1.0,
+                            W + (kb + w) + c0 * ldw, ldw, W + (kb + w) + c0 * ldw, ldw));
+    return DS_OK;
+  };
+  auto bcast = [&](int64_t k) -> int {  // owner: panel k into every peer's slot k&1
+    if (G <= 1) return DS_OK;
+    const int64_t kb = k * nb, w = bw(k);
+    if (k >= 2) {  // slot k&1 held panel k-2: every peer finished step k-2
+      sh_wait_set_kernel<<<1, 32, 0, ctx->stream>>>(S.flag, FLAG_DONE, G, q, -1, base + (unsigned long long)(k - 1),
+                                                    S.err, tmo);
+      count_launch(ctx);
+    }
+    const size_t so = (size_t)(k & 1) * slot;
+    const size_t po = so + round256((size_t)n * nb * sizeof(T)), zo = po + round256((size_t)nb * 8);
+    sh_bcast_panel_kernel<T><<<ctx->num_sms, kShT, 0, ctx->stream>>>(S.peers, W + kb + lcol(k) * ldw, ldw, n - kb, w,
+                                                                      piv + kb, zero + kb, so, po, zo,
+                                                                      base + (unsigned long long)(k + 1), ticket);
+    count_launch(ctx);
+    DS_CHECK_LAUNCH();
+    return DS_OK;
+  };
+
+  if (nblocks > 0 && q == 0) DS_TRY(factor(0));
+  for (int64_t k = 0; k < nblocks; ++k) {
+    const int o = (int)(k % G);
+    const int64_t kb = k * nb, w = bw(k);
+    const T* L;
+    int64_t ldl;
+    if (q == o) {
+      DS_TRY(bcast(k));
+      L = W + kb + lcol(k) * ldw;
+      ldl = ldw;
+    } else {
+      sh_wait_set_kernel<<<1, 32, 0, ctx->stream>>>(S.flag, FLAG_BCAST, G, q, o, base + (unsigned long long)(k + 1),
+                                                    S.err, tmo);
+      count_launch(ctx);
+      const size_t so = (size_t)(k & 1) * slot;
+      const size_t po = so + round256((size_t)n * nb * sizeof(T)), zo = po + round256((size_t)nb * 8);
+      L = reinterpret_cast<const T*>(S.xbuf + so);
+      ldl = n - kb;
+      DS_CUDA(cudaMemcpyAsync(piv + kb, S.xbuf + po, (size_t)w * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+      DS_CUDA(cudaMemcpyAsync(zero + kb, S.xbuf + zo, (size_t)w, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    // the panel's row swaps on every local column outside block k (full-row swaps, direct.py:68-70)
+    if (q == o) {
+      DS_TRY(laswp_range<T>(ctx, W, ldw, lcol(k), kb, kb + w, piv));
+      DS_TRY(laswp_range<T>(ctx, W + (lcol(k) + w) * ldw, ldw, ncols - lcol(k) - w, kb, kb + w, piv));
+    } else if (ncols > 0) {
+      DS_TRY(laswp_range<T>(ctx, W, ldw, ncols, kb, kb + w, piv));
+    }
+    // local blocks right of k: from the first own block with index > k to the end
+    int64_t kr = k + 1 + (((q - (int)((k + 1) % G)) % G + G) % G);  // first own block >= k+1
+    if (kr < nblocks) {
+      const int64_t c0 = lcol(kr);
+      if (kr == k + 1) {  // look-ahead: this shard owns block k+1
+        DS_TRY(update(k, L, ldl, c0, c0 + bw(kr)));
+        DS_TRY(factor(k + 1));
+        DS_TRY(update(k, L, ldl, c0 + bw(kr), ncols));
+      } else {
+        DS_TRY(update(k, L, ldl, c0, ncols));
+      }
+    }
+    if (G > 1) {  // done with the slot of panel k
+      sh_signal_set_kernel<<<1, 32, 0, ctx->stream>>>(S.peers, FLAG_DONE, base + (unsigned long long)(k + 1));
+      count_launch(ctx);
+    }
+    DS_CHECK_LAUNCH();
+  }
+  DS_CUDA(cudaMemsetAsync(d_any, 0, sizeof(int), ctx->stream));
+  sh_any_kernel<<<1, 256, 0, ctx->stream>>>(zero, n, d_any);
+  count_launch(ctx);
+  if (h_piv) DS_CUDA(cudaMemcpyAsync(h_piv, piv, (size_t)n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  DS_CUDA(cudaMemcpyAsync(h_sing, d_any, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  DS_CUDA(cudaStreamSynchronize(ctx->stream));
+  DS_TRY(check_watchdog(S));
+  S.lu_epoch = base + (unsigned long long)nblocks;
+  return DS_OK;
+}
+
 // run fn(i) for every local shard: inline for one, one host thread per shard otherwise;
 // the first failing shard's status and message are returned
 template <typename F>
@@ -1123,18 +1358,23 @@ void shard_kernel_list(std::vector<const void*>& f) {
   f.push_back((const void*)sh_cg_update_kernel<T>);
   f.push_back((const void*)sh_cg_finish_kernel<T>);
   f.push_back((const void*)sh_cg_reduce_pap_kernel<T>);
+  f.push_back((const void*)sh_bcast_panel_kernel<T>);
   f.push_back((const void*)sh_parts_kernel<T>);
   f.push_back((const void*)sh_copy_block_kernel<T>);
 }
 int preload_kernels() {
   std::vector<const void*> f = {(const void*)sh_wait_kernel, (const void*)sh_signal_kernel,
                                 (const void*)sh_publish2_kernel, (const void*)sh_cg_init_kernel,
-                                (const void*)sh_publish_array_kernel};
+                                (const void*)sh_publish_array_kernel, (const void*)sh_wait_set_kernel,
+                                (const void*)sh_signal_set_kernel, (const void*)sh_piv_offset_kernel,
+                                (const void*)sh_any_kernel};
   shard_kernel_list<double>(f);
   shard_kernel_list<float>(f);
   cudaFuncAttributes a;
   for (const void* p : f) DS_CUDA(cudaFuncGetAttributes(&a, p));
   DS_TRY(preload_sharded_kernels_blas());
+  DS_TRY(preload_dense_kernels_blas());
+  DS_TRY(preload_lu_kernels());
   return preload_sharded_kernels_dist();
 }
 
@@ -1330,6 +1570,45 @@ int ds_shardset_gather(ds_shardset* ss, int dtype, const void* const* d_loc, voi
     DS_CUDA(cudaStreamSynchronize(S.ctx->stream));
     return check_watchdog(S);
   });
+  if (st == DS_ECUDA) ss->broken = true;
+  return st;
+}
+
+int ds_lu_block_cyclic(ds_shardset* ss, int dtype, void* const* d_W, int64_t ldw, int64_t nb, int64_t b,
+                       int64_t* h_piv, int32_t* h_singular) {
+  if (!ss || !ss->connected) {
+    set_error("shard set is not connected");
+    return DS_EINVAL;
+  }
+  if (ss->broken) {
+    set_error("shard set is unusable after an earlier failed exchange; create a new one");
+    return DS_ECUDA;
+  }
+  if (dtype_size(dtype) != ss->elem) {
+    set_error("dtype does not match the shard set");
+    return DS_EPREC;
+  }
+  if (nb < 1 || b < 1 || ldw < ss->n) {
+    set_error("invalid block-cyclic LU configuration (nb=%lld, b=%lld, ldw=%lld)", (long long)nb, (long long)b,
+              (long long)ldw);
+    return DS_EINVAL;
+  }
+  const int L = (int)ss->loc.size();
+  std::vector<int> sing(L, 0);
+  HostBarrier allocated(L);
+  const int st = for_each_local(ss, [&](int i) -> int {
+    ShardLocal& S = ss->loc[i];
+    const int e = ctx_begin(S.ctx);
+    if (e != DS_OK) {
+      allocated.arrive_and_wait();
+      return e;
+    }
+    std::lock_guard<std::recursive_mutex> guard(S.ctx->mu);
+    if (dtype == DS_F64)
+      return sh_lu_run<double>(S, ss, (double*)d_W[i], ldw, nb, b, i == 0 ? h_piv : nullptr, &sing[i], &allocated);
+    return sh_lu_run<float>(S, ss, (float*)d_W[i], ldw, nb, b, i == 0 ? h_piv : nullptr, &sing[i], &allocated);
+  });
+  if (h_singular) *h_singular = sing.empty() ? 0 : sing[0];
   if (st == DS_ECUDA) ss->broken = true;
   return st;
 }

@@ -43,7 +43,7 @@ def _destroy_shardset(lib, handle, ctxs):
 class ShardSet:
     """One ds_shardset: the exchange regions of the local shards for a system of size n."""
 
-    def __init__(self, backend: "ShardedB200Backend", n: int, dtype):
+    def __init__(self, backend: "ShardedB200Backend", n: int, dtype, xbytes: int | None = None):
         self.lib = _lib.load_library()
         self.n = int(n)
         self.dtype = np.dtype(dtype)
@@ -52,7 +52,9 @@ class ShardSet:
         self.ranks = backend.local_ranks
         self.ctxs = backend.shard_contexts
         n_loc = -(-self.n // self.G)
-        xbytes = n_loc * n_loc * self.dtype.itemsize if self.G > 1 else 0
+        if xbytes is None:  # the symmetry gate's transposed blocks (row-sharded Krylov)
+            xbytes = n_loc * n_loc * self.dtype.itemsize
+        xbytes = xbytes if self.G > 1 else 0
         h = c_void_p()
         arr = (c_void_p * len(self.ctxs))(*[c.handle for c in self.ctxs])
         ranks = (c_int * len(self.ranks))(*self.ranks)
@@ -171,11 +173,17 @@ class ShardedB200Backend(B200Backend):
             self._shard_ctxs = [_lib.Context(d, owned=True) for d in self.devices]
         return self._shard_ctxs
 
-    def shardset(self, n: int, dtype) -> ShardSet:
-        key = (int(n), np.dtype(dtype).str)
+    def shardset(self, n: int, dtype, kind: str = "rows", nb: int = 0) -> ShardSet:
+        """The exchange regions for systems of size n: "rows" (row-sharded Krylov) or "lu"
+        (block-cyclic LU with nb-wide column blocks: two panel slots of n x nb)."""
+        key = (int(n), np.dtype(dtype).str, kind, int(nb))
         s = self._sets.get(key)
         if s is None:
-            s = ShardSet(self, n, dtype)
+            xb = None
+            if kind == "lu":
+                r256 = lambda v: -(-v // 256) * 256  # noqa: E731
+                xb = 2 * (r256(n * nb * np.dtype(dtype).itemsize) + r256(nb * 8) + r256(nb))
+            s = ShardSet(self, n, dtype, xbytes=xb)
             self._sets[key] = s
         return s
 
@@ -282,127 +290,6 @@ def cg_solve_sharded(A, b, x0, cfg, be: ShardedB200Backend):
 # ---------------------------------------------------------------------------
 # GMRES(m) and block-cyclic LU over the backend's shards
 # ---------------------------------------------------------------------------
-class ThreadComm:
-    """Collectives among the local shards of ONE process, one Python thread per shard
-    (devices=[...]).  Data moves device to device (cudaMemcpyPeerAsync over NVLink for
-    shards on different GPUs); every phase is ordered by CUDA events recorded on the
-    producers' streams and waited on by the consumers' streams, with a host barrier so a
-    wait is never enqueued before the record it refers to.  No kernel spins and no host
-    stream synchronisation happens inside a collective."""
-
-    def __init__(self, shared: dict, rank: int, size: int):
-        self.shared, self.rank, self.size = shared, rank, size
-
-    def _phase(self, value):
-        """Publish value (+ an event on this shard's stream); return everybody's."""
-        import torch
-
-        sh = self.shared
-        ev = torch.cuda.Event()
-        ev.record(torch.cuda.current_stream())
-        sh["slots"][self.rank] = (value, ev)
-        sh["barrier"].wait()
-        got = list(sh["slots"])
-        sh["barrier"].wait()  # every thread read the slots before they are reused
-        for v, e in got:
-            torch.cuda.current_stream().wait_event(e)
-        return [v for v, _ in got]
-
-    def allgather(self, out, inp):
-        inp = inp.contiguous()
-        parts = self._phase(inp)
-        L = inp.numel()
-        flat = out.reshape(-1)
-        for t, p in enumerate(parts):
-            flat[t * L:(t + 1) * L].copy_(p, non_blocking=True)
-        self._phase(None)  # the inputs stay untouched until every shard copied them
-
-    def broadcast(self, t, src: int):
-        parts = self._phase(t if self.rank == src else None)
-        if self.rank != src:
-            t.copy_(parts[src], non_blocking=True)
-        self._phase(None)
-
-    def allreduce_max(self, t):
-        parts = self._phase(t.clone())
-        for p in parts:
-            t.copy_(t.maximum(p.to(t.device, non_blocking=True)))
-        self._phase(None)
-
-    def alltoall(self, out, inp):
-        inp = inp.contiguous()
-        parts = self._phase(inp)
-        L = inp.numel() // self.size
-        flat = out.reshape(-1)
-        for s, p in enumerate(parts):
-            flat[s * L:(s + 1) * L].copy_(p.reshape(-1)[self.rank * L:(self.rank + 1) * L], non_blocking=True)
-        self._phase(None)
-
-    def barrier(self):
-        self._phase(None)
-
-
-def _run_local_shards(be: ShardedB200Backend, work):
-    """work(rank, size, comm, ops, device) on every local shard: one thread per shard in
-    a multi-GPU process (ThreadComm), inline with torch.distributed collectives under
-    distributed=True.  Returns the per-shard results in local order; re-raises the first
-    shard's exception."""
-    import threading
-
-    import torch
-
-    from .distributed import CudaShardOps, TorchComm
-
-    ctxs = be.shard_contexts
-    if be.distributed:
-        dev = be.devices[0]
-        torch.cuda.set_device(dev)
-        ops = CudaShardOps(ctxs[0])
-        ops.bind_current_stream()
-        return [work(be.local_ranks[0], be.nshards, TorchComm(be.group), ops, dev)]
-    G = be.nshards
-    shared = {"barrier": threading.Barrier(G), "slots": [None] * G}
-    results, errors = [None] * G, [None] * G
-
-    def run(i):
-        try:
-            torch.cuda.set_device(be.devices[i])
-            stream = torch.cuda.Stream(be.devices[i])
-            with torch.cuda.stream(stream):
-                ops = CudaShardOps(ctxs[i])
-                ctxs[i].set_stream(stream.cuda_stream)
-                results[i] = work(i, G, ThreadComm(shared, i, G), ops, be.devices[i])
-                stream.synchronize()
-        except BaseException as e:  # noqa: BLE001 - re-raised below in shard order
-            errors[i] = e
-            shared["barrier"].abort()  # release the peers instead of leaving them waiting
-        finally:
-            ctxs[i].set_stream(None)
-
-    if G == 1:
-        run(0)
-    else:
-        th = [threading.Thread(target=run, args=(i,), name=f"densolve-shard-{i}") for i in range(G)]
-        for t in th:
-            t.start()
-        for t in th:
-            t.join()
-    real = [e for e in errors if e is not None and not isinstance(e, threading.BrokenBarrierError)]
-    if real or any(errors):
-        raise (real or [e for e in errors if e is not None])[0]
-    return results
-
-
-def _row_block_tensor(A: np.ndarray, r0: int, r1: int, n_loc: int, dev, torch):
-    """Rows [r0, r1) of a host matrix as the drivers' (n, n_loc) tensor (column-major
-    n_loc x n block, zero rows past n)."""
-    n = A.shape[1]
-    t = torch.zeros((n, n_loc), dtype=torch.float64 if A.dtype == np.float64 else torch.float32, device=dev)
-    if r1 > r0:
-        t[:, : r1 - r0] = torch.from_numpy(np.ascontiguousarray(A[r0:r1, :].T)).to(dev)
-    return t
-
-
 def gmres_solve_rows(A, b, x0, cfg, be: ShardedB200Backend):
     """krylov.gmres_solve (krylov.py:75-182) with A split by rows over the backend's shards:
     ds_gmres_sharded runs the restarted Arnoldi loop in the library (the v_k slices, the
@@ -446,32 +333,39 @@ def gmres_solve_rows(A, b, x0, cfg, be: ShardedB200Backend):
 
 def lu_factor_block_cyclic_api(A, b: int, be: ShardedB200Backend):
     """direct.lu_factor_blocked (direct.py:50-84) with the columns dealt to the backend's
-    shards in NB-wide blocks, round-robin (distributed.lu_factor_block_cyclic per shard).
+    shards in NB-wide blocks, round-robin: ds_lu_block_cyclic factors them in the library
+    (panels broadcast over the peer-memory regions, look-ahead on the next panel's owner).
     Returns (packed F-order host factors, pivots, singular)."""
-    import torch
-
     from . import distributed as D
 
     A = np.asarray(A)
     n = A.shape[0]
+    NB = D.outer_block(b, n)
+    ss = be.shardset(n, A.dtype, kind="lu", nb=NB)
     G = be.nshards
-    tdt = torch.float64 if A.dtype == np.float64 else torch.float32
+    nblocks = -(-n // NB)
+    ld = _padded_ld(n)
+    blocks, cols = [], []
+    for ctx, q in zip(ss.ctxs, ss.ranks):
+        mine = D.local_blocks(nblocks, q, G)
+        idx = np.concatenate([np.arange(k * NB, min((k + 1) * NB, n)) for k in mine]) if mine else np.zeros(0, np.int64)
+        d = DeviceArray(ctx, (n, max(len(idx), 1)), A.dtype, ld=ld)
+        if len(idx):
+            d.upload(np.asfortranarray(A[:, idx]))
+        blocks.append(d)
+        cols.append(idx)
+    piv = np.empty(n, dtype=np.int64)
+    sing = ctypes.c_int32(0)
+    _lib.check(be.ctx.lib.ds_lu_block_cyclic(ss.handle, ss.dcode, _ptr_array([d.ptr for d in blocks]), ld, NB,
+                                             max(int(b), 1), piv.ctypes.data_as(c_void_p), ctypes.byref(sing)))
+    packed = np.empty((n, n), dtype=A.dtype, order="F")
+    local = [(idx, d.to_host()[:, : len(idx)]) for idx, d in zip(cols, blocks) if len(idx)]
+    if be.distributed:  # every rank returns the whole factorization
+        import torch.distributed as dist
 
-    def work(q, size, comm, ops, dev):
-        W_loc, idx = D.scatter_block_cyclic(A, n, b, q, size, torch, dev, tdt)
-        piv, singular = D.lu_factor_block_cyclic(W_loc, n, b, comm, ops)
-        if be.distributed:
-            packed = D.gather_block_cyclic(W_loc, idx, n, comm)
-        else:
-            packed = (idx, W_loc.cpu().numpy())
-        return packed, piv.cpu().numpy(), singular
-
-    res = _run_local_shards(be, work)
-    if be.distributed:
-        packed = res[0][0]
-    else:
-        packed = np.empty((n, n), dtype=A.dtype, order="F")
-        for (idx, cols), _, _ in res:
-            if len(idx):
-                packed[:, idx] = cols.T
-    return packed, res[0][1], bool(res[0][2])
+        allp = [None] * G
+        dist.all_gather_object(allp, local, group=be.group)
+        local = [item for part in allp for item in part]
+    for idx, c in local:
+        packed[:, idx] = c
+    return packed, piv, bool(sing.value)

@@ -119,7 +119,10 @@ def _dist_worker(rank, world, port, q):
         from paper_1511_07207_b200 import gmres_solve
         An, bn, _ = O.generate_problem("general_nonsymmetric", 301, 4)
         xg, repg = gmres_solve(An, bn, np.zeros_like(bn), SolverConfig(tolerance=1e-10, restart_m=8), be)
-        q.put((rank, x, rep.iterations, rep.residual_history, xg, repg.iterations))
+        from paper_1511_07207_b200 import lu_factor_blocked
+        Au = np.asfortranarray(np.random.default_rng(600).uniform(-1, 1, (600, 600)))
+        f = lu_factor_blocked(Au, 64, be)
+        q.put((rank, x, rep.iterations, rep.residual_history, xg, (repg.iterations, np.asarray(f.pivots), f.packed)))
         dist.barrier()
         dist.destroy_process_group()
     except Exception:
@@ -150,9 +153,16 @@ def test_distributed_cg_two_processes_ipc():
     assert np.linalg.norm(xa - xo, np.inf) <= 1e-9 * np.linalg.norm(xo, np.inf)
     An, bn, _ = O.generate_problem("general_nonsymmetric", 301, 4)
     xgo, rgo = O.gmres(An, bn, np.zeros_like(bn), 1e-10, 8)
+    (gia, pa, La), (gib, pb, Lb) = gia, gib
     assert gia == gib and np.array_equal(ga, gb)
     assert abs(gia - rgo["iterations"]) <= 1
     assert np.linalg.norm(ga - xgo, np.inf) <= 1e-8 * np.linalg.norm(xgo, np.inf)
+    # block-cyclic LU over the two processes: identical factors on both ranks, the oracle's pivots
+    Au = np.asfortranarray(np.random.default_rng(600).uniform(-1, 1, (600, 600)))
+    W, piv, _ = O.lu_factor_blocked(Au, 64)
+    assert np.array_equal(pa, pb) and np.array_equal(La, Lb)
+    assert np.array_equal(pa, piv)
+    assert np.abs(La - W).max() <= 100 * 600 * np.finfo(np.float64).eps
 
 
 @pytest.mark.parametrize("devices,m,orth", [([0], 20, "modified"), ([0, 0], 20, "modified"),
@@ -199,11 +209,13 @@ def test_sharded_gmres_fp32_and_errors():
     assert r1.converged
 
 
-@pytest.mark.parametrize("devices,n,b", [([0], 300, 64), ([0, 0], 600, 64), ([0, 0, 0], 777, 32)])
+@pytest.mark.parametrize("devices,n,b", [([0], 300, 64), ([0, 0], 600, 64), ([0, 0, 0], 777, 32),
+                                         ([0, 0], 1100, 64), ([0, 0, 0, 0], 2100, 48)])
 def test_sharded_lu_matches_oracle(devices, n, b):
-    """direct.lu_factor_blocked with the columns dealt block-cyclically to the shards:
-    the pivot sequence equals the oracle's, the factors agree within the blocked-vs-
-    unblocked bound, lu_solve solves."""
+    """direct.lu_factor_blocked with the columns dealt block-cyclically to the shards
+    (ds_lu_block_cyclic: panels broadcast over peer memory, look-ahead): the pivot sequence
+    equals the oracle's, the factors agree within the blocked-vs-unblocked bound, lu_solve
+    solves."""
     from paper_1511_07207_b200 import get_backend, lu_factor_blocked, lu_solve
 
     A = np.asfortranarray(np.random.default_rng(n).uniform(-1, 1, (n, n)))
