@@ -836,10 +836,7 @@ def bench_sharded_cg(args, torch, dev, local):
     barrier()
     lu = None
     if multi and not getattr(args, "only_cg", False):
-        from paper_1511_07207_b200.distributed import CudaShardOps, TorchComm
-        ops = CudaShardOps(gen.ctx)
-        ops.bind_current_stream()
-        lu = bench_block_cyclic_lu(args, torch, dev, TorchComm(), ops)
+        lu = bench_block_cyclic_lu(args, torch, dev, be)
     if q == 0:
         value = iters * args.steps / (ms / 1e3)
         unit = f"CG iters/s (n={n} fp64)"
@@ -865,49 +862,54 @@ def bench_sharded_cg(args, torch, dev, local):
             "timing": "max over ranks of CUDA-event time"}), flush=True)
 
 
-def bench_block_cyclic_lu(args, torch, dev, comm, ops):
+def bench_block_cyclic_lu(args, torch, dev, be):
     """1-D block-cyclic LU (b=64, NB-wide column blocks dealt round-robin) of a uniform
     U[-1,1] n x n matrix (every column block seeded by its index, so the matrix does not
-    depend on N); GFLOP/s of 2n^3/3, max over ranks of the CUDA-event time."""
+    depend on N), factored in the library (ds_lu_block_cyclic: panels broadcast over peer
+    memory); GFLOP/s of 2n^3/3, max over ranks of the CUDA-event time."""
     import torch.distributed as dist
 
-    from paper_1511_07207_b200.distributed import local_blocks, lu_factor_block_cyclic, outer_block
+    from paper_1511_07207_b200.device import DeviceArray, _padded_ld
+    from paper_1511_07207_b200.distributed import local_blocks, outer_block
+    from paper_1511_07207_b200.sharded import lu_block_cyclic_device
 
     n, b = args.lu_n5, 64
-    G, q = comm.size, comm.rank
+    G, q = be.nshards, be.local_ranks[0]
     NB = outer_block(b, n)
     blocks = local_blocks(-(-n // NB), q, G)
     ncols = sum(min(NB, n - k * NB) for k in blocks)
+    sctx = be.shard_contexts[0]
+    W = DeviceArray(sctx, (n, max(ncols, 1)), np.float64, ld=_padded_ld(n))
+    tW = torch.as_tensor(W, device=dev)  # (n, ncols) view, column-major
 
     def make():
-        W = torch.empty((ncols, n), dtype=torch.float64, device=dev)
         c0 = 0
         for k in blocks:
             w = min(NB, n - k * NB)
             g = torch.Generator(device=dev)
             g.manual_seed(1000 + k)
-            W[c0:c0 + w] = torch.rand((w, n), dtype=torch.float64, device=dev, generator=g).mul_(2.0).sub_(1.0)
+            tW[:, c0:c0 + w] = torch.rand((w, n), dtype=torch.float64, device=dev, generator=g).mul_(2.0).sub_(1.0).t()
             c0 += w
-        return W
+        torch.cuda.synchronize()
 
-    W = make()
-    lu_factor_block_cyclic(W, n, b, comm, ops)  # warm-up
-    W = make()
-    torch.cuda.synchronize()
-    comm.barrier()
+    make()
+    lu_block_cyclic_device(be, [W], n, b, np.float64)  # warm-up
+    make()
+    dist.barrier()
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    piv, sing = lu_factor_block_cyclic(W, n, b, comm, ops)
+    piv, sing = lu_block_cyclic_device(be, [W], n, b, np.float64)
     e1.record(stream)
     torch.cuda.synchronize()
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
     tf = 2.0 * n ** 3 / 3.0 / (ms / 1e3) / 1e12
-    del W
+    del tW, W
     torch.cuda.empty_cache()
-    return {"workload": f"1-D block-cyclic LU b=64 (NB={NB} column blocks) uniform U[-1,1] n={n} fp64 over {G} GPUs",
+    return {"workload": f"1-D block-cyclic LU b=64 (NB={NB} column blocks) uniform U[-1,1] n={n} fp64 over {G} GPUs "
+                        "(ds_lu_block_cyclic, device-resident)",
             "value": round(tf * 1e3, 1), "unit": "GFLOP/s", "ms": round(ms, 2), "singular": sing,
             "fp64_peak_tflops_per_gpu": 37.1, "frac_of_aggregate_fp64_peak": round(tf / (37.1 * G), 4)}
 

@@ -354,10 +354,7 @@ def lu_factor_block_cyclic_api(A, b: int, be: ShardedB200Backend):
             d.upload(np.asfortranarray(A[:, idx]))
         blocks.append(d)
         cols.append(idx)
-    piv = np.empty(n, dtype=np.int64)
-    sing = ctypes.c_int32(0)
-    _lib.check(be.ctx.lib.ds_lu_block_cyclic(ss.handle, ss.dcode, _ptr_array([d.ptr for d in blocks]), ld, NB,
-                                             max(int(b), 1), piv.ctypes.data_as(c_void_p), ctypes.byref(sing)))
+    piv, singular = lu_block_cyclic_device(be, blocks, n, b, A.dtype)
     packed = np.empty((n, n), dtype=A.dtype, order="F")
     local = [(idx, d.to_host()[:, : len(idx)]) for idx, d in zip(cols, blocks) if len(idx)]
     if be.distributed:  # every rank returns the whole factorization
@@ -368,4 +365,20 @@ def lu_factor_block_cyclic_api(A, b: int, be: ShardedB200Backend):
         local = [item for part in allp for item in part]
     for idx, c in local:
         packed[:, idx] = c
-    return packed, piv, bool(sing.value)
+    return packed, piv, singular
+
+
+def lu_block_cyclic_device(be: ShardedB200Backend, blocks, n: int, b: int, dtype):
+    """Factor device-resident block-cyclic column blocks in place (blocks[i]: the n x cols
+    DeviceArray of local shard i, NB = distributed.outer_block(b, n) wide blocks in
+    increasing global order).  Returns (pivots, singular)."""
+    from . import distributed as D
+
+    NB = D.outer_block(b, n)
+    ss = be.shardset(n, dtype, kind="lu", nb=NB)
+    piv = np.empty(n, dtype=np.int64)
+    sing = ctypes.c_int32(0)
+    _lib.check(be.ctx.lib.ds_lu_block_cyclic(ss.handle, ss.dcode, _ptr_array([d.ptr for d in blocks]),
+                                             blocks[0].ld, NB, max(int(b), 1), piv.ctypes.data_as(c_void_p),
+                                             ctypes.byref(sing)))
+    return piv, bool(sing.value)
