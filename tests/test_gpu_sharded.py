@@ -227,3 +227,33 @@ def test_sharded_lu_matches_oracle(devices, n, b):
     rhs = np.ones(n)
     x = lu_solve(f, rhs)
     assert np.linalg.norm(A @ x - rhs) <= 1e-10 * np.linalg.norm(A, 1) * np.linalg.norm(x)
+
+
+def test_sharded_edge_cases():
+    """Edge cases through the sharded engines (2 shards): CG from the exact solution (0
+    iterations), GMRES happy breakdown on the identity, a singular block-cyclic LU, fp32
+    block-cyclic LU against the oracle."""
+    from paper_1511_07207_b200 import SolverConfig, cg_solve, get_backend, gmres_solve, lu_factor_blocked
+
+    be = get_backend("b200", devices=[0, 0])
+    A, b = _spd(160, 21)
+    xs = np.linalg.solve(A, b)
+    x, rep = cg_solve(A, b, xs, SolverConfig(tolerance=1e-8), be)
+    xo, ro = O.cg(A, b, xs, 1e-8)
+    assert rep.iterations == ro["iterations"] and rep.converged
+    I = np.asfortranarray(np.eye(90))
+    bi = np.random.default_rng(3).standard_normal(90)
+    xg, rg = gmres_solve(I, bi, np.zeros(90), SolverConfig(tolerance=1e-10, restart_m=10), be)
+    xgo, rgo = O.gmres(I, bi, np.zeros(90), 1e-10, 10)
+    assert rg.converged and rg.iterations == rgo["iterations"] and rg.breakdown == rgo["breakdown"]
+    assert np.allclose(xg, bi)
+    S = np.asfortranarray(np.random.default_rng(4).uniform(-1, 1, (700, 700)))
+    S[:, 400] = 0.0
+    f = lu_factor_blocked(S, 64, be)
+    W, piv, sing = O.lu_factor_blocked(S, 64)
+    assert f.singular == bool(sing) and np.array_equal(np.asarray(f.pivots), piv)
+    A32 = np.asfortranarray(np.random.default_rng(5).uniform(-1, 1, (520, 520)).astype(np.float32))
+    f32 = lu_factor_blocked(A32, 32, be)
+    W32, piv32, _ = O.lu_factor_blocked(A32, 32)
+    assert f32.packed.dtype == np.float32 and np.array_equal(np.asarray(f32.pivots), piv32)
+    assert np.abs(f32.packed - W32).max() <= 100 * 520 * np.finfo(np.float32).eps
