@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <ctime>
@@ -950,23 +951,41 @@ __global__ void __launch_bounds__(256)
   __shared__ int S[kPlanMax];             // slot swapped with position k
   __shared__ int rank[kPlanMax];          // compact index of an outside row (first occurrence)
   __shared__ int s_nout;
+  // outside rows -> their first position k: an open-addressing table (load <= 1/2), so the
+  // first-occurrence test is O(cnt) instead of a scan of all earlier pivots per entry
+  constexpr int kH = 2 * kPlanMax;
+  __shared__ unsigned long long hkey[kH];
+  __shared__ int hfirst[kH];
   const int cnt = (int)(bf - kb);
   const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < kH; i += blockDim.x) {
+    hkey[i] = ~0ull;
+    hfirst[i] = INT_MAX;
+  }
   for (int k = tid; k < cnt; k += blockDim.x) P[k] = piv[kb + k];
   __syncthreads();
-  // first occurrence of each outside row
+  auto slot_of = [&](unsigned long long key) {
+    unsigned h = (unsigned)((key * 0x9E3779B97F4A7C15ull) >> 40) & (kH - 1);
+    while (hkey[h] != key) h = (h + 1) & (kH - 1);
+    return h;
+  };
   for (int k = tid; k < cnt; k += blockDim.x) {
-    int f = 0;
-    if (P[k] >= bf) {
-      f = 1;
-      for (int j = 0; j < k; ++j)
-        if (P[j] == P[k]) {
-          f = 0;
-          break;
-        }
+    if (P[k] < bf) continue;
+    const unsigned long long key = (unsigned long long)P[k];
+    unsigned h = (unsigned)((key * 0x9E3779B97F4A7C15ull) >> 40) & (kH - 1);
+    while (true) {
+      const unsigned long long prev = atomicCAS(&hkey[h], ~0ull, key);
+      if (prev == ~0ull || prev == key) {
+        atomicMin(&hfirst[h], k);
+        break;
+      }
+      h = (h + 1) & (kH - 1);
     }
-    rank[k] = f;
   }
+  __syncthreads();
+  // first occurrence of each outside row
+  for (int k = tid; k < cnt; k += blockDim.x)
+    rank[k] = P[k] >= bf && hfirst[slot_of((unsigned long long)P[k])] == k ? 1 : 0;
   __syncthreads();
   if (tid < 32) {  // exclusive scan of the first-occurrence flags
     int base = 0;
@@ -988,11 +1007,7 @@ __global__ void __launch_bounds__(256)
     } else {
       int r = rank[k];
       if (r < 0) {
-        for (int j = 0; j < k; ++j)
-          if (P[j] == p) {
-            r = rank[j];
-            break;
-          }
+        r = rank[hfirst[slot_of((unsigned long long)p)]];
       } else {
         home[cnt + r] = p;
         orig[cnt + r] = p;
