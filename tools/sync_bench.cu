@@ -60,7 +60,7 @@ __global__ void bench(int mode, int rounds, unsigned* bar, double* cand, uint64_
       }
     } else {
       const uint32_t ep = (uint32_t)r + 1;
-      const int stride = mode == 5 ? 16 : 4;
+      const int stride = mode >= 5 ? 16 : 4;
       uint64_t* mine = hdr + ((size_t)(r & 1) * G + blockIdx.x) * stride;
       if (threadIdx.x == 0) {
         st_relaxed(mine, ((uint64_t)ep << 32) | 1u);
@@ -81,6 +81,35 @@ __global__ void bench(int mode, int rounds, unsigned* bar, double* cand, uint64_
               break;
             }
           }
+        }
+        __syncthreads();
+      } else if (mode == 6 || mode == 7) {
+        // the LU poller pattern: one warp, 128-B padded headers, pending mask (mode 7: 1 word per header)
+        if (threadIdx.x < 32) {
+          const int lane = threadIdx.x;
+          uint64_t x[5][3];
+          unsigned pending = 0;
+          for (int q = 0; q < 5; ++q)
+            if (lane + 32 * q < (int)G) pending |= 1u << q;
+          while (pending) {
+#pragma unroll
+            for (int q = 0; q < 5; ++q)
+              if (pending >> q & 1u) {
+                const uint64_t* h = hdr + ((size_t)(r & 1) * G + lane + 32 * q) * 16;
+                x[q][0] = ld_relaxed(h);
+                if (mode == 6) {
+                  x[q][1] = ld_relaxed(h + 1);
+                  x[q][2] = ld_relaxed(h + 2);
+                } else {
+                  x[q][1] = x[q][2] = x[q][0];
+                }
+              }
+#pragma unroll
+            for (int q = 0; q < 5; ++q)
+              if ((pending >> q & 1u) && (x[q][0] >> 32) == ep && (x[q][1] >> 32) == ep && (x[q][2] >> 32) == ep)
+                pending &= ~(1u << q);
+          }
+          acc += (double)(x[0][0] & 7);
         }
         __syncthreads();
       } else {
@@ -113,6 +142,34 @@ __global__ void bench(int mode, int rounds, unsigned* bar, double* cand, uint64_
   if (acc == 12345.678) out[1] = 1;
 }
 
+// cluster exchange: every CTA writes its candidate into every CTA's shared memory
+// (DSMEM), then one cluster barrier; rounds of (write, barrier, reduce)
+__global__ void bench_cluster(int rounds, long long* out) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ double slots[2][16];
+  const unsigned me = cl.block_rank(), G = cl.num_blocks();
+  double acc = 0;
+  cl.sync();
+  long long t0 = clock64();
+  for (int r = 0; r < rounds; ++r) {
+    const int par = r & 1;
+    if (threadIdx.x < G) {
+      double* dst = cl.map_shared_rank(&slots[par][0], threadIdx.x);
+      dst[me] = (double)(r + me);
+    }
+    cl.sync();
+    if (threadIdx.x < 32) {
+      double v = threadIdx.x < G ? slots[par][threadIdx.x] : 0.0;
+      for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+      acc += v;
+    }
+  }
+  long long t1 = clock64();
+  if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = t1 - t0;
+  if (acc == 12345.678) out[1] = 1;
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -128,9 +185,35 @@ int main() {
   cudaMalloc(&out, 64);
   cudaMemset(cand, 0, 8 * 8192);
   const char* names[] = {"fence+atomic barrier", "red.release barrier", "barrier + 2 dependent L2 loads",
-                         "LL all threads poll", "LL one warp polls", "LL padded lines, all threads"};
-  for (int G : {148, 74, 37}) {
-    for (int mode = 0; mode < 6; ++mode) {
+                         "LL all threads poll", "LL one warp polls", "LL padded lines, all threads",
+                         "LL padded, one warp, pending mask", "LL padded, one warp, 1 word"};
+  for (int G : {2, 4, 8, 16}) {
+    cudaFuncSetAttribute(bench_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(128);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const int rounds = 20000;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    cudaLaunchKernelEx(&cfg, bench_cluster, rounds, out);
+    cudaEventRecord(e1);
+    cudaError_t err = cudaDeviceSynchronize();
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("cluster G=%2d DSMEM write + cluster.sync     %7.3f us/round (%s)\n", G, 1e3 * ms / rounds,
+           cudaGetErrorString(err));
+  }
+  for (int G : {148, 74, 37, 16, 10}) {
+    for (int mode = 0; mode < 8; ++mode) {
       const int rounds = 2000;
       cudaMemset(bar, 0, 256);
       cudaMemset(hdr, 0, 8 * 16 * 2 * 1024);
