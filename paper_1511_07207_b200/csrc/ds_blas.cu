@@ -205,25 +205,71 @@ GemvPlan gemv_wide_plan(ds_ctx* ctx, int64_t m, int64_t n, size_t elem) {
   return p;
 }
 
+// Prefetch (pf > 0, full row tiles): before griddepcontrol.wait — i.e. while the previous
+// kernel (the orthogonalisation cluster) still runs and HBM is otherwise idle — one thread
+// moves the first pf columns of every column group's A tile into shared memory with
+// cp.async.bulk (each column segment of the tile is contiguous); A is not written by the
+// solver, so reading it early is safe.  The group loops then take those columns from shared
+// memory: same values, same order of accumulation (bitwise the non-prefetching kernel).
 template <typename T, int VEC, int UNR, int CS>
 __global__ void __launch_bounds__(kGemvThreads * CS)
     ds_colstream_mv_wide_kernel(const T* __restrict__ A, int64_t lda, int64_t m, int64_t n, const T* __restrict__ x,
-                                int64_t chunk, double* __restrict__ part, Gate gate) {
-  pdl_wait();  // x and the stop word come from the previous kernel
-  if (gated(gate)) return;
-  pdl_launch_dependents();
+                                int64_t chunk, double* __restrict__ part, Gate gate, int pf) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* xs = reinterpret_cast<T*>(smem_raw);
-  double* red = reinterpret_cast<double*>(smem_raw + ((size_t)chunk * sizeof(T) + 15) / 16 * 16);
+  unsigned char* region = smem_raw + ((size_t)chunk * sizeof(T) + 15) / 16 * 16;
+  T* pre = reinterpret_cast<T*>(region);       // [CS][pf][kGemvThreads * VEC]
+  double* red = reinterpret_cast<double*>(region);  // reuses the prefetch region at the end
+  constexpr int kRows = kGemvThreads * VEC;
   const int tl = threadIdx.x % kGemvThreads, grp = threadIdx.x / kGemvThreads;
   const int64_t c0 = (int64_t)blockIdx.y * chunk;
   const int64_t cn = min(chunk, n - c0);
+  const int64_t gsz = ceil_div(cn, (int64_t)CS);
+  const int64_t rbase = (int64_t)blockIdx.x * kRows;
+  // columns prefetched per group: only for full row tiles and whole groups
+  const int npf = (rbase + kRows <= m && gsz * CS == cn) ? (int)min((int64_t)pf, gsz) : 0;
+  __shared__ __align__(8) uint64_t pbar;
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&pbar);
+  if (npf > 0 && threadIdx.x == 0) {
+    constexpr unsigned colbytes = kRows * sizeof(T);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar),
+                 "r"((unsigned)(CS * npf) * colbytes)
+                 : "memory");
+    for (int g = 0; g < CS; ++g)
+      for (int jj = 0; jj < npf; ++jj) {
+        const T* src = A + (c0 + g * gsz + jj) * lda + rbase;
+        T* dst = pre + ((size_t)g * npf + jj) * kRows;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                (unsigned)__cvta_generic_to_shared(dst)),
+            "l"(src), "r"(colbytes), "r"(bar)
+            : "memory");
+      }
+  }
+  pdl_wait();  // x and the stop word come from the previous kernel
+  if (gated(gate)) {
+    if (npf > 0) {  // no bulk copy may still target the shared memory of an exited CTA
+      __syncthreads();
+      asm volatile(
+          "{\n .reg .pred P1;\n PG_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n @!P1 bra PG_%=;\n}\n" ::"r"(
+              bar)
+          : "memory");
+    }
+    return;
+  }
+  pdl_launch_dependents();
   for (int64_t j = threadIdx.x; j < cn; j += blockDim.x) xs[j] = x[c0 + j];
   __syncthreads();
-  const int64_t gsz = ceil_div(cn, (int64_t)CS);
+  if (npf > 0)
+    asm volatile(
+        "{\n .reg .pred P1;\n PW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n @!P1 bra PW_%=;\n}\n" ::"r"(
+            bar)
+        : "memory");
   const int64_t g0 = min(cn, grp * gsz), g1 = min(cn, g0 + gsz);
   using V = typename VecT<T, VEC>::type;
-  const int64_t r0 = (int64_t)blockIdx.x * (kGemvThreads * VEC) + (int64_t)tl * VEC;
+  const int64_t r0 = rbase + (int64_t)tl * VEC;
   double acc[VEC];
 #pragma unroll
   for (int e = 0; e < VEC; ++e) acc[e] = 0.0;
@@ -231,6 +277,15 @@ __global__ void __launch_bounds__(kGemvThreads * CS)
     const T* a = A + c0 * lda + r0;
     if (r0 + VEC <= m) {
       int64_t j = g0;
+      // the prefetched columns (npf > 0 only for full tiles), then the rest from HBM
+      for (int jj = 0; jj < npf; ++jj, ++j) {
+        const V v = *reinterpret_cast<const V*>(pre + ((size_t)grp * npf + jj) * kRows + tl * VEC);
+        T t[VEC];
+        vec_to_array<T, VEC>(v, t);
+        const double xv = (double)xs[j];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[e] = fma((double)t[e], xv, acc[e]);
+      }
       for (; j + UNR <= g1; j += UNR) {
         V v[UNR];
 #pragma unroll
@@ -261,6 +316,7 @@ __global__ void __launch_bounds__(kGemvThreads * CS)
       }
     }
   }
+  if (npf > 0) __syncthreads();  // every group is done with the prefetched columns: red reuses them
   if (grp > 0) {
 #pragma unroll
     for (int e = 0; e < VEC; ++e) red[(size_t)(grp - 1) * kGemvThreads * VEC + tl * VEC + e] = acc[e];
@@ -287,11 +343,32 @@ int gemv_partial_wide_pdl_launch(ds_ctx* ctx, const GemvPlan& p, const T* A, int
     return DS_EINVAL;
   }
   const int kWideGroups = wide_groups();
+  // A-tile prefetch depth (columns per group, DENSOLVE_GEMV_PREFETCH; 0 disables): as many as
+  // fit beside the x chunk in ~200 KB of shared memory
+  static const int pf_env = [] {
+    const char* e = getenv("DENSOLVE_GEMV_PREFETCH");
+    return e ? std::max(0, atoi(e)) : 12;
+  }();
+  const size_t xbytes = ((size_t)p.chunk * sizeof(T) + 15) / 16 * 16;
+  const size_t colbytes = (size_t)kGemvThreads * VEC * sizeof(T);
+  const size_t red_bytes = (size_t)(kWideGroups - 1) * kGemvThreads * VEC * sizeof(double);
+  const size_t budget = 200 * 1024;
+  int pf = pf_env;
+  while (pf > 0 && xbytes + (size_t)kWideGroups * pf * colbytes > budget) --pf;
+  const size_t region = std::max(red_bytes, (size_t)kWideGroups * pf * colbytes);
+  static size_t attr_done[2] = {0, 0};
+  size_t& done = attr_done[sizeof(T) == 8 ? 1 : 0];
+  if (xbytes + region > 48 * 1024 && done == 0) {
+    DS_CUDA(cudaFuncSetAttribute(ds_colstream_mv_wide_kernel<T, VEC, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(budget + 16 * 1024)));
+    DS_CUDA(cudaFuncSetAttribute(ds_colstream_mv_wide_kernel<T, VEC, 8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(budget + 16 * 1024)));
+    done = 1;
+  }
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3((unsigned)p.rowtiles, (unsigned)p.nchunks);
   lc.blockDim = dim3(kGemvThreads * kWideGroups);
-  lc.dynamicSmemBytes = ((size_t)p.chunk * sizeof(T) + 15) / 16 * 16 +
-                        (size_t)(kWideGroups - 1) * kGemvThreads * VEC * sizeof(double);
+  lc.dynamicSmemBytes = xbytes + region;
   lc.stream = ctx->stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -300,9 +377,9 @@ int gemv_partial_wide_pdl_launch(ds_ctx* ctx, const GemvPlan& p, const T* A, int
   lc.numAttrs = 1;
   const int64_t m = p.m, n = p.n, chunk = p.chunk;
   if (kWideGroups == 2)
-    DS_CUDA(cudaLaunchKernelEx(&lc, ds_colstream_mv_wide_kernel<T, VEC, 8, 2>, A, lda, m, n, x, chunk, part, stop));
+    DS_CUDA(cudaLaunchKernelEx(&lc, ds_colstream_mv_wide_kernel<T, VEC, 8, 2>, A, lda, m, n, x, chunk, part, stop, pf));
   else
-    DS_CUDA(cudaLaunchKernelEx(&lc, ds_colstream_mv_wide_kernel<T, VEC, 8, 4>, A, lda, m, n, x, chunk, part, stop));
+    DS_CUDA(cudaLaunchKernelEx(&lc, ds_colstream_mv_wide_kernel<T, VEC, 8, 4>, A, lda, m, n, x, chunk, part, stop, pf));
   count_launch(ctx);
   DS_CHECK_LAUNCH();
   return DS_OK;

@@ -885,10 +885,18 @@ __global__ void __launch_bounds__(kOrthThreads, 2)
 // y = H[:inner,:inner]^-1 g[:inner] (backward_substitution, direct.py:139-152): the
 // block stages the upper triangle in shared memory, then one thread runs the
 // dependent recurrence out of shared memory (no global round trip per term)
+// inner < 0: the cycle's stop step is read on the device (inner = min(stop_k, -inner)) and
+// y is written up to -inner with zeros past it, so the host enqueues the cycle's tail
+// without a readback (the x update then runs over -inner columns).
 template <typename T>
 __global__ void gm_lsq_kernel(const T* H, int64_t ldh, const T* g, int inner, T* y, GmDev* st) {
   __shared__ T Hs[64][65];
   __shared__ T ys[64];
+  const int ypad = inner < 0 ? -inner : inner;
+  if (inner < 0) {
+    inner = (int)min(st->stop_k, (int64_t)ypad);
+    for (int i = inner + (int)threadIdx.x; i < ypad; i += blockDim.x) y[i] = T(0);
+  }
   for (int idx = threadIdx.x; idx < inner * inner; idx += blockDim.x) {
     const int i = idx % inner, j = idx / inner;
     if (i <= j) Hs[i][j] = H[i + (int64_t)j * ldh];
@@ -940,14 +948,29 @@ __global__ void gm_lsq_global_kernel(const T* H, int64_t ldh, const T* g, int in
 }
 
 // cycle start: V[:,0] = scal(1/beta, r); g = beta e1 (krylov.py:116-123)
+// cycle start: V[:,0] = scal(1/beta, r), the rest of V, H, Hraw, g, cs, sn zeroed, g = beta e1
+// (krylov.py:116-123), and the device state of the cycle initialised (one launch instead of
+// four memsets, a host-to-device copy and the scaling kernel)
 template <typename T>
-__global__ void gm_cycle_start_kernel(int64_t n, const T* __restrict__ r, T* __restrict__ v0,
-                                      double beta, T* g) {
+__global__ void gm_cycle_start_kernel(int64_t n, const T* __restrict__ r, T* __restrict__ V, int64_t vlen,
+                                      T* __restrict__ H, T* __restrict__ Hraw, int64_t hlen, T* __restrict__ g,
+                                      int64_t glen, double beta, double bnorm, int64_t m, GmDev* st) {
   const T s = (T)(1.0 / beta);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    v0[i] = mul_rn(s, r[i]);
-  if (blockIdx.x == 0 && threadIdx.x == 0) g[0] = (T)beta;
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = i0; i < vlen; i += step) V[i] = i < n ? mul_rn(s, r[i]) : T(0);
+  for (int64_t i = i0; i < hlen; i += step) {
+    H[i] = T(0);
+    Hraw[i] = T(0);
+  }
+  for (int64_t i = i0; i < glen; i += step) g[i] = i == 0 ? (T)beta : T(0);
+  if (i0 == 0) {
+    GmDev d{};
+    d.stop_k = m;
+    d.bad_row = -1;
+    d.beta = beta;
+    d.bnorm = bnorm;
+    *st = d;
+  }
 }
 
 __global__ void finish_resid_kernel(const double* red, int nblk, double* out) {
@@ -1098,13 +1121,21 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
   DS_TRY(ctx_hostbuf(ctx, (size_t)(128 + m + 64) * sizeof(double), (void**)&hbuf));
 
   // ||b|| via nrm2 (krylov.py:87) and the plain ||b|| of relative_residual (core.py:207)
+  // read back together with the first cycle's r = b - A x0 (one host synchronisation)
   int nb = 0;
   DS_TRY(ssq_launch<T>(ctx, n, b, red_b, &nb));
   DS_TRY(finish_ssq(ctx, red_b, nb, scal));
   int nb2 = 0;
   DS_TRY(dot_launch<T>(ctx, n, b, b, red_a, &nb2));
   DS_TRY(finish_sum(ctx, red_a, nb2, scal + 1));
-  DS_CUDA(cudaMemcpyAsync(hbuf, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  if (x != x0) DS_CUDA(cudaMemcpyAsync(x, x0, n * sizeof(T), cudaMemcpyDeviceToDevice, ctx->stream));
+  {
+    int rb = 0;
+    DS_TRY(gemv_launch<T>(ctx, gp, A, lda, x, r, part, EPI_RESID, b, red_a, &rb));
+    finish_resid_kernel<<<1, 256, 0, ctx->stream>>>(red_a, rb, scal + 2);
+    count_launch(ctx);
+  }
+  DS_CUDA(cudaMemcpyAsync(hbuf, scal, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   DS_CUDA(cudaStreamSynchronize(ctx->stream));
   const double bnorm = hbuf[0];
   const double bnorm_plain = sqrt(hbuf[1]);
@@ -1112,7 +1143,6 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
     set_error("||b|| = 0");
     return DS_EDEGRHS;
   }
-  if (x != x0) DS_CUDA(cudaMemcpyAsync(x, x0, n * sizeof(T), cudaMemcpyDeviceToDevice, ctx->stream));
 
   std::vector<double> history;
   std::vector<int64_t> cycles;
@@ -1129,8 +1159,8 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
   int64_t residual_evals = 0;
   // the previous cycle's true residual (same x, same kernels) is this cycle's r and beta:
   // reused instead of recomputed (still tallied as the reference's evaluation)
-  bool have_r = false;
-  double next_beta = 0.0;
+  bool have_r = true;
+  double next_beta = hbuf[2];
   while (true) {
     // r = b - A x ; beta = nrm2(r)   (krylov.py:104-106)
     ++residual_evals;
@@ -1158,18 +1188,9 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
     cycles.push_back(total_it);
     const double cycle_start_res = relres;
 
-    // fresh cycle state (krylov.py:116-123)
-    DS_CUDA(cudaMemsetAsync(V, 0, (size_t)ldv * (m + 1) * sizeof(T), ctx->stream));
-    DS_CUDA(cudaMemsetAsync(H, 0, (size_t)ldh * m * sizeof(T), ctx->stream));
-    DS_CUDA(cudaMemsetAsync(Hraw, 0, (size_t)ldh * m * sizeof(T), ctx->stream));
-    DS_CUDA(cudaMemsetAsync(g, 0, (size_t)(m + 2) * sizeof(T) * 3, ctx->stream));
-    GmDev init{};
-    init.stop_k = m;
-    init.beta = beta;
-    init.bnorm = bnorm;
-    init.bad_row = -1;
-    DS_CUDA(cudaMemcpyAsync(st, &init, sizeof(GmDev), cudaMemcpyHostToDevice, ctx->stream));
-    gm_cycle_start_kernel<T><<<vg, kT, 0, ctx->stream>>>(n, r, V, beta, g);
+    // fresh cycle state (krylov.py:116-123); g, cs, sn are contiguous
+    gm_cycle_start_kernel<T><<<vg, kT, 0, ctx->stream>>>(n, r, V, ldv * (m + 1), H, Hraw, ldh * m, g,
+                                                         3 * (m + 2), beta, bnorm, m, st);
     count_launch(ctx);
     DS_CHECK_LAUNCH();
 
@@ -1182,7 +1203,11 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
     GmDev* h_st = reinterpret_cast<GmDev*>(hbuf + 64);
     double* h_est = hbuf + 128;
     static_assert(sizeof(GmDev) <= 64 * sizeof(double), "GmDev staging slot");
+    // m <= 64 without a sink: the tail (LS solve, x update, true residual) reads the stop step
+    // on the device, so the cycle needs one host synchronisation (after the true residual)
+    const bool dev_tail = !sink && m <= 64;
     while (true) {
+      if (k > 0 && dev_tail) break;
       if (k > 0) {
         DS_CUDA(cudaMemcpyAsync(h_st, st, sizeof(GmDev), cudaMemcpyDeviceToHost, ctx->stream));
         DS_CUDA(cudaMemcpyAsync(h_est, est, (size_t)m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1287,14 +1312,22 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
       DS_CHECK_LAUNCH();
       chunk = std::min<int64_t>(chunk * 2, 32);
     }
-    GmDev hst = *h_st;  // read by the chunk loop's final readback
-    const int inner = (int)std::min<int64_t>(hst.stop_k, m);
-    const bool happy = hst.happy != 0;
-    for (int i = 0; i < inner; ++i) history.push_back(h_est[i]);
-    total_it += inner;
+    int inner = (int)m;
+    bool happy = false;
+    if (!dev_tail) {
+      const GmDev hst = *h_st;  // read by the chunk loop's final readback
+      inner = (int)std::min<int64_t>(hst.stop_k, m);
+      happy = hst.happy != 0;
+      for (int i = 0; i < inner; ++i) history.push_back(h_est[i]);
+      total_it += inner;
+    }
 
-    // cycle end: y = H^-1 g ; x += V y   (krylov.py:166-167)
-    if (inner <= 64)
+    // cycle end: y = H^-1 g ; x += V y   (krylov.py:166-167).  dev_tail: the stop step is read
+    // on the device and the update runs over all m columns with y = 0 past it (one column
+    // chunk for m <= 64, the same order of accumulation)
+    if (dev_tail)
+      gm_lsq_kernel<T><<<1, 256, 0, ctx->stream>>>(H, ldh, g, -(int)m, y, st);
+    else if (inner <= 64)
       gm_lsq_kernel<T><<<1, 256, 0, ctx->stream>>>(H, ldh, g, inner, y, st);
     else
       gm_lsq_global_kernel<T><<<1, 32, 0, ctx->stream>>>(H, ldh, g, inner, y, st);
@@ -1340,7 +1373,15 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
       DS_CUDA(cudaMemcpyAsync(hbuf, scal + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost,
                               ctx->stream));
       DS_CUDA(cudaMemcpyAsync(h_st, st, sizeof(GmDev), cudaMemcpyDeviceToHost, ctx->stream));
+      if (dev_tail)
+        DS_CUDA(cudaMemcpyAsync(h_est, est, (size_t)m * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
       DS_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (dev_tail) {
+        inner = (int)std::min<int64_t>(h_st->stop_k, m);
+        happy = h_st->happy != 0;
+        for (int i = 0; i < inner; ++i) history.push_back(h_est[i]);
+        total_it += inner;
+      }
       DS_TRY(singular_check());  // the least-squares solve's zero-diagonal flag (krylov.py:166)
     }
     have_r = true;
