@@ -1157,24 +1157,14 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
   };
 
   int64_t residual_evals = 0;
-  // the previous cycle's true residual (same x, same kernels) is this cycle's r and beta:
-  // reused instead of recomputed (still tallied as the reference's evaluation)
-  bool have_r = true;
+  // r = b - A x and beta: the first cycle's were computed above with ||b||; every later
+  // cycle's are the previous cycle's true residual (same x, same kernels), reused instead of
+  // recomputed (still tallied as the reference's evaluation)
   double next_beta = hbuf[2];
   while (true) {
     // r = b - A x ; beta = nrm2(r)   (krylov.py:104-106)
     ++residual_evals;
-    double beta = next_beta;
-    if (!have_r) {
-      int rb = 0;
-      DS_TRY(gemv_launch<T>(ctx, gp, A, lda, x, r, part, EPI_RESID, b, red_a, &rb));
-      finish_resid_kernel<<<1, 256, 0, ctx->stream>>>(red_a, rb, scal + 2);
-      count_launch(ctx);
-      DS_CUDA(cudaMemcpyAsync(hbuf, scal + 2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-      DS_CUDA(cudaStreamSynchronize(ctx->stream));
-      beta = hbuf[0];
-    }
-    have_r = false;
+    const double beta = next_beta;
     const double relres = beta / bnorm;
     if (total_it == 0) history.push_back(relres);
     if (relres <= tol) {
@@ -1384,7 +1374,6 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
       }
       DS_TRY(singular_check());  // the least-squares solve's zero-diagonal flag (krylov.py:166)
     }
-    have_r = true;
     next_beta = hbuf[0];
     const double true_res = sqrt(hbuf[1]) / bnorm_plain;
     if (happy || history.back() <= tol || true_res <= tol) {  // krylov.py:172-175
