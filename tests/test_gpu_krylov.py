@@ -206,6 +206,26 @@ def test_gmres_arnoldi_workspace_invariants(backend):
         assert np.linalg.norm(A @ ws["V"][:, :k] - V @ H) <= 10 * k * u * np.linalg.norm(A)
 
 
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("n,m,tol", [(200, 30, 1e-9), (333, 7, 1e-10), (96, 64, 1e-12), (4096, 30, 1e-8)])
+def test_gmres_device_tail_matches_host_tail(backend, prec, n, m, tol):
+    """Without a workspace sink (m <= 64) the cycle tail (LS solve, x update, true residual)
+    reads the stop step on the device and updates x over all m columns with y = 0 past it;
+    with a sink the host reads the stop step first and updates over `inner` columns.  Both
+    must give the same x bits, history and cycles, including cycles that stop mid-way."""
+    if prec == "f32":
+        tol = max(tol, 1e-5)
+    A, b, _ = nonsym(n, 11, prec)
+    cfg = SolverConfig(tolerance=tol, restart_m=m)
+    x1, r1 = gmres_solve(A, b, np.zeros_like(b), cfg, backend)
+    x2, r2 = gmres_solve(A, b, np.zeros_like(b), cfg, backend, workspace_sink=[])
+    assert r1.converged and r2.converged
+    assert r1.iterations == r2.iterations and r1.restart_cycles == r2.restart_cycles
+    assert r1.iterations % m != 0 or len(r1.restart_cycles) > 1  # a partial or multi-cycle run
+    np.testing.assert_array_equal(x1, x2)
+    assert r1.residual_history == r2.residual_history
+
+
 def test_gmres_ls_residual_monotone(backend):
     A, b, _ = nonsym(128, 8)
     x, rep = gmres_solve(A, b, np.zeros_like(b), SolverConfig(tolerance=1e-10, restart_m=20), backend)
