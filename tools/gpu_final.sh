@@ -4,7 +4,7 @@ tag=${1:-r02f}
 out=gpurun_out; mkdir -p $out
 NCU=/usr/local/cuda/bin/ncu
 timeout 1200 python -m pytest tests -m gpu -q > $out/pytest_gpu_$tag.log 2>&1; echo "pytest exit $?"; tail -2 $out/pytest_gpu_$tag.log
-timeout 900 python bench.py > $out/bench_$tag.json 2> $out/bench_$tag.err; echo "bench exit $?"
+t0=$(date +%s); timeout 900 python bench.py > $out/bench_$tag.json 2> $out/bench_$tag.err; echo "bench exit $? ($(( $(date +%s) - t0 )) s)"
 timeout 300 python bench.py --force-sharded --only-cg --steps 5 --warmup 3 > $out/bench_fs_$tag.json 2>/dev/null; echo "fs exit $?"
 timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file $out/launches_bench_$tag.csv \
   python bench.py --steps 1 --warmup 3 --only-cg --no-cpu-baseline > /dev/null 2>&1; echo "list bench $?"
