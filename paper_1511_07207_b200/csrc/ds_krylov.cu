@@ -265,6 +265,7 @@ struct GmDev {
   int64_t bad_row;
   double beta;     // ||r0|| of the cycle
   double bnorm;    // nrm2(b)
+  int64_t givens_done;  // cluster path with deferred Givens: columns rotated so far
 };
 
 // multi-dot  h_j = V[:,j] . w  for j < kc (one pass over V, w kept in registers)
@@ -688,12 +689,76 @@ __global__ void __launch_bounds__(kArnThreads)
 constexpr int kOrthThreads = 512;
 constexpr unsigned kOrthMaxCluster = 16;  // the launch uses 16 or 8
 
+// Givens step of column kk (krylov.py:146-163) by ONE thread, from shared-memory copies:
+// hc = raw H[0..kk+1, kk], css / sns = the rotations of the earlier columns.  The running
+// H[j+1] is carried in a register (no store -> load round trip per rotation).  Writes the
+// rotated column, cs / sn[kk], g[kk..kk+1] and est[kk]; returns the estimate.
+template <typename T>
+__device__ __forceinline__ double gm_givens_apply(int kk, const T* hc, const T* css, const T* sns, T gk, double bnorm,
+                                                  T* H, int64_t ldh, T* g, T* cs, T* sn, double* est_out) {
+  T* Hk = H + (int64_t)kk * ldh;
+  const T col_last = hc[kk + 1];
+  T cur = hc[0];
+  for (int j = 0; j < kk; ++j) {
+    const T nxt = hc[j + 1];
+    const T c = css[j], s_ = sns[j];
+    const T t = add_rn(mul_rn(c, cur), mul_rn(s_, nxt));
+    cur = add_rn(mul_rn(-s_, cur), mul_rn(c, nxt));
+    Hk[j] = t;
+  }
+  // cur = rotated H[kk], col_last = H[kk+1]
+  const T denom = sizeof(T) == 8 ? (T)hypot((double)cur, (double)col_last) : (T)hypotf((float)cur, (float)col_last);
+  const T ck = div_rn(cur, denom), sk = div_rn(col_last, denom);
+  cs[kk] = ck;
+  sn[kk] = sk;
+  Hk[kk] = denom;
+  Hk[kk + 1] = T(0);
+  g[kk + 1] = mul_rn(-sk, gk);
+  g[kk] = mul_rn(ck, gk);
+  const double est = fabs((double)mul_rn(-sk, gk)) / bnorm;
+  est_out[kk] = est;
+  return est;
+}
+
+// one warp stages raw H[:, kk] and the earlier rotations in shared memory; the scalars the
+// chain needs at its end (g[kk], ||b||) are loaded in the same round trip
+template <typename T>
+__device__ __forceinline__ void gm_givens_stage(int kk, const T* Hraw, int64_t ldh, const T* cs, const T* sn, T* hc,
+                                                T* css, T* sns, int lane) {
+  const T* Hr = Hraw + (int64_t)kk * ldh;
+  for (int j = lane; j <= kk + 1; j += 32) hc[j] = Hr[j];
+  for (int j = lane; j < kk; j += 32) {
+    css[j] = cs[j];
+    sns[j] = sn[j];
+  }
+}
+
+// Cycle tail of the deferred-Givens cluster path: the last executed step's Givens (its
+// cluster had no successor, or the successor was gated by a happy / cap stop).
+template <typename T>
+__global__ void gm_givens_tail_kernel(int64_t kend, const T* Hraw, T* H, int64_t ldh, T* g, T* cs, T* sn,
+                                      double* est_out, GmDev* st, double tol) {
+  __shared__ T hc[66], css[64], sns[64];
+  const int64_t E = min(st->stop_k, kend);
+  if (st->givens_done >= E) return;
+  const int kk = (int)(E - 1);
+  gm_givens_stage<T>(kk, Hraw, ldh, cs, sn, hc, css, sns, (int)threadIdx.x);
+  const T gk = g[kk];
+  const double bnorm = st->bnorm;
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    const double est = gm_givens_apply<T>(kk, hc, css, sns, gk, bnorm, H, ldh, g, cs, sn, est_out);
+    if (est <= tol) st->stop_k = kk + 1;
+    st->givens_done = kk + 1;
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kOrthThreads, 2)
     arnoldi_orth_cluster_kernel(int64_t n, T* V, int64_t ldv, int k, int passes, T* H, T* Hraw, int64_t ldh, T* g,
                                 T* cs, T* sn, double* est_out, GmDev* st, double tol, int64_t total_before,
                                 int64_t cap, Gate gate, const double* __restrict__ gpart, int64_t nchunks,
-                                unsigned long long* trace) {
+                                unsigned long long* trace, int defer) {
   namespace cgr = cooperative_groups;
   pdl_wait();  // the GEMV partials, V and the stop word come from earlier kernels
   if (gated(gate)) return;
@@ -715,7 +780,9 @@ __global__ void __launch_bounds__(kOrthThreads, 2)
   __shared__ double part[2][64];                      // my CGS partials, buffer per pass
   __shared__ double inbox[2][kOrthMaxCluster];        // norm partials pushed by every CTA
   __shared__ double hs[64], hsave[64], sm[64];
-  __shared__ T hcol[64], css[64], sns[64];            // rank 0: H[:, k] and the rotations so far
+  __shared__ T hcol[66], css[64], sns[64];            // rank 0: H[:, k] and the rotations so far
+  __shared__ T ghc[66], gcs[64], gsn[64];             // defer: column k-1's Givens inputs
+  __shared__ int s_abort;                             // defer (rank 0): column k-1 stopped the cycle
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kOrthThreads / 32;
   const int64_t per = ceil_div(ceil_div(n, (int64_t)CL), 4) * 4;
   const int64_t r0 = (int64_t)rank * per;
@@ -742,11 +809,35 @@ __global__ void __launch_bounds__(kOrthThreads, 2)
     }
     wv[r] = (double)(T)s;
   }
-  if (rank == 0)
+  if (defer) {
+    // deferred Givens of column k - 1 (the previous step's estimate and stop test), by the last
+    // warp of rank 0, which has no rows here (host: rows per CTA <= kOrthThreads - 32), while
+    // the CTA sums the partials; its stop aborts this step before it writes anything
+    if (rank == 0 && warp == nw - 1) {
+      bool stop = false;
+      if (k > 0) {
+        // every load of the step in one round trip: the staged column and rotations, g[k-1],
+        // ||b|| and the done count (a chunked enqueue's tail may have rotated k-1 already)
+        gm_givens_stage<T>(k - 1, Hraw, ldh, cs, sn, ghc, gcs, gsn, lane);
+        const int64_t done = st->givens_done;
+        const T gk = g[k - 1];
+        const double bnorm = st->bnorm;
+        __syncwarp();
+        if (done == k - 1 && lane == 31) {
+          const double est = gm_givens_apply<T>(k - 1, ghc, gcs, gsn, gk, bnorm, H, ldh, g, cs, sn, est_out);
+          stop = est <= tol;
+          if (stop) st->stop_k = k;
+          st->givens_done = k;
+        }
+      }
+      if (lane == 31) s_abort = stop ? 1 : 0;
+    }
+  } else if (rank == 0) {
     for (int j = tid; j < k; j += blockDim.x) {
       css[j] = cs[j];
       sns[j] = sn[j];
     }
+  }
   __syncthreads();
   stamp(1);
   for (int ps = 0; ps < passes; ++ps) {
@@ -761,6 +852,10 @@ __global__ void __launch_bounds__(kOrthThreads, 2)
     }
     stamp(2 + 4 * ps);
     cluster.sync();
+    if (defer && ps == 0 && *cluster.map_shared_rank(&s_abort, 0)) {
+      cluster.sync();  // rank 0's flag stays readable until every CTA has seen it
+      return;
+    }
     stamp(3 + 4 * ps);
     for (int j = tid; j < kc; j += blockDim.x) {  // rank-ordered sum over the cluster (DSMEM)
       double v[kOrthMaxCluster];  // every remote load in flight before the ordered sum
@@ -846,38 +941,21 @@ __global__ void __launch_bounds__(kOrthThreads, 2)
     for (int r = tid; r < nr; r += blockDim.x) w[r0 + r] = happy ? (T)wv[r] : mul_rn(sc, (T)wv[r]);
   }
   stamp(11);
-  if (rank == 0 && tid == 0) {  // Givens, estimate, stop (krylov.py:146-163)
-    T* Hk = H + (int64_t)k * ldh;
+  if (rank == 0) {  // raw column, then Givens, estimate, stop (krylov.py:146-163)
     T* Hr = Hraw + (int64_t)k * ldh;
-    // the column from shared memory (hsave/hs of the passes), rotations in registers:
-    // the running H[j+1] is carried, so no store -> load round trip per rotation
-    T col_last = (T)hk1;
-    for (int j = 0; j <= k; ++j) Hr[j] = hcol[j];
-    Hr[k + 1] = col_last;
-    T cur = hcol[0];
-    for (int j = 0; j < k; ++j) {
-      const T nxt = hcol[j + 1];
-      const T c = css[j], s_ = sns[j];
-      const T t = add_rn(mul_rn(c, cur), mul_rn(s_, nxt));
-      cur = add_rn(mul_rn(-s_, cur), mul_rn(c, nxt));
-      Hk[j] = t;
+    for (int j = tid; j <= k; j += blockDim.x) Hr[j] = hcol[j];
+    if (tid == 0) {
+      Hr[k + 1] = (T)hk1;
+      const int64_t total = total_before + k + 1;
+      if (happy) st->happy = 1;
+      if (defer) {  // the estimate waits for the next step's cluster (or the cycle tail)
+        if (happy || total >= cap) st->stop_k = k + 1;
+      } else {
+        hcol[k + 1] = (T)hk1;
+        const double est = gm_givens_apply<T>(k, hcol, css, sns, g[k], st->bnorm, H, ldh, g, cs, sn, est_out);
+        if (happy || est <= tol || total >= cap) st->stop_k = k + 1;
+      }
     }
-    // cur = rotated H[k], col_last = H[k+1]
-    const T denom = sizeof(T) == 8 ? (T)hypot((double)cur, (double)col_last)
-                                   : (T)hypotf((float)cur, (float)col_last);
-    const T ck = div_rn(cur, denom), sk = div_rn(col_last, denom);
-    cs[k] = ck;
-    sn[k] = sk;
-    Hk[k] = denom;
-    Hk[k + 1] = T(0);
-    const T gk = g[k];
-    g[k + 1] = mul_rn(-sk, gk);
-    g[k] = mul_rn(ck, gk);
-    const double est = fabs((double)mul_rn(-sk, gk)) / st->bnorm;
-    est_out[k] = est;
-    const int64_t total = total_before + k + 1;
-    if (happy) st->happy = 1;
-    if (happy || est <= tol || total >= cap) st->stop_k = k + 1;
   }
   stamp(12);
 }
@@ -1028,6 +1106,7 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
     return !(e && e[0] == '0');
   }();
   unsigned long long* orth_trace = nullptr;
+  int orth_defer = 0;
   {
     const char* oe = getenv("DENSOLVE_GMRES_ORTH");
     const bool want = !(oe && strcmp(oe, "grid") == 0) && n <= 16 * 4096 && !big_m;
@@ -1071,6 +1150,16 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
         // read per CTA (C2: 128 KB); at n = 65536 (1.2 MB per CTA, ~40 us on 16 SMs) the
         // reduce kernel on every SM is faster
         orth_fold = ceil_div(n, (int64_t)bc) * gp.nchunks * (int64_t)sizeof(double) <= 256 * 1024;
+        // each step's Givens deferred to the next step's cluster (off the GEMV -> cluster
+        // chain) when the last warp of a CTA has no rows and the GEMV writes only its
+        // partials (a step that runs past an estimate stop then leaves no trace: the next
+        // GEMV writes scratch, the next cluster aborts before writing); DENSOLVE_ORTH_DEFER=0
+        // disables
+        static const bool defer_env = [] {
+          const char* e = getenv("DENSOLVE_ORTH_DEFER");
+          return !(e && e[0] == '0');
+        }();
+        orth_defer = defer_env && orth_fold && ceil_div(ceil_div(n, (int64_t)bc), 4) * 4 <= kOrthThreads - 32 ? 1 : 0;
       }
     }
   }
@@ -1239,7 +1328,7 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
                                      cs, sn, est, st, tol, total_it, cap, gt,
                                      orth_fold ? (const double*)part : nullptr,
                                      (int64_t)(pdl_on && wide ? wp.nchunks : gp.nchunks),
-                                     orth_trace));
+                                     orth_trace, orth_defer));
           count_launch(ctx);
           continue;
         }
@@ -1297,6 +1386,10 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
         gm_step_finish_kernel<T><<<vg, kT, 0, ctx->stream>>>(n, w, red_b, vg, H, Hraw, ldh, g, cs,
                                                              sn, (int)k, est, st, tol, total_it,
                                                              cap, gt);
+        count_launch(ctx);
+      }
+      if (orth_cl > 0 && orth_defer) {  // the last executed step's Givens
+        gm_givens_tail_kernel<T><<<1, 32, 0, ctx->stream>>>(kend, Hraw, H, ldh, g, cs, sn, est, st, tol);
         count_launch(ctx);
       }
       DS_CHECK_LAUNCH();
