@@ -1,3 +1,6 @@
+"""GMRES per-call cost split: one-cycle calls at m = 5, 10, 30, 60 for n = 4096 and 256, so
+t = fixed + m * per_step separates the call overhead from the Arnoldi step.
+python tools/gmres_overhead.py"""
 import os, sys, time
 import numpy as np, torch
 sys.path.insert(0, os.getcwd())
