@@ -271,7 +271,6 @@ struct ds_ctx {
   cudaStream_t aux = nullptr;  // low-priority stream for the swaps of already-factored L columns
   cudaStream_t copy = nullptr;  // asynchronous host->device staging (ds_upload_async)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
-  unsigned panel_seq = 0;  // LU panel launches (epochs of the LL exchange words)
   // Serialises the entry points on this context: its workspace, streams, pinned buffer
   // and events are shared state ("one solve at a time" per backend, backends.py:80-81).
   // Recursive: a GMRES workspace sink may call back into the library on this thread.
@@ -279,7 +278,10 @@ struct ds_ctx {
 };
 
 namespace ds {
-int ctx_workspace(ds_ctx* ctx, size_t bytes, void** out);
+int ctx_workspace(ds_ctx* ctx, size_t bytes, void** out);  // grow-only, zero-filled when (re)allocated
+// Epoch of the next LL exchange (LU panel, fused Arnoldi step): unique in the process, so a
+// workspace that reuses memory freed by another context can never hold a word that matches.
+unsigned next_ll_epoch();
 int ctx_hostbuf(ds_ctx* ctx, size_t bytes, void** out);
 int ctx_begin(ds_ctx* ctx);  // cudaSetDevice
 inline void count_launch(ds_ctx* ctx, int n = 1) { ctx->launches += n; }

@@ -3,6 +3,7 @@
 // Replaces the Backend staging seam (backends.py:94-100: stage_in/stage_out,
 // "preserved for a future accelerator backend") with real
 // host<->device transfers, and the F-order coercion of core.py:82-87.
+#include <atomic>
 #include <cuda_runtime.h>
 
 #include <cstdarg>
@@ -41,10 +42,17 @@ int ctx_workspace(ds_ctx* ctx, size_t bytes, void** out) {
     }
     size_t want = bytes < (1u << 20) ? (1u << 20) : bytes;
     DS_CUDA(cudaMalloc(&ctx->ws, want));
+    // the LL exchange buffers carved from it are polled before their first write
+    DS_CUDA(cudaMemsetAsync(ctx->ws, 0, want, ctx->stream));
     ctx->ws_bytes = want;
   }
   *out = ctx->ws;
   return DS_OK;
+}
+
+unsigned next_ll_epoch() {
+  static std::atomic<unsigned> ctr{0};
+  return ++ctr;
 }
 
 int ctx_hostbuf(ds_ctx* ctx, size_t bytes, void** out) {

@@ -1032,7 +1032,8 @@ __global__ void gm_lsq_global_kernel(const T* H, int64_t ldh, const T* g, int in
 template <typename T>
 __global__ void gm_cycle_start_kernel(int64_t n, const T* __restrict__ r, T* __restrict__ V, int64_t vlen,
                                       T* __restrict__ H, T* __restrict__ Hraw, int64_t hlen, T* __restrict__ g,
-                                      int64_t glen, double beta, double bnorm, int64_t m, GmDev* st) {
+                                      int64_t glen, double* __restrict__ est, double beta, double bnorm, int64_t m,
+                                      GmDev* st) {
   const T s = (T)(1.0 / beta);
   const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, step = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = i0; i < vlen; i += step) V[i] = i < n ? mul_rn(s, r[i]) : T(0);
@@ -1041,6 +1042,7 @@ __global__ void gm_cycle_start_kernel(int64_t n, const T* __restrict__ r, T* __r
     Hraw[i] = T(0);
   }
   for (int64_t i = i0; i < glen; i += step) g[i] = i == 0 ? (T)beta : T(0);
+  for (int64_t i = i0; i < m; i += step) est[i] = 0.0;  // read back whole with the device-side tail
   if (i0 == 0) {
     GmDev d{};
     d.stop_k = m;
@@ -1269,7 +1271,7 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
 
     // fresh cycle state (krylov.py:116-123); g, cs, sn are contiguous
     gm_cycle_start_kernel<T><<<vg, kT, 0, ctx->stream>>>(n, r, V, ldv * (m + 1), H, Hraw, ldh * m, g,
-                                                         3 * (m + 2), beta, bnorm, m, st);
+                                                         3 * (m + 2), est, beta, bnorm, m, st);
     count_launch(ctx);
     DS_CHECK_LAUNCH();
 
@@ -1352,7 +1354,7 @@ int gmres_impl(ds_ctx* ctx, int64_t n, const T* A, int64_t lda, const T* b, cons
           aa.k = (int)k;
           aa.passes = orth == DS_ORTH_CLASSICAL ? 1 : 2;
           aa.per = (int)arn_per;
-          aa.seq = ++ctx->panel_seq;
+          aa.seq = next_ll_epoch();
           aa.tol = tol;
           aa.ll = arn_ll;
           aa.est = est;

@@ -194,7 +194,7 @@ __device__ __forceinline__ void cta_argmax_key(unsigned long long& key, int64_t&
     wk[wid] = wkey;
     wi[wid] = widx == 0xffffffffu ? INT64_MAX : (int64_t)widx;
   }
-  __syncthreads();
+  __syncthreads();  // the poller-warp panel reaches it with every warp at the same code location
   // every warp combines the nw warp records itself (lane w reads record w): the same
   // reduction in every warp, no second barrier
   const int nw = (int)(blockDim.x >> 5);
@@ -569,20 +569,78 @@ __global__ void __launch_bounds__(kPanelWarpThreads, 1) lu_panel_warp_kernel(T* 
   uint64_t* rows = a.ll_row;   // [2][G][kPanelMaxW * VW]
   uint64_t* diag = a.ll_diag;  // [2][kPanelMaxW * VW]
   const int RW = kPanelMaxW * VW;
-  if (t == 0) mbar_init(&s_bar, 1);
+  if (t == 0) mbar_init(&s_bar, 32);  // every lane of the exchange warp arrives (releases its own writes)
 
   __syncthreads();  // mbarrier initialised
-  if (poller) {
-    // ======== exchange warp
-    {
-      unsigned long long ck = 0ull;
-      int64_t ci = INT64_MAX;
-      cta_argmax_key(ck, ci, wk[0], wi[0]);
+  // One loop for both roles, so that every warp reaches the CTA-wide barrier of the candidate
+  // argmax (cta_argmax_key) at the same code location: the exchange warp (no rows, its
+  // candidate is "none") polls and hands over column c, the row warps swap / scale, then all
+  // meet in the argmax of column c + 1, then the row warps publish it and finish the update.
+  T y[PW];  // y[k] = current value of panel column c + k of my row (zeros in the exchange warp)
+#pragma unroll
+  for (int k = 0; k < PW; ++k) y[k] = (mine && k < ncol) ? W[g + (a.kb + k) * a.ld] : T(0);
+  // column cc's CTA candidate ci and row kb + cc go out as LL words.  y[0] holds
+  // column `base` (cc == base: current rows; cc == base + 1: the candidate's
+  // column cc is current, columns > cc still miss column base's update).
+  auto publish = [&](int cc, int base, int64_t ci) {
+    const int par = cc & 1;
+    const uint32_t ep = a.seq * 128u + (uint32_t)cc + 1u;
+    const int64_t ii = a.kb + cc;
+    const bool has_c = ci != INT64_MAX;
+    const bool has_d = ii >= my_lo && ii < my_hi;
+    const int cw = has_c ? 1 + ((int)(ci - my_lo) >> 5) : -1;
+    const int dw = has_d ? 1 + ((int)(ii - my_lo) >> 5) : -1;
+    if (has_c ? (mine && g == ci) : t == 32) {
+      uint64_t* h = hdr + ((size_t)par * G + blockIdx.x) * kHdrWords;
+      const T hv = cc == base ? y[0] : y[1];
+      const unsigned long long b = (unsigned long long)__double_as_longlong(has_c ? (double)hv : 0.0);
+      ll_store(h, (uint32_t)b, ep);
+      ll_store(h + 1, (uint32_t)(b >> 32), ep);
+      ll_store(h + 2, has_c ? (uint32_t)ci : 0xffffffffu, ep);
     }
-    bool prev_zero = false;  // column c - 1 had a zero pivot (its update was skipped)
-    for (int c = 0; c < ncol; ++c) {
-      const int64_t i = a.kb + c;
-      const int par = c & 1;
+    if (wid == cw || wid == dw) {
+      if (mine && (g == ci || g == ii)) {  // y[k] -> slot base + k (slots < cc are not read)
+        T* st = wstage[wid][g == ci ? 0 : 1] + base;
+#pragma unroll
+        for (int k = 0; k < PW; ++k) st[k] = y[k];
+        if (g == ci && g == ii) {
+          T* st2 = wstage[wid][1] + base;
+#pragma unroll
+          for (int k = 0; k < PW; ++k) st2[k] = y[k];
+        }
+      }
+      __syncwarp();
+      for (int j = lane; j < ncol; j += 32) {
+        if (wid == cw) {
+          const T v = j < cc ? Ls[j * ldt + (int)(ci - my_lo)] : wstage[wid][0][j];
+          LLVal<T>::put(rows + ((size_t)par * G + blockIdx.x) * RW + j * VW, v, ep);
+        }
+        if (wid == dw) {
+          const T v = j < cc ? Ls[j * ldt + (int)(ii - my_lo)] : wstage[wid][1][j];
+          LLVal<T>::put(diag + (size_t)par * RW + j * VW, v, ep);
+        }
+      }
+      __syncwarp();
+    }
+  };
+
+  bool prev_zero = false;  // exchange warp: column c - 1 had a zero pivot (its update was skipped)
+  {
+    unsigned long long ck = mine ? piv_key(fabs((double)y[0])) : 0ull;
+    int64_t ci = mine ? g : INT64_MAX;
+    cta_argmax_key(ck, ci, wk[0], wi[0]);
+    if (!poller) publish(0, 0, ci);
+  }
+  for (int c = 0; c < ncol; ++c) {
+    const int64_t i = a.kb + c;
+    const int par = c & 1;
+    // row-warp state carried across the argmax
+    const T* pr = prot[par];
+    bool act = false;
+    T l = T(0);
+    long long tr_c = 0, tr_e2 = 0, tr_f = 0;
+    if (poller) {
+      // ======== exchange warp
       const uint32_t ep = a.seq * 128u + (uint32_t)c + 1u;
       const long long t_c = a.trace ? clock64() : 0;
       // ---- pivot: poll the G headers, reduce (first max, ties -> lowest row)
@@ -719,83 +777,19 @@ __global__ void __launch_bounds__(kPanelWarpThreads, 1) lu_panel_warp_kernel(T* 
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&s_bar);
+      mbar_arrive(&s_bar);
       if (a.trace && t == 0) {
         unsigned long long* tr = a.trace + (size_t)blockIdx.x * 8;
         tr[2] += t_d - t_c;         // header poll + reduce
         tr[4] += clock64() - t_d;   // row poll + handoff
       }
-      if (c + 1 < ncol) {
-        unsigned long long ck = 0ull;
-        int64_t ci = INT64_MAX;
-        cta_argmax_key(ck, ci, wk[(c + 1) & 1], wi[(c + 1) & 1]);
-      }
-    }
-  } else {
-    // ======== row warps
-    T y[PW];  // y[k] = current value of panel column c + k of my row
-#pragma unroll
-    for (int k = 0; k < PW; ++k) y[k] = (mine && k < ncol) ? W[g + (a.kb + k) * a.ld] : T(0);
-    // column cc's CTA candidate ci and row kb + cc go out as LL words.  y[0] holds
-    // column `base` (cc == base: current rows; cc == base + 1: the candidate's
-    // column cc is current, columns > cc still miss column base's update).
-    auto publish = [&](int cc, int base, int64_t ci) {
-      const int par = cc & 1;
-      const uint32_t ep = a.seq * 128u + (uint32_t)cc + 1u;
-      const int64_t ii = a.kb + cc;
-      const bool has_c = ci != INT64_MAX;
-      const bool has_d = ii >= my_lo && ii < my_hi;
-      const int cw = has_c ? 1 + ((int)(ci - my_lo) >> 5) : -1;
-      const int dw = has_d ? 1 + ((int)(ii - my_lo) >> 5) : -1;
-      if (has_c ? (mine && g == ci) : t == 32) {
-        uint64_t* h = hdr + ((size_t)par * G + blockIdx.x) * kHdrWords;
-        const T hv = cc == base ? y[0] : y[1];
-        const unsigned long long b = (unsigned long long)__double_as_longlong(has_c ? (double)hv : 0.0);
-        ll_store(h, (uint32_t)b, ep);
-        ll_store(h + 1, (uint32_t)(b >> 32), ep);
-        ll_store(h + 2, has_c ? (uint32_t)ci : 0xffffffffu, ep);
-      }
-      if (wid == cw || wid == dw) {
-        if (mine && (g == ci || g == ii)) {  // y[k] -> slot base + k (slots < cc are not read)
-          T* st = wstage[wid][g == ci ? 0 : 1] + base;
-#pragma unroll
-          for (int k = 0; k < PW; ++k) st[k] = y[k];
-          if (g == ci && g == ii) {
-            T* st2 = wstage[wid][1] + base;
-#pragma unroll
-            for (int k = 0; k < PW; ++k) st2[k] = y[k];
-          }
-        }
-        __syncwarp();
-        for (int j = lane; j < ncol; j += 32) {
-          if (wid == cw) {
-            const T v = j < cc ? Ls[j * ldt + (int)(ci - my_lo)] : wstage[wid][0][j];
-            LLVal<T>::put(rows + ((size_t)par * G + blockIdx.x) * RW + j * VW, v, ep);
-          }
-          if (wid == dw) {
-            const T v = j < cc ? Ls[j * ldt + (int)(ii - my_lo)] : wstage[wid][1][j];
-            LLVal<T>::put(diag + (size_t)par * RW + j * VW, v, ep);
-          }
-        }
-        __syncwarp();
-      }
-    };
-
-    {
-      unsigned long long ck = mine ? piv_key(fabs((double)y[0])) : 0ull;
-      int64_t ci = mine ? g : INT64_MAX;
-      cta_argmax_key(ck, ci, wk[0], wi[0]);
-      publish(0, 0, ci);
-    }
-    for (int c = 0; c < ncol; ++c) {
-      const int64_t i = a.kb + c;
-      const int par = c & 1;
-      const long long t_c = a.trace ? clock64() : 0;
+    } else {
+      // ======== row warps
+      tr_c = a.trace ? clock64() : 0;
       mbar_wait(&s_bar, (unsigned)par);
-      const long long t_e2 = a.trace ? clock64() : 0;
+      tr_e2 = a.trace ? clock64() : 0;
       const T* pa = pabs[par];
       const T* da = dabs[par];
-      const T* pr = prot[par];
       const T* dr = drot[par];
       const int64_t p = s_piv[par];
       const T aii = pr[0];
@@ -814,25 +808,26 @@ __global__ void __launch_bounds__(kPanelWarpThreads, 1) lu_panel_warp_kernel(T* 
         }
       }
       // ---- reciprocal scale and the update of column c + 1 first
-      const bool act = mine && g > i && !zero;
-      T l = T(0);
+      act = mine && g > i && !zero;
       if (act) {
         l = mul_rn(s_rcp[par], y[0]);
         y[0] = l;
         y[1] = sub_rn(y[1], mul_rn(l, pr[1]));
       }
       if (mine) Ls[c * ldt + r] = y[0];  // retire column c
-      const long long t_f = a.trace ? clock64() : 0;
-      // ---- next column's CTA candidate (rows >= i + 1): the one CTA-wide barrier,
-      // then its header and rows go out before the rest of the update
-      int64_t ci = INT64_MAX;
-      if (c + 1 < ncol) {
-        unsigned long long ck = (mine && g > i) ? piv_key(fabs((double)y[1])) : 0ull;
-        ci = (mine && g > i) ? g : INT64_MAX;
-        cta_argmax_key(ck, ci, wk[(c + 1) & 1], wi[(c + 1) & 1]);
-        publish(c + 1, c, ci);
-      }
-      const long long t_g = a.trace ? clock64() : 0;
+      tr_f = a.trace ? clock64() : 0;
+    }
+    // ---- next column's CTA candidate (rows >= i + 1): the one CTA-wide barrier, then its
+    // header and rows go out before the rest of the update
+    if (c + 1 < ncol) {
+      const bool cand = !poller && mine && g > i;
+      unsigned long long ck = cand ? piv_key(fabs((double)y[1])) : 0ull;
+      int64_t ci = cand ? g : INT64_MAX;
+      cta_argmax_key(ck, ci, wk[(c + 1) & 1], wi[(c + 1) & 1]);
+      if (!poller) publish(c + 1, c, ci);
+    }
+    if (!poller) {
+      const long long tr_g = a.trace ? clock64() : 0;
       // ---- rest of the rank-1 update (direct.py:75-79), then rotate by one
       if (act) {
 #pragma unroll
@@ -844,10 +839,10 @@ __global__ void __launch_bounds__(kPanelWarpThreads, 1) lu_panel_warp_kernel(T* 
       if (a.trace && t == 32) {
         const long long t_h = clock64();
         unsigned long long* tr = a.trace + (size_t)blockIdx.x * 8;
-        tr[3] += t_e2 - t_c;  // wait for the handoff
-        tr[0] += t_f - t_e2;  // swap, scale
-        tr[1] += t_g - t_f;   // next column's CTA argmax + publish
-        tr[5] += t_h - t_g;   // update, rotate
+        tr[3] += tr_e2 - tr_c;  // wait for the handoff
+        tr[0] += tr_f - tr_e2;  // swap, scale
+        tr[1] += tr_g - tr_f;   // next column's CTA argmax + publish
+        tr[5] += t_h - tr_g;    // update, rotate
       }
     }
   }
@@ -1242,7 +1237,7 @@ int panel_launch(ds_ctx* ctx, T* W, int64_t n, int64_t ld, int64_t kb, int64_t b
   a.ll_hdr = cv.take<uint64_t>(sizeof(uint64_t) * 2 * 1024 * kHdrWords);
   a.ll_row = cv.take<uint64_t>(sizeof(uint64_t) * 2 * 1024 * kPanelMaxW * 2);
   a.ll_diag = cv.take<uint64_t>(sizeof(uint64_t) * 2 * kPanelMaxW * 2);
-  a.seq = ++ctx->panel_seq;
+  a.seq = next_ll_epoch();
   a.trace = nullptr;
   static const int backoff = [] {
     const char* e = getenv("DENSOLVE_PANEL_BACKOFF");
