@@ -1292,6 +1292,164 @@ __global__ void __launch_bounds__(gemm64::THREADS, 2)
   }
 }
 
+// Persistent form of gemm64_tma_kernel<1> (out = C - A B) for the LU trailing update that
+// runs beside the look-ahead panel on the side stream.  A CTA that lands on one of the
+// first `reserve` SMs leaves at once (unless no worker has registered yet), so the side
+// stream's panel and inner kernels find those SMs free instead of waiting for trailing-GEMM
+// CTAs (~67 us each at K = 512) to retire.  The workers take 128 x 64 tiles from a device
+// counter in the non-persistent kernel's order (m fastest); the elected producer thread
+// claims the tiles, passes their indices to the compute warps through a shared-memory queue
+// published by the stage's full mbarrier, and keeps the TMA ring full across tile
+// boundaries (slab counters run over the CTA's whole tile sequence); a sentinel index ends
+// the loop.  Per tile the same accumulator start (C), DMMA sequence and store: bitwise equal
+// to the non-persistent kernel.
+//   ctr[0]: next tile, ctr[1]: registered workers (both zeroed before the launch)
+__global__ void __launch_bounds__(gemm64::THREADS, 2)
+    gemm64_tma_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                              int64_t m, int64_t n, int64_t k, const double* C, int64_t ldc, double* out,
+                              int64_t ldo, int reserve, unsigned* ctr) {
+  using namespace gemm64;
+  constexpr int Q = 8;  // tile-index queue (the producer runs <= STAGES - 1 slabs ahead)
+  __shared__ int tile_q[Q];
+  __shared__ int s_work;
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES];
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;\n" : "=r"(smid));
+    int work = (int)smid >= reserve;
+    if (!work) work = atomicAdd(&ctr[1], 0u) == 0u;  // never leave the tiles without a worker
+    if (work) atomicAdd(&ctr[1], 1u);
+    s_work = work;
+  }
+  __syncthreads();
+  if (!s_work) return;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t ktiles = ceil_div(k, BK);
+  const int64_t mtiles = ceil_div(m, BM);
+  const int64_t ntiles = mtiles * ceil_div(n, BN);
+  // producer state (thread 0 only; in shared memory to keep the compute warps' registers):
+  // slabs issued, slab within the current tile, current tile, tile ordinal, done
+  __shared__ int p_cnt, p_kt, p_tile, p_j, p_done;
+  auto produce = [&]() {  // issue the next slab (or the sentinel) into ring slot p_cnt
+    if (p_done) return;
+    const int s = p_cnt % STAGES;
+    if (p_cnt >= STAGES) mbar_wait_cta(&empty_bar[s], (unsigned)(((p_cnt - STAGES) / STAGES) & 1));
+    if (p_kt == (int)ktiles) {  // claim the next tile
+      const unsigned tl = atomicAdd(&ctr[0], 1u);
+      if ((int64_t)tl >= ntiles) {
+        tile_q[p_j % Q] = -1;
+        mbar_arrive_cta(&full_bar[s]);  // releases the sentinel (count 1, no bytes)
+        p_done = 1;
+        ++p_cnt;
+        return;
+      }
+      p_tile = (int)tl;
+      tile_q[p_j % Q] = p_tile;
+      ++p_j;
+      p_kt = 0;
+    }
+    unsigned char* st = sm + (size_t)s * STAGE_TMA_BYTES;
+    mbar_arrive_expect_tx(&full_bar[s], STAGE_TMA_BYTES);
+    const int kc = p_kt * BK;
+    const int pm0 = (int)((p_tile % mtiles) * BM), pn0 = (int)((p_tile / mtiles) * BN);
+#pragma unroll
+    for (int b = 0; b < BM / 16; ++b) tma_load_2d(st + b * 2048, &tmA, pm0 + 16 * b, kc, &full_bar[s]);
+    tma_load_2d(st + A_TMA_BYTES, &tmB, kc, pn0, &full_bar[s]);
+    ++p_kt;
+    ++p_cnt;
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init_cta(&full_bar[s], 1);
+      mbar_init_cta(&empty_bar[s], THREADS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    p_cnt = 0;
+    p_kt = (int)ktiles;
+    p_tile = 0;
+    p_j = 0;
+    p_done = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int s = 0; s < STAGES - 1; ++s) produce();
+
+  const unsigned a_lane = (unsigned)(wm * 2) * 2048u + (unsigned)t * 128u + ((unsigned)((g >> 1) ^ t) << 4) +
+                          ((unsigned)(g & 1) << 3);
+  unsigned b_lane[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    b_lane[q] = (unsigned)A_TMA_BYTES + (unsigned)(wn * 32 + g) * 128u +
+                ((unsigned)(((t >> 1) ^ g) ^ (2 * q)) << 4) + ((unsigned)(t & 1) << 3);
+  int c_cnt = 0;  // slabs consumed
+  for (int jc = 0;; ++jc) {
+    mbar_wait_cta(&full_bar[c_cnt % STAGES], (unsigned)((c_cnt / STAGES) & 1));  // first slab of tile jc
+    const int tile = tile_q[jc % Q];
+    if (tile < 0) break;
+    const int64_t m0 = (tile % mtiles) * BM, n0 = (tile / mtiles) * BN;
+    double acc[MI][4][2];
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      const int64_t r = m0 + wm * WR + i * 8 + g;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t c = n0 + wn * 32 + j * 8 + 2 * t + e;
+          acc[i][j][e] = (r < m && c < n) ? C[r + c * ldc] : 0.0;
+        }
+    }
+    for (int kt = 0; kt < (int)ktiles; ++kt, ++c_cnt) {
+      if (warp == 0) {
+        if (lane == 0) produce();  // slab c_cnt + STAGES - 1 (its slot was released at c_cnt - 1)
+        __syncwarp();
+      }
+      const int s = (int)(c_cnt % STAGES);
+      if (kt > 0) mbar_wait_cta(&full_bar[s], (unsigned)((c_cnt / STAGES) & 1));
+      const unsigned char* st = sm + (size_t)s * STAGE_TMA_BYTES;
+#pragma unroll
+      for (int q = 0; q < BK / 4; ++q) {
+        double a[MI], b[4];
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const unsigned off = a_lane + (unsigned)(i >> 1) * 2048u + (unsigned)q * 512u +
+                               ((unsigned)(((i & 1) << 2) ^ ((q & 1) << 2)) << 4);
+          a[i] = -*reinterpret_cast<const double*>(st + off);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = *reinterpret_cast<const double*>(st + b_lane[q] + (unsigned)j * 1024u);
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&empty_bar[s]);
+    }
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      const int64_t r = m0 + wm * WR + i * 8 + g;
+      if (r >= m) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t c = n0 + wn * 32 + j * 8 + 2 * t + e;
+          if (c < n) out[r + c * ldo] = acc[i][j][e];
+        }
+    }
+  }
+}
+
 // Host side: the driver's tensor-map encoder, resolved once through the runtime (no
 // libcuda link).  A 2-D map of a column-major matrix: dim 0 = rows (contiguous), dim 1 =
 // columns, box {16, box_cols}, 128-byte swizzle, out-of-range elements zero-filled.
@@ -1514,7 +1672,18 @@ static int gemm_impl(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha,
                                      (int)SMEM_TMA));
         tma_attr = true;
       }
-      if (sub)
+      if (sub && !tri && ctx->gemm_reserve > 0) {  // LU trailing update beside the look-ahead panel
+        static bool pattr = false;
+        if (!pattr) {
+          DS_CUDA(cudaFuncSetAttribute(gemm64_tma_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)SMEM_TMA));
+          pattr = true;
+        }
+        if (!ctx->gemm_ctr) DS_CUDA(cudaMalloc((void**)&ctx->gemm_ctr, 2 * sizeof(unsigned)));
+        DS_CUDA(cudaMemsetAsync(ctx->gemm_ctr, 0, 2 * sizeof(unsigned), ctx->stream));
+        gemm64_tma_persist_kernel<<<2 * ctx->num_sms, THREADS, SMEM_TMA, ctx->stream>>>(
+            ta, tb, m, n, k, C, ldc, out, ldo, ctx->gemm_reserve, ctx->gemm_ctr);
+      } else if (sub)
         gemm64_tma_kernel<1><<<grid, THREADS, SMEM_TMA, ctx->stream>>>(ta, tb, m, n, k, alpha, beta, C, ldc, out,
                                                                        ldo, tri);
       else

@@ -271,6 +271,10 @@ struct ds_ctx {
   cudaStream_t aux = nullptr;  // low-priority stream for the swaps of already-factored L columns
   cudaStream_t copy = nullptr;  // asynchronous host->device staging (ds_upload_async)
   cudaEvent_t ev_a = nullptr, ev_b = nullptr, ev_c = nullptr;
+  // LU trailing GEMM beside the look-ahead panel: > 0 runs the fp64 C - AB update as the
+  // persistent kernel that leaves SMs [0, gemm_reserve) to the side stream (ds_lu.cu)
+  int gemm_reserve = 0;
+  unsigned* gemm_ctr = nullptr;  // its tile / worker counters (2 words, zeroed per launch)
   // Serialises the entry points on this context: its workspace, streams, pinned buffer
   // and events are shared state ("one solve at a time" per backend, backends.py:80-81).
   // Recursive: a GMRES workspace sink may call back into the library on this thread.

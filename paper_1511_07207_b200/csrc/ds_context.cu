@@ -151,6 +151,7 @@ int ds_ctx_destroy(ds_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->gemm_ctr) cudaFree(ctx->gemm_ctr);
   if (ctx->copy) cudaStreamDestroy(ctx->copy);
   if (ctx->hbuf) cudaFreeHost(ctx->hbuf);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);

@@ -1444,7 +1444,7 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
     return DS_OK;
   };
   // U01 = L00^-1 A01 and A11 -= L10 U01 for trailing columns [c0, c1)
-  auto outer_update = [&](int64_t kb, int64_t bf, int64_t c0, int64_t c1) -> int {
+  auto outer_update = [&](int64_t kb, int64_t bf, int64_t c0, int64_t c1, int reserve) -> int {
     if (c1 <= c0) return DS_OK;
     for (int64_t ib = kb; ib < bf; ib += b) {
       const int64_t ibf = std::min<int64_t>(ib + b, bf);
@@ -1454,8 +1454,31 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
         DS_TRY(gemm_launch<T>(ctx, bf - ibf, c1 - c0, ibf - ib, -1.0, W + ibf + ib * ld, ld, Ur, ld, 1.0,
                               W + ibf + c0 * ld, ld, W + ibf + c0 * ld, ld));
     }
-    return gemm_launch<T>(ctx, m - bf, c1 - c0, bf - kb, -1.0, W + bf + kb * ld, ld, W + kb + c0 * ld, ld, 1.0,
-                          W + bf + c0 * ld, ld, W + bf + c0 * ld, ld);
+    ctx->gemm_reserve = reserve;
+    const int rc = gemm_launch<T>(ctx, m - bf, c1 - c0, bf - kb, -1.0, W + bf + kb * ld, ld, W + kb + c0 * ld, ld,
+                                  1.0, W + bf + c0 * ld, ld, W + bf + c0 * ld, ld);
+    ctx->gemm_reserve = 0;
+    return rc;
+  };
+  // SMs kept free of the trailing GEMM while the look-ahead factorization of the outer panel
+  // [bf, bf2) runs on the side stream (0: none).  Only where the GEMM on the remaining SMs is
+  // predicted to finish within the side stream's time (the tail of the factorization, where
+  // the chain of panels is the critical path): there every side-stream launch would otherwise
+  // wait for trailing-GEMM CTAs to retire.  Model: 33 TFLOP/s DMMA, ~4.5 us per panel column.
+  static const double reserve_ratio = [] {
+    const char* e = getenv("DENSOLVE_LU_RESERVE");  // tuning knob: 0 disables
+    return e ? atof(e) : 1.0;
+  }();
+  auto side_reserve = [&](int64_t bf, int64_t bf2) -> int {
+    if (reserve_ratio <= 0 || sizeof(T) != 8) return 0;
+    const int64_t rows = m - bf, nsm = ctx->num_sms;
+    const int64_t gw = ceil_div(rows, (int64_t)kPanelWarpRows);
+    const int64_t gp = (gw >= 2 && gw <= 40) ? gw : std::min<int64_t>(nsm, ceil_div(rows, (int64_t)256));
+    const int64_t r = gp + 4;
+    if (r > nsm - 16) return 0;
+    const double t_gemm = 2.0 * (double)(m - bf) * (double)(w - bf2) * (double)NB / (33e12 * (double)(nsm - r) / nsm);
+    const double t_side = (double)(bf2 - bf) * 4.5e-6;
+    return t_gemm <= reserve_ratio * t_side ? (int)r : 0;
   };
 
   DS_TRY(factor_outer(0, std::min<int64_t>(NB, w)));
@@ -1508,7 +1531,7 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
     // the look-ahead columns [bf, bf2) get their swaps and update first: that is the
     // only work between this panel and the next panel's factorization
     DS_TRY(laswp_apply<T>(ctx, W, ld, bf, bf2, op));
-    DS_TRY(outer_update(kb, bf, bf, bf2));
+    DS_TRY(outer_update(kb, bf, bf, bf2, 0));
     if (lookahead) {
       DS_CUDA(cudaEventRecord(ctx->ev_a, ctx->stream));
       DS_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_a, 0));
@@ -1530,11 +1553,11 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
       DS_CUDA(cudaEventRecord(ctx->ev_b, ctx->side));
       // the rest of the trailing matrix (disjoint columns) overlaps the next panel
       DS_TRY(laswp_apply<T>(ctx, W, ld, bf2, w, op));
-      DS_TRY(outer_update(kb, bf, bf2, w));
+      DS_TRY(outer_update(kb, bf, bf2, w, side_reserve(bf, bf2)));
       DS_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_b, 0));
     } else {
       DS_TRY(laswp_apply<T>(ctx, W, ld, bf2, w, op));
-      DS_TRY(outer_update(kb, bf, bf2, w));
+      DS_TRY(outer_update(kb, bf, bf2, w, 0));
       DS_TRY(factor_outer(bf, bf2));
     }
   }

@@ -30,6 +30,8 @@ for _ in range(reps + 1):
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
 best = min(ts[1:])
-tag = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith("DENSOLVE_PANEL"))
-print(f"LU n={n}: best {best:.2f} ms = {2 / 3 * n ** 3 / best / 1e9:.1f} TFLOP/s  runs {[round(t, 1) for t in ts[1:]]}  {tag}",
-      flush=True)
+tag = " ".join(f"{k}={v}" for k, v in os.environ.items() if k.startswith(("DENSOLVE_PANEL", "DENSOLVE_LU")))
+import hashlib  # noqa: E402
+digest = hashlib.sha256(np.ascontiguousarray(dA.to_host()).tobytes()).hexdigest()[:16]
+print(f"LU n={n}: best {best:.2f} ms = {2 / 3 * n ** 3 / best / 1e9:.1f} TFLOP/s  runs {[round(t, 1) for t in ts[1:]]}  {tag}"
+      f"  factors sha256 {digest}", flush=True)
