@@ -1,5 +1,6 @@
 # Round-end evidence: GPU tests, the bench line (+ force-sharded), launch lists of the
-# headline, LU and GMRES C2, and full captures of the GEMV and the K=512 TMA GEMM.
+# headline, LU and GMRES C2, and full captures of the GEMV, the K=512 TMA GEMM and the
+# persistent (SM-reserving) LU trailing GEMM.
 tag=${1:-r02f}
 out=gpurun_out; mkdir -p $out
 NCU=/usr/local/cuda/bin/ncu
@@ -16,4 +17,6 @@ timeout 600 $NCU --set full --clock-control none --import-source on -k regex:col
   -o $out/gemv_full_$tag -f python tools/profile_run.py gemv 32768 > /dev/null 2>&1; echo "gemv full $?"
 timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemm64 -s 1 -c 1 \
   -o $out/gemm_full_$tag -f python tools/profile_run.py gemm 16384 16384 512 > /dev/null 2>&1; echo "gemm full $?"
+timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemm64_tma_persist -s 3 -c 1 \
+  -o $out/gemm_persist_full_$tag -f python tools/profile_run.py lu 16384 > /dev/null 2>&1; echo "persist gemm full $?"
 for f in $out/launches_*_$tag.csv; do python tools/launch_summary.py $f | head -14; done
