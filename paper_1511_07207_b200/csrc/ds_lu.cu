@@ -1654,6 +1654,10 @@ __global__ void gather_kernel(int64_t n, const int* __restrict__ idx, const T* _
 // ----------------------------------------------------------------------------
 constexpr int kTrsvNB = 64;
 constexpr int kTrsvThreads = 256;
+#ifndef DS_TRSV_DEPTH
+#define DS_TRSV_DEPTH 3
+#endif
+constexpr int kTrsvDepth = DS_TRSV_DEPTH;  // earlier blocks in flight per CTA during the fold
 
 // TRANS (upper only): solve with U = M^T, i.e. U[i,j] = M[j + i*ld] (the
 // backward sweep of cholesky_solve on L^T, direct.py:166-171, without forming L^T).
@@ -1795,9 +1799,12 @@ __global__ void __launch_bounds__(kTrsvThreads)
   if (t > 1) {
     auto block_col0 = [&](int64_t sidx) -> int64_t { return (LOWER ? sidx : nblk - 1 - sidx) * kTrsvNB; };
     constexpr int CPW = kTrsvNB / NW;  // columns per warp per block (non-TRANS)
-    double mv[2 * CPW];
-    uint64_t xw0[2], xw1[2];
-    auto issue = [&](int64_t sidx) {
+    // kTrsvDepth blocks in flight per CTA: block sidx lives in slot sidx % kTrsvDepth, its
+    // matrix values and LL words issued kTrsvDepth blocks ahead (static slot indices: the
+    // loop is unrolled by the depth)
+    double mv[kTrsvDepth][2 * CPW];
+    uint64_t xw0[kTrsvDepth][2], xw1[kTrsvDepth][2];
+    auto issue = [&](int64_t sidx, double (&m)[2 * CPW], uint64_t (&w0)[2], uint64_t (&w1)[2]) {
       const int64_t c0 = block_col0(sidx);
       const int nc = (int)min((int64_t)kTrsvNB, n - c0);
       if (!TRANS) {
@@ -1805,13 +1812,13 @@ __global__ void __launch_bounds__(kTrsvThreads)
         for (int j = 0; j < CPW; ++j) {
           const int c = warp + NW * j;
           const T* col = M + (c0 + c) * ld + r0;
-          mv[2 * j] = (c < nc && ra < nr) ? (double)col[ra] : 0.0;
-          mv[2 * j + 1] = (c < nc && rb < nr) ? (double)col[rb] : 0.0;
+          m[2 * j] = (c < nc && ra < nr) ? (double)col[ra] : 0.0;
+          m[2 * j + 1] = (c < nc && rb < nr) ? (double)col[rb] : 0.0;
         }
         const int c = warp + NW * (lane & (CPW - 1));
         const uint64_t* p = ll + 2 * (c0 + min(c, nc - 1));
-        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(xw0[0]) : "l"(p) : "memory");
-        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(xw1[0]) : "l"(p + 1) : "memory");
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(w0[0]) : "l"(p) : "memory");
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(w1[0]) : "l"(p + 1) : "memory");
       } else {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -1819,55 +1826,61 @@ __global__ void __launch_bounds__(kTrsvThreads)
 #pragma unroll
           for (int j = 0; j < CPW; ++j) {
             const int r = warp + NW * j;
-            mv[h * CPW + j] = (c < nc && r < nr) ? (double)M[(c0 + c) + (r0 + r) * ld] : 0.0;
+            m[h * CPW + j] = (c < nc && r < nr) ? (double)M[(c0 + c) + (r0 + r) * ld] : 0.0;
           }
           const uint64_t* p = ll + 2 * (c0 + min(c, nc - 1));
-          asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(xw0[h]) : "l"(p) : "memory");
-          asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(xw1[h]) : "l"(p + 1) : "memory");
+          asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(w0[h]) : "l"(p) : "memory");
+          asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(w1[h]) : "l"(p + 1) : "memory");
         }
       }
     };
-    auto validate = [&](int64_t sidx, int h) -> double {
+    auto validate = [&](int64_t sidx, int h, uint64_t (&w0)[2], uint64_t (&w1)[2]) -> double {
       // re-poll the LL words of my unknown until both carry the flag
       const int64_t c0 = block_col0(sidx);
       const int nc = (int)min((int64_t)kTrsvNB, n - c0);
       const int c = TRANS ? lane + 32 * h : warp + NW * (lane & (CPW - 1));
       const uint64_t* p = ll + 2 * (c0 + min(c, nc - 1));
-      while ((xw0[h] >> 32) != 1u)
-        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(xw0[h]) : "l"(p) : "memory");
+      while ((w0[h] >> 32) != 1u)
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(w0[h]) : "l"(p) : "memory");
       if (sizeof(T) == 8) {
-        while ((xw1[h] >> 32) != 1u)
-          asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(xw1[h]) : "l"(p + 1) : "memory");
-        return __longlong_as_double((long long)((xw1[h] << 32) | (xw0[h] & 0xffffffffull)));
+        while ((w1[h] >> 32) != 1u)
+          asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(w1[h]) : "l"(p + 1) : "memory");
+        return __longlong_as_double((long long)((w1[h] << 32) | (w0[h] & 0xffffffffull)));
       }
-      return (double)__uint_as_float((unsigned)(xw0[h] & 0xffffffffull));
+      return (double)__uint_as_float((unsigned)(w0[h] & 0xffffffffull));
     };
-    issue(0);
-    for (int64_t sidx = 0; sidx + 1 < t; ++sidx) {
-      double cur[2 * CPW];
+    const int64_t nfold = t - 1;  // blocks folded here (all but the preceding one)
 #pragma unroll
-      for (int j = 0; j < 2 * CPW; ++j) cur[j] = mv[j];
-      uint64_t c0w0[2] = {xw0[0], xw0[1]}, c0w1[2] = {xw1[0], xw1[1]};
-      if (sidx + 2 < t) issue(sidx + 1);  // prefetch the next block
-      uint64_t nw0[2] = {xw0[0], xw0[1]}, nw1[2] = {xw1[0], xw1[1]};
-      xw0[0] = c0w0[0]; xw0[1] = c0w0[1]; xw1[0] = c0w1[0]; xw1[1] = c0w1[1];
-      if (!TRANS) {
-        const double xmine = validate(sidx, 0);
+    for (int d = 0; d < kTrsvDepth; ++d)
+      if (d < nfold) issue(d, mv[d], xw0[d], xw1[d]);
+    for (int64_t s0 = 0; s0 < nfold; s0 += kTrsvDepth) {
 #pragma unroll
-        for (int j = 0; j < CPW; ++j) {
-          const double xv = __shfl_sync(0xffffffffu, xmine, j);
-          a0 = fma(cur[2 * j], xv, a0);
-          a1 = fma(cur[2 * j + 1], xv, a1);
-        }
-      } else {
+      for (int d = 0; d < kTrsvDepth; ++d) {
+        const int64_t sidx = s0 + d;
+        if (sidx < nfold) {
+          double cur[2 * CPW];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const double xv = validate(sidx, h);
+          for (int j = 0; j < 2 * CPW; ++j) cur[j] = mv[d][j];
+          uint64_t cw0[2] = {xw0[d][0], xw0[d][1]}, cw1[2] = {xw1[d][0], xw1[d][1]};
+          if (sidx + kTrsvDepth < nfold) issue(sidx + kTrsvDepth, mv[d], xw0[d], xw1[d]);  // refill the slot
+          if (!TRANS) {
+            const double xmine = validate(sidx, 0, cw0, cw1);
 #pragma unroll
-          for (int j = 0; j < CPW; ++j) at[j] = fma(cur[h * CPW + j], xv, at[j]);
+            for (int j = 0; j < CPW; ++j) {
+              const double xv = __shfl_sync(0xffffffffu, xmine, j);
+              a0 = fma(cur[2 * j], xv, a0);
+              a1 = fma(cur[2 * j + 1], xv, a1);
+            }
+          } else {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const double xv = validate(sidx, h, cw0, cw1);
+#pragma unroll
+              for (int j = 0; j < CPW; ++j) at[j] = fma(cur[h * CPW + j], xv, at[j]);
+            }
+          }
         }
       }
-      xw0[0] = nw0[0]; xw0[1] = nw0[1]; xw1[0] = nw1[0]; xw1[1] = nw1[1];
     }
   }
   if (t > 0) {  // the preceding block: its unknowns arrive as LL words, then its staged tile

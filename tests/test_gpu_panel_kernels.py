@@ -35,9 +35,9 @@ CASES = [(200, 64, 1, "float64"), (1000, 48, 2, "float64"), (3000, 64, 3, "float
          (12000, 64, 5, "float64"), (3000, 64, 6, "float32"), (700, 40, 7, "float32")]
 
 
-def _run(force):
-    env = dict(os.environ, DENSOLVE_PANEL_KERNEL=str(force))
-    out = subprocess.run([sys.executable, "-c", _SCRIPT.format(root=ROOT, cases=CASES)], env=env,
+def _run(force, cases=CASES, **extra):
+    env = dict(os.environ, DENSOLVE_PANEL_KERNEL=str(force), **extra)
+    out = subprocess.run([sys.executable, "-c", _SCRIPT.format(root=ROOT, cases=cases)], env=env,
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     return [line.split() for line in out.stdout.strip().splitlines()]
@@ -47,6 +47,16 @@ def test_panel_kernels_bitwise_identical():
     runs = {force: _run(force) for force in (0, 1, 2)}
     assert len(runs[0]) == len(CASES)
     assert runs[0] == runs[1] == runs[2]
+
+
+def test_sm_reservation_is_bitwise_neutral():
+    # the tail trailing GEMMs beside the look-ahead panel run as the persistent kernel that
+    # leaves the panel's SMs free (ds_blas.cu gemm64_tma_persist_kernel, dynamic tile order):
+    # same per-tile DMMA chain, so the same bits as the ordinary launch (DENSOLVE_LU_RESERVE=0)
+    cases = [(8192, 64, 8, "float64"), (6000, 64, 9, "float64")]
+    on = _run(0, cases)
+    off = _run(0, cases, DENSOLVE_LU_RESERVE="0")
+    assert len(on) == len(cases) and on == off
 
 
 def test_poller_kernel_factorization_is_valid():
