@@ -1335,14 +1335,12 @@ __global__ void __launch_bounds__(gemm64::THREADS, 2)
   // producer state (thread 0 only; in shared memory to keep the compute warps' registers):
   // slabs issued, slab within the current tile, current tile, tile ordinal, done
   __shared__ int p_cnt, p_kt, p_tile, p_j, p_done;
-  unsigned next_tl = 0;  // thread 0: the tile claimed one tile ahead (the atomic's latency hides behind a tile)
   auto produce = [&]() {  // issue the next slab (or the sentinel) into ring slot p_cnt
     if (p_done) return;
     const int s = p_cnt % STAGES;
     if (p_cnt >= STAGES) mbar_wait_cta(&empty_bar[s], (unsigned)(((p_cnt - STAGES) / STAGES) & 1));
-    if (p_kt == (int)ktiles) {  // take the claimed tile, claim the one after it
-      const unsigned tl = next_tl;
-      if ((int64_t)tl < ntiles) next_tl = atomicAdd(&ctr[0], 1u);
+    if (p_kt == (int)ktiles) {  // claim the next tile
+      const unsigned tl = atomicAdd(&ctr[0], 1u);
       if ((int64_t)tl >= ntiles) {
         tile_q[p_j % Q] = -1;
         mbar_arrive_cta(&full_bar[s]);  // releases the sentinel (count 1, no bytes)
@@ -1381,10 +1379,8 @@ __global__ void __launch_bounds__(gemm64::THREADS, 2)
     p_done = 0;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    next_tl = atomicAdd(&ctr[0], 1u);
+  if (threadIdx.x == 0)
     for (int s = 0; s < STAGES - 1; ++s) produce();
-  }
 
   const unsigned a_lane = (unsigned)(wm * 2) * 2048u + (unsigned)t * 128u + ((unsigned)((g >> 1) ^ t) << 4) +
                           ((unsigned)(g & 1) << 3);
@@ -1676,11 +1672,7 @@ static int gemm_impl(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha,
                                      (int)SMEM_TMA));
         tma_attr = true;
       }
-      static const bool persist_all = [] {  // A/B knob: every C - AB update persistent, no SMs reserved
-        const char* e = getenv("DENSOLVE_GEMM_PERSIST");
-        return e && e[0] == '1';
-      }();
-      if (sub && !tri && (ctx->gemm_reserve > 0 || persist_all)) {  // LU trailing update beside the look-ahead panel
+      if (sub && !tri && ctx->gemm_reserve > 0) {  // LU trailing update beside the look-ahead panel
         static bool pattr = false;
         if (!pattr) {
           DS_CUDA(cudaFuncSetAttribute(gemm64_tma_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
