@@ -1672,14 +1672,13 @@ static int gemm_impl(ds_ctx* ctx, int64_t m, int64_t n, int64_t k, double alpha,
                                      (int)SMEM_TMA));
         tma_attr = true;
       }
-      if (sub && !tri && ctx->gemm_reserve > 0) {  // LU trailing update beside the look-ahead panel
+      if (sub && !tri && ctx->gemm_reserve > 0 && ctx->gemm_ctr) {  // LU trailing update beside the look-ahead panel
         static bool pattr = false;
         if (!pattr) {
           DS_CUDA(cudaFuncSetAttribute(gemm64_tma_persist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)SMEM_TMA));
           pattr = true;
         }
-        if (!ctx->gemm_ctr) DS_CUDA(cudaMalloc((void**)&ctx->gemm_ctr, 2 * sizeof(unsigned)));
         DS_CUDA(cudaMemsetAsync(ctx->gemm_ctr, 0, 2 * sizeof(unsigned), ctx->stream));
         gemm64_tma_persist_kernel<<<2 * ctx->num_sms, THREADS, SMEM_TMA, ctx->stream>>>(
             ta, tb, m, n, k, C, ldc, out, ldo, ctx->gemm_reserve, ctx->gemm_ctr);

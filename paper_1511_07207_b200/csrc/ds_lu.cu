@@ -1415,6 +1415,9 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
     DS_CUDA(cudaEventCreateWithFlags(&ctx->ev_b, cudaEventDisableTiming));
     DS_CUDA(cudaEventCreateWithFlags(&ctx->ev_c, cudaEventDisableTiming));
   }
+  // tile / worker counters of the SM-reserving trailing GEMM (allocated once per context,
+  // outside the enqueue sequence)
+  if (lookahead && !ctx->gemm_ctr) DS_CUDA(cudaMalloc((void**)&ctx->gemm_ctr, 2 * sizeof(unsigned)));
   // swap plans of the L-column swaps (aux stream): one per outer panel, kept
   // alive until the aux stream drains
   const int64_t nouter = ceil_div(w, NB);
