@@ -51,6 +51,8 @@ def _peaks():
 
 
 FP64_PEAK_TFLOPS = 37.1  # DMMA/DFMA measured on this pool (profiles/fp64_peak_r01.txt)
+FP32_PEAK_TFLOPS = 74.4  # FFMA: 148 SMs x 128 lanes x 2 flop x 1.965 GHz (nominal at the max SM clock)
+FP32_PEAK_SOURCE = "nominal: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz (not measured)"
 
 
 # ---------------------------------------------------------------------------- clocks
@@ -457,6 +459,9 @@ def run_b200(args):
         lu_fit = None if args.no_cpu_baseline else reference_lu_fit()
         components["lu_c3"] = bench_lu(args, torch, stream, be, args.lu_n, lu_fit, hbm_peak)
         components["lu_c5"] = bench_lu(args, torch, stream, be, args.lu_n5, lu_fit, hbm_peak)
+        # fp32 LU (the reference's f32 families, tests/test_direct.py:123-139) at the C3 size
+        lu_fit32 = None if args.no_cpu_baseline else reference_lu_fit(np.float32)
+        components["lu_c3_f32"] = bench_lu(args, torch, stream, be, args.lu_n, lu_fit32, hbm_peak, "f32")
 
     line = {"metric": BASELINE_METRIC, "value": round(value, 3), "unit": f"CG iters/s (n={n} fp64)",
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4),
@@ -640,7 +645,7 @@ def bench_cholesky(args, torch, stream, be, dA, n, cholesky_factor, A_h=None):
     return out
 
 
-def reference_lu_fit():
+def reference_lu_fit(dtype=np.float64):
     """The reference lu_factor_blocked (b=64, 'blocked' backend, all cores) on the uniform
     recipe at n = 2048 and 4096, fitted to t = a n^3 (full n needs hours)."""
     from paper_1511_07207_b200.harness import generate_uniform
@@ -649,6 +654,7 @@ def reference_lu_fit():
     pts = []
     for n in (2048, 4096):
         A, _, _ = generate_uniform(n, 1)
+        A = np.asfortranarray(A, dtype=dtype)
         t0 = time.perf_counter()
         densolve.lu_factor_blocked(A, 64, be)
         pts.append((n, time.perf_counter() - t0))
@@ -657,14 +663,15 @@ def reference_lu_fit():
                                for n, t in pts]}
 
 
-def bench_lu(args, torch, stream, be, n, lu_fit, hbm_peak):
+def bench_lu(args, torch, stream, be, n, lu_fit, hbm_peak, prec="f64"):
     """Blocked LU b=64 on the uniform recipe (C3 pivoting family, default_rng([1, n, 1]),
     ds_generate) + lu_solve of b = A x_true; CPU: the reference extrapolated from n=2048/4096
     and LAPACK getrf (scipy) at full n as a labelled comparator."""
     from paper_1511_07207_b200 import lu_factor_blocked, lu_solve
     from paper_1511_07207_b200.harness import generate_problem_device
 
-    dA, db, dxt = generate_problem_device("uniform", n, 1, "f64", be)
+    dA, db, dxt = generate_problem_device("uniform", n, 1, prec, be)
+    esize = 8 if prec == "f64" else 4
     torch.cuda.synchronize()
     f = lu_factor_blocked(dA, 64, be)  # warm-up
     del f
@@ -674,16 +681,22 @@ def bench_lu(args, torch, stream, be, n, lu_fit, hbm_peak):
     f = lu_factor_blocked(dA, 64, be)
     sms, x = _timed(torch, stream, lambda: lu_solve(f, db), 5)
     err = float(np.max(np.abs(x.to_host() - dxt.to_host())))
-    sbytes = 8.0 * n * n  # one pass over each triangle of the packed factors
+    sbytes = float(esize) * n * n  # one pass over each triangle of the packed factors
     flops = 2.0 * n ** 3 / 3.0
     tf = flops / (ms / 1e3) / 1e12
-    out = {"workload": f"blocked LU b=64, uniform recipe n={n} fp64 (pivoting family), device-resident "
-                       "(includes the device copy of A, direct.py:61); best of 3 after 1 warm-up",
-           "value": round(tf * 1e3, 1), "unit": "GFLOP/s", "ms": round(ms, 2), "ms_runs": [round(r, 2) for r in runs],
-           "fp64_peak_tflops": FP64_PEAK_TFLOPS, "frac_of_fp64_peak": round(tf / FP64_PEAK_TFLOPS, 4),
+    out = {"workload": f"blocked LU b=64, uniform recipe n={n} {'fp64' if prec == 'f64' else 'fp32'} "
+                       "(pivoting family), device-resident (includes the device copy of A, direct.py:61); "
+                       "best of 3 after 1 warm-up",
+           "value": round(tf * 1e3, 1), "unit": "GFLOP/s", "ms": round(ms, 2), "ms_runs": [round(r, 2) for r in runs]}
+    if prec == "f64":
+        out.update({"fp64_peak_tflops": FP64_PEAK_TFLOPS, "frac_of_fp64_peak": round(tf / FP64_PEAK_TFLOPS, 4)})
+    else:  # FFMA on the CUDA cores (no FP32 tensor-core GEMM that keeps fp32 rounding)
+        out.update({"fp32_peak_tflops": FP32_PEAK_TFLOPS, "fp32_peak_source": FP32_PEAK_SOURCE,
+                    "frac_of_fp32_peak": round(tf / FP32_PEAK_TFLOPS, 4)})
+    out.update({
            "lu_solve": {"ms": round(sms, 4), "GBps": round(sbytes / (sms / 1e3) / 1e9, 1),
                         "frac_of_hbm_peak": round(sbytes / (sms / 1e3) / 1e9 / hbm_peak, 4),
-                        "algorithmic_bytes": sbytes, "max_abs_err_vs_x_true": err}}
+                        "algorithmic_bytes": sbytes, "max_abs_err_vs_x_true": err}})
     del f
     if lu_fit is not None:
         import scipy.linalg
@@ -702,7 +715,7 @@ def bench_lu(args, torch, stream, be, n, lu_fit, hbm_peak):
                                "points": lu_fit["points"],
                                "lapack_comparator": {"value": round(flops / tl / 1e9, 1), "unit": "GFLOP/s",
                                                      "s": round(tl, 2),
-                                                     "what": "scipy.linalg.lu_factor (LAPACK dgetrf, OpenBLAS) at "
+                                                     "what": f"scipy.linalg.lu_factor (LAPACK {'d' if prec == 'f64' else 's'}getrf, OpenBLAS) at "
                                                              "full n on the same bytes; NOT the reference"}}
     torch.cuda.empty_cache()
     return out
