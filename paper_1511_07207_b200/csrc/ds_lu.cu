@@ -1805,9 +1805,11 @@ __global__ void __launch_bounds__(kTrsvThreads)
     // kTrsvDepth blocks in flight per CTA: block sidx lives in slot sidx % kTrsvDepth, its
     // matrix values and LL words issued kTrsvDepth blocks ahead (static slot indices: the
     // loop is unrolled by the depth)
-    double mv[kTrsvDepth][2 * CPW];
+    // kept in T until the FMA: a conversion right after the load would wait for it and
+    // serialise the prefetch (fp32)
+    T mv[kTrsvDepth][2 * CPW];
     uint64_t xw0[kTrsvDepth][2], xw1[kTrsvDepth][2];
-    auto issue = [&](int64_t sidx, double (&m)[2 * CPW], uint64_t (&w0)[2], uint64_t (&w1)[2]) {
+    auto issue = [&](int64_t sidx, T (&m)[2 * CPW], uint64_t (&w0)[2], uint64_t (&w1)[2]) {
       const int64_t c0 = block_col0(sidx);
       const int nc = (int)min((int64_t)kTrsvNB, n - c0);
       if (!TRANS) {
@@ -1815,8 +1817,8 @@ __global__ void __launch_bounds__(kTrsvThreads)
         for (int j = 0; j < CPW; ++j) {
           const int c = warp + NW * j;
           const T* col = M + (c0 + c) * ld + r0;
-          m[2 * j] = (c < nc && ra < nr) ? (double)col[ra] : 0.0;
-          m[2 * j + 1] = (c < nc && rb < nr) ? (double)col[rb] : 0.0;
+          m[2 * j] = (c < nc && ra < nr) ? col[ra] : T(0);
+          m[2 * j + 1] = (c < nc && rb < nr) ? col[rb] : T(0);
         }
         const int c = warp + NW * (lane & (CPW - 1));
         const uint64_t* p = ll + 2 * (c0 + min(c, nc - 1));
@@ -1829,7 +1831,7 @@ __global__ void __launch_bounds__(kTrsvThreads)
 #pragma unroll
           for (int j = 0; j < CPW; ++j) {
             const int r = warp + NW * j;
-            m[h * CPW + j] = (c < nc && r < nr) ? (double)M[(c0 + c) + (r0 + r) * ld] : 0.0;
+            m[h * CPW + j] = (c < nc && r < nr) ? M[(c0 + c) + (r0 + r) * ld] : T(0);
           }
           const uint64_t* p = ll + 2 * (c0 + min(c, nc - 1));
           asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(w0[h]) : "l"(p) : "memory");
@@ -1861,7 +1863,7 @@ __global__ void __launch_bounds__(kTrsvThreads)
       for (int d = 0; d < kTrsvDepth; ++d) {
         const int64_t sidx = s0 + d;
         if (sidx < nfold) {
-          double cur[2 * CPW];
+          T cur[2 * CPW];
 #pragma unroll
           for (int j = 0; j < 2 * CPW; ++j) cur[j] = mv[d][j];
           uint64_t cw0[2] = {xw0[d][0], xw0[d][1]}, cw1[2] = {xw1[d][0], xw1[d][1]};
@@ -1871,15 +1873,15 @@ __global__ void __launch_bounds__(kTrsvThreads)
 #pragma unroll
             for (int j = 0; j < CPW; ++j) {
               const double xv = __shfl_sync(0xffffffffu, xmine, j);
-              a0 = fma(cur[2 * j], xv, a0);
-              a1 = fma(cur[2 * j + 1], xv, a1);
+              a0 = fma((double)cur[2 * j], xv, a0);
+              a1 = fma((double)cur[2 * j + 1], xv, a1);
             }
           } else {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const double xv = validate(sidx, h, cw0, cw1);
 #pragma unroll
-              for (int j = 0; j < CPW; ++j) at[j] = fma(cur[h * CPW + j], xv, at[j]);
+              for (int j = 0; j < CPW; ++j) at[j] = fma((double)cur[h * CPW + j], xv, at[j]);
             }
           }
         }
