@@ -1863,11 +1863,11 @@ __global__ void __launch_bounds__(kTrsvThreads)
       for (int d = 0; d < kTrsvDepth; ++d) {
         const int64_t sidx = s0 + d;
         if (sidx < nfold) {
-          T cur[2 * CPW];
-#pragma unroll
-          for (int j = 0; j < 2 * CPW; ++j) cur[j] = mv[d][j];
-          uint64_t cw0[2] = {xw0[d][0], xw0[d][1]}, cw1[2] = {xw1[d][0], xw1[d][1]};
-          if (sidx + kTrsvDepth < nfold) issue(sidx + kTrsvDepth, mv[d], xw0[d], xw1[d]);  // refill the slot
+          // the slot is consumed in place and refilled after its FMAs (a copy out of the slot
+          // before the refill waited on the slot's loads)
+          T (&cur)[2 * CPW] = mv[d];
+          uint64_t (&cw0)[2] = xw0[d];
+          uint64_t (&cw1)[2] = xw1[d];
           if (!TRANS) {
             const double xmine = validate(sidx, 0, cw0, cw1);
 #pragma unroll
@@ -1884,6 +1884,7 @@ __global__ void __launch_bounds__(kTrsvThreads)
               for (int j = 0; j < CPW; ++j) at[j] = fma((double)cur[h * CPW + j], xv, at[j]);
             }
           }
+          if (sidx + kTrsvDepth < nfold) issue(sidx + kTrsvDepth, mv[d], xw0[d], xw1[d]);  // refill the slot
         }
       }
     }
