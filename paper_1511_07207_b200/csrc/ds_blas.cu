@@ -1923,6 +1923,115 @@ int trsm_lower_unit_launch(ds_ctx* ctx, int64_t b, int64_t m, const T* L, int64_
   DS_CHECK_LAUNCH();
   return DS_OK;
 }
+// U01 of an outer panel, one CTA per 32 columns (the thread <-> column mapping of
+// trsm_lower_unit_cols64: 8 threads per column, 8 rows each).  Per 64-row block ib:
+//   (a) z = L_ib^-1 (rows of the block): the same shuffle substitution, same order;
+//   (b) rows below the block inside the outer panel -= L[below, ib] z: per element the
+//       accumulator starts from the stored value and takes the 16 k-steps of 4 of
+//       mma.m8n8k4 with the negated L operand, in k order: the K = 64 chain of
+//       gemm64(_tma)_kernel<1>, hence bitwise its result.
+// Shared memory: the block's strict lower triangle (column-major) and the solved z strip.
+__global__ void __launch_bounds__(256, 1)
+    u01_fused_kernel(double* __restrict__ W, int64_t ld, int64_t kb, int nblk, int64_t c0, int64_t c1) {
+  extern __shared__ __align__(16) double u01_smem[];
+  double (*Ls)[64] = reinterpret_cast<double (*)[64]>(u01_smem);           // Ls[j][i] = L[i, j], i > j
+  double (*Zs)[33] = reinterpret_cast<double (*)[33]>(u01_smem + 64 * 64);  // Zs[k][col]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, sub = lane & 7, gbase = lane & ~7;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t cs = c0 + (int64_t)blockIdx.x * 32;  // first column of the strip
+  const int cl = tid >> 3;                            // trsm: my column in the strip
+  const bool act = cs + cl < c1;
+  const int64_t rend = kb + (int64_t)nblk * 64;
+  for (int ib = 0; ib < nblk; ++ib) {
+    const int64_t r0 = kb + (int64_t)ib * 64;
+    __syncthreads();  // the previous block's update is done with Zs / Ls
+    {
+      double v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int e = tid + u * 256, i = e & 63, j = e >> 6;
+        v[u] = i > j ? W[(r0 + i) + (r0 + j) * ld] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int e = tid + u * 256;
+        Ls[e >> 6][e & 63] = v[u];
+      }
+    }
+    __syncthreads();
+    double z[8];
+    double* bb = W + (act ? cs + cl : c0) * ld + r0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) z[k] = act ? bb[sub + 8 * k] : 0.0;
+#pragma unroll
+    for (int j = 0; j < 63; ++j) {
+      const double zj = __shfl_sync(0xffffffffu, z[j >> 3], gbase + (j & 7));
+#pragma unroll
+      for (int k = j >> 3; k < 8; ++k) {
+        const int i = sub + 8 * k;
+        if (i > j) z[k] = fma(-Ls[j][i], zj, z[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      Zs[sub + 8 * k][cl] = act ? z[k] : 0.0;
+      if (act) bb[sub + 8 * k] = z[k];
+    }
+    __syncthreads();
+    // (b) rows [r0 + 64, rend) x the strip, 32-row tiles over the 8 warps
+    const int64_t rb = r0 + 64;
+    const int ntile = (int)((rend - rb) / 32);
+    for (int tl = warp; tl < ntile; tl += 8) {
+      const int64_t m0 = rb + (int64_t)tl * 32;
+      double acc[4][4][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int64_t c = cs + j * 8 + 2 * t + e;
+            acc[i][j][e] = c < c1 ? W[(m0 + i * 8 + g) + c * ld] : 0.0;
+          }
+#pragma unroll 4
+      for (int q = 0; q < 16; ++q) {
+        double a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = -W[(m0 + i * 8 + g) + (r0 + 4 * q + t) * ld];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Zs[4 * q + t][j * 8 + g];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int64_t c = cs + j * 8 + 2 * t + e;
+            if (c < c1) W[(m0 + i * 8 + g) + c * ld] = acc[i][j][e];
+          }
+    }
+  }
+}
+
+int u01_fused_launch(ds_ctx* ctx, double* W, int64_t ld, int64_t kb, int nblk, int64_t c0, int64_t c1) {
+  if (c1 <= c0 || nblk <= 0) return DS_OK;
+  constexpr int smem = (64 * 64 + 64 * 33) * (int)sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    DS_CUDA(cudaFuncSetAttribute(u01_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  u01_fused_kernel<<<(unsigned)ceil_div(c1 - c0, (int64_t)32), 256, smem, ctx->stream>>>(W, ld, kb, nblk, c0, c1);
+  count_launch(ctx);
+  DS_CHECK_LAUNCH();
+  return DS_OK;
+}
+
 template <typename T>
 int trsm_upper_launch(ds_ctx* ctx, int64_t b, int64_t m, const T* U, int64_t ldu, const T* B,
                       int64_t ldb, T* Z, int64_t ldz) {

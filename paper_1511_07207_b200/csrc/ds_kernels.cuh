@@ -117,6 +117,11 @@ int trsm_lower_unit_launch(ds_ctx* ctx, int64_t b, int64_t m, const T* L, int64_
 template <typename T>
 int trsm_upper_launch(ds_ctx* ctx, int64_t b, int64_t m, const T* U, int64_t ldu, const T* B,
                       int64_t ldb, T* Z, int64_t ldz);
+// U01 of an outer LU panel in one launch (fp64, b = 64): for the columns [c0, c1) of W and
+// the nblk 64-row blocks starting at row kb, block by block: the unit-lower TRSM of the
+// block's rows, then the update of the outer panel's rows below it (the K = 64 DMMA chain of
+// gemm64 from C).  Bitwise equal to the trsm_lower_unit_cols64 / gemm launch chain.
+int u01_fused_launch(ds_ctx* ctx, double* W, int64_t ld, int64_t kb, int nblk, int64_t c0, int64_t c1);
 template <typename T>
 int ger_launch(ds_ctx* ctx, int64_t m, int64_t n, const T* A, int64_t lda, double alpha,
                const T* x, const T* y, T* out, int64_t ldo);

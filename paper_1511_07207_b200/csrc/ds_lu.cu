@@ -1447,8 +1447,17 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
     return DS_OK;
   };
   // U01 = L00^-1 A01 and A11 -= L10 U01 for trailing columns [c0, c1)
-  auto outer_update = [&](int64_t kb, int64_t bf, int64_t c0, int64_t c1, int reserve) -> int {
+  // U01 of the outer panel in one launch (fp64, b = 64, whole 64-row blocks); bitwise the
+  // TRSM / GEMM chain below.  DENSOLVE_LU_U01_FUSED=0 keeps the chain.
+  static const bool u01_fused = [] {
+    const char* e = getenv("DENSOLVE_LU_U01_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  auto outer_update = [&](int64_t kb, int64_t bf, int64_t c0, int64_t c1, int reserve, bool fuse = false) -> int {
     if (c1 <= c0) return DS_OK;
+    if (fuse && sizeof(T) == 8 && u01_fused && b == 64 && (bf - kb) % 64 == 0) {
+      DS_TRY(u01_fused_launch(ctx, reinterpret_cast<double*>(W), ld, kb, (int)((bf - kb) / 64), c0, c1));
+    } else
     for (int64_t ib = kb; ib < bf; ib += b) {
       const int64_t ibf = std::min<int64_t>(ib + b, bf);
       T* Ur = W + ib + c0 * ld;
@@ -1534,7 +1543,7 @@ int lu_factor_impl(ds_ctx* ctx, int64_t m, int64_t w, T* W, int64_t ld, int64_t 
     // the look-ahead columns [bf, bf2) get their swaps and update first: that is the
     // only work between this panel and the next panel's factorization
     DS_TRY(laswp_apply<T>(ctx, W, ld, bf, bf2, op));
-    DS_TRY(outer_update(kb, bf, bf, bf2, 0));
+    DS_TRY(outer_update(kb, bf, bf, bf2, 0, true));  // the look-ahead columns: on the panel chain
     if (lookahead) {
       DS_CUDA(cudaEventRecord(ctx->ev_a, ctx->stream));
       DS_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_a, 0));

@@ -59,6 +59,15 @@ def test_sm_reservation_is_bitwise_neutral():
     assert len(on) == len(cases) and on == off
 
 
+def test_u01_fused_is_bitwise_neutral():
+    # the outer panel's U01 (TRSM of each 64-row block + the K = 64 update of the rows below)
+    # in one launch (ds_blas.cu u01_fused_kernel) vs the TRSM / GEMM launch chain
+    cases = [(3000, 64, 10, "float64"), (8192, 64, 11, "float64"), (2048, 64, 12, "float32")]
+    on = _run(0, cases)
+    off = _run(0, cases, DENSOLVE_LU_U01_FUSED="0")
+    assert len(on) == len(cases) and on == off
+
+
 def test_poller_kernel_factorization_is_valid():
     # the hashes above prove agreement; this checks the shared result is a valid
     # partial-pivoting factorization (in-process, default kernel choice)
